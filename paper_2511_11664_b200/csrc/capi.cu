@@ -1,0 +1,1413 @@
+// capi.cu -- host orchestration and the extern "C" boundary of libsczip_b200.
+//
+// Single translation unit: includes the kernel files so launch code sees the
+// parameter structs.  One context = one CUDA stream + grow-only scratch; no
+// global mutable state (SPEC.md:85-86 reentrancy).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "encode.cu"
+#include "select.cu"
+#include "rans.cu"
+#include "decode.cu"
+
+using namespace scz;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n + n / 8, 4096);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    template <typename T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n + n / 8, 4096);
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    template <typename T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// optimizer.py:51-75 (divisors, candidate_bounds, candidate_rows)
+std::vector<uint64_t> candidate_rows(uint64_t total, int q_bits) {
+    std::vector<uint64_t> small, large;
+    for (uint64_t d = 1; d * d <= total; ++d)
+        if (total % d == 0) {
+            small.push_back(d);
+            if (d != total / d) large.push_back(total / d);
+        }
+    std::vector<uint64_t> divs(small);
+    divs.insert(divs.end(), large.rbegin(), large.rend());
+    uint64_t isq = 0;
+    while ((isq + 1) * (isq + 1) <= total) ++isq;
+    uint64_t qk = 1ull << q_bits;
+    uint64_t n_min = std::max(isq + 1, (total + qk - 1) / qk);
+    std::vector<uint64_t> out;
+    for (auto it = divs.rbegin(); it != divs.rend(); ++it)
+        if (*it >= n_min && *it <= total) out.push_back(*it);
+    return out;
+}
+
+uint64_t gcd64(uint64_t a, uint64_t b) {
+    while (b) {
+        uint64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+int width_for(uint64_t maxsym) { return maxsym <= 255 ? 1 : (maxsym <= 65535 ? 2 : 4); }
+
+}  // namespace
+
+struct scz_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    int num_sms = 148;
+    // encode scratch
+    DevBuf x_in, bitmap, tile_stats, tile_off, state, vhist, v8, cr, hp, rhist, counts, terms,
+        freqs, cum, enctab, slots, block_len, blk_off, cand_out, info, payload, ticket, dsym_in;
+    // decode scratch
+    DevBuf dinfo, dfreqs, dblocks, dpayload, cumtab, dblk_off, dsym, chunk_sum, dstatus, out_off, dout;
+    // host staging
+    HostBuf h_info, h_payload, h_freqs, h_blocks, h_status, h_misc;
+    int32_t* h_status_async = nullptr;
+    uint32_t last_batch = 0;
+    HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
+
+    // Optional per-kernel timing with CUDA events on this stream: kernel i
+    // spans [end event of the previous launch (or the API-entry mark), its
+    // own end event].  Used by bench.py for the live roofline.
+    struct Span {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    bool timing = false;
+    cudaEvent_t last_ev = nullptr;
+    std::vector<Span> spans;
+    std::vector<cudaEvent_t> ev_pool, ev_used;
+    std::vector<std::pair<std::string, std::pair<double, uint64_t>>> acc;
+    cudaEvent_t take_event() {
+        cudaEvent_t e = nullptr;
+        if (!ev_pool.empty()) {
+            e = ev_pool.back();
+            ev_pool.pop_back();
+        } else {
+            cudaEventCreate(&e);
+        }
+        ev_used.push_back(e);
+        return e;
+    }
+    void mark() {
+        if (!timing) return;
+        last_ev = take_event();
+        cudaEventRecord(last_ev, stream);
+    }
+    void collect() {
+        if (spans.empty() && ev_used.empty()) return;
+        cudaStreamSynchronize(stream);
+        for (const Span& s : spans) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, s.a, s.b);
+            bool found = false;
+            for (auto& kv : acc)
+                if (kv.first == s.name) {
+                    kv.second.first += ms;
+                    kv.second.second += 1;
+                    found = true;
+                    break;
+                }
+            if (!found) acc.push_back({s.name, {ms, 1}});
+        }
+        spans.clear();
+        ev_pool.insert(ev_pool.end(), ev_used.begin(), ev_used.end());
+        ev_used.clear();
+        last_ev = nullptr;
+    }
+
+    int fail(int code, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return code;
+    }
+    int cuda(cudaError_t e, const char* where) {
+        if (e == cudaSuccess) return SCZ_OK;
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? SCZ_OUT_OF_MEMORY : SCZ_CUDA_ERROR, "%s: %s",
+                    where, cudaGetErrorString(e));
+    }
+    int launched(const char* name) {
+        ++launches;
+        int st = cuda(cudaGetLastError(), name);
+        if (st == SCZ_OK && timing && last_ev) {
+            cudaEvent_t e = take_event();
+            cudaEventRecord(e, stream);
+            spans.push_back({name, last_ev, e});
+            last_ev = e;
+        }
+        return st;
+    }
+};
+
+#define CK(expr)                                         \
+    do {                                                 \
+        int _st = ctx->cuda((expr), #expr);              \
+        if (_st != SCZ_OK) return _st;                   \
+    } while (0)
+#define LAUNCHED(name)                                   \
+    do {                                                 \
+        int _st = ctx->launched(name);                   \
+        if (_st != SCZ_OK) return _st;                   \
+    } while (0)
+
+namespace {
+
+// Everything the encode kernels need for one batch geometry.
+struct EncPlan {
+    uint64_t T;
+    uint32_t B;
+    int q_bits, precision, format;
+    uint32_t lanes, block_syms;
+    bool searching;
+    std::vector<uint64_t> rows;  // candidate N, descending
+    uint32_t n_tiles, words_pad;
+    uint32_t acap;
+    uint64_t L_max;
+    uint32_t nblk_cap;
+    uint64_t slot_cap;
+    uint64_t period;  // P
+    uint32_t widths;  // bitmask of c/r symbol widths present among candidates
+    uint64_t payload_cap;  // packed payload bytes per tensor (upper bound)
+};
+
+int plan_encode(scz_ctx* ctx, uint64_t T, uint32_t B, int q_bits, int64_t n_rows, int precision,
+                int format, uint32_t lanes, uint32_t block_syms, EncPlan* pl,
+                const std::vector<uint64_t>* explicit_rows = nullptr) {
+    // container.py:80-84 precision check first, then compute_params' q check
+    if (precision < 8 || precision > 15)
+        return ctx->fail(SCZ_INVALID_INPUT, "container precision must be in [8, 15]");
+    if (q_bits < 2 || q_bits > 8) return ctx->fail(SCZ_INVALID_INPUT, "q_bits must be in [2, 8]");
+    if (T < 1) return ctx->fail(SCZ_INVALID_INPUT, "empty tensor");
+    if (T >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "tensors of >= 2^31 elements");
+    if (B < 1) return ctx->fail(SCZ_INVALID_INPUT, "batch must be >= 1");
+    if (n_rows >= 0 && (n_rows < 1 || T % (uint64_t)n_rows != 0))
+        return ctx->fail(SCZ_NON_DIVISIBLE, "%lld does not divide element count %llu",
+                         (long long)n_rows, (unsigned long long)T);
+    if (format != 1 && format != 2) return ctx->fail(SCZ_INVALID_INPUT, "format must be 1 or 2");
+    if (format == 2) {
+        if (lanes != 32) return ctx->fail(SCZ_UNSUPPORTED, "v2 encoder supports 32 lanes");
+        if (block_syms < 32 || block_syms % 32)
+            return ctx->fail(SCZ_INVALID_INPUT, "block_syms must be a positive multiple of 32");
+    }
+    pl->T = T;
+    pl->B = B;
+    pl->q_bits = q_bits;
+    pl->precision = precision;
+    pl->format = format;
+    pl->lanes = format == 2 ? lanes : 1;
+    pl->block_syms = block_syms;
+    pl->searching = n_rows < 0;
+    if (explicit_rows) {  // optimizer.cost over caller-chosen reshapes (all priced)
+        for (uint64_t n : *explicit_rows)
+            if (n < 1 || T % n) return ctx->fail(SCZ_NON_DIVISIBLE, "%llu does not divide element count %llu",
+                                                 (unsigned long long)n, (unsigned long long)T);
+        pl->rows = *explicit_rows;
+        pl->searching = true;
+    } else if (pl->searching) {
+        pl->rows = candidate_rows(T, q_bits);
+        if (pl->rows.empty()) pl->rows.push_back(T);  // optimizer.py:124-125
+    } else {
+        pl->rows = {(uint64_t)n_rows};
+    }
+    if (pl->rows.empty()) return ctx->fail(SCZ_INVALID_INPUT, "no reshape candidates");
+    if (pl->rows.size() > (size_t)MAX_CAND)
+        return ctx->fail(SCZ_UNSUPPORTED, "%zu reshape candidates (max %d)", pl->rows.size(), MAX_CAND);
+    pl->n_tiles = ceil_div_u32(T, TILE);
+    pl->words_pad = pl->n_tiles * TILE_WORDS;
+    uint64_t kmax = 0, lcm = 1;
+    uint64_t nmax = 0;
+    pl->widths = 0;
+    for (uint64_t n : pl->rows) {
+        uint64_t k = T / n;
+        kmax = std::max(kmax, k);
+        nmax = std::max(nmax, n);
+        pl->widths |= (uint32_t)width_for(k);
+        if (lcm <= (1ull << 40)) lcm = lcm / gcd64(lcm, k) * k;
+    }
+    uint64_t P = lcm / gcd64(lcm, 32) * 32;
+    if (P > (1ull << 28)) return ctx->fail(SCZ_UNSUPPORTED, "column-histogram period too large");
+    pl->period = P;
+    pl->acap = (uint32_t)std::max<uint64_t>(1ull << q_bits, kmax + 1);
+    pl->L_max = 2 * T + nmax;
+    if (format == 2) {
+        pl->nblk_cap = ceil_div_u32(pl->L_max, block_syms);
+        pl->slot_cap = 4ull * 32 + 2ull * block_syms;
+    } else {
+        pl->nblk_cap = 1;
+        pl->slot_cap = 4 + 2 * pl->L_max;
+    }
+    pl->slot_cap = (pl->slot_cap + 15) & ~15ull;
+    pl->payload_cap = (uint64_t)pl->nblk_cap * pl->slot_cap;
+    return SCZ_OK;
+}
+
+struct EncOut {
+    double* cand_out = nullptr;  // device, optional
+};
+
+__global__ void k_finalize(TensorState* state, uint32_t B, uint64_t total, int q_bits, int precision,
+                           int format, uint32_t block_syms, const uint32_t* block_len,
+                           uint32_t slots_per_tensor, uint32_t* blk_off, uint32_t acap,
+                           scz_info* info, uint32_t* ticket) {
+    const uint32_t b = blockIdx.x;
+    TensorState& st = state[b];
+    __shared__ uint32_t s_scan[33];
+    __shared__ uint32_t s_last;
+    uint32_t nb = 0;
+    unsigned long long plen = 0;
+    if (st.status == SCZ_OK) {
+        if (st.errbits & 1u) st.status = SCZ_ALPHABET_OVERFLOW;
+        else if (st.errbits & 2u) st.status = SCZ_UNCODABLE_SYMBOL;
+    }
+    __syncthreads();
+    if (st.status == SCZ_OK) {
+        nb = format == 2 ? ceil_div_u32(st.stream_len, block_syms) : 1;
+        const uint32_t* bl = block_len + (uint64_t)b * slots_per_tensor;
+        uint32_t* bo = blk_off + (uint64_t)b * slots_per_tensor;
+        for (uint32_t base = 0; base < nb; base += 256) {
+            uint32_t i = base + threadIdx.x;
+            uint32_t v = i < nb ? bl[i] : 0;
+            uint32_t tot;
+            uint32_t ex = block_exclusive_scan<256>(v, s_scan, &tot);
+            if (i < nb) bo[i] = (uint32_t)(plen + ex);
+            plen += tot;
+        }
+    }
+    if (threadIdx.x == 0) {
+        scz_info& in = info[b];
+        in.status = st.status;
+        in.version = (uint8_t)format;
+        in.q_bits = (uint8_t)q_bits;
+        in.precision = (uint8_t)precision;
+        in.sym_bytes = (uint8_t)st.sym_bytes;
+        in.total = total;
+        in.n_rows = st.n_rows;
+        in.n_cols = st.n_cols;
+        in.nnz = st.nnz;
+        in.scale = st.scale;
+        in.zero_point = st.zero_point;
+        in.alphabet = st.alphabet;
+        in.lanes = format == 2 ? 32 : 1;
+        in.block_syms = format == 2 ? block_syms : (uint32_t)st.stream_len;
+        in.n_blocks = nb;
+        in.payload_len = plen;
+        in.freqs_off = (uint64_t)b * acap;
+        in.blocks_off = (uint64_t)b * slots_per_tensor;
+        in.search_flags = st.search_flags;
+        in.n_evaluated = st.n_evaluated;
+        __threadfence();
+        s_last = (atomicAdd(ticket, 1u) == B - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // last CTA: pack offsets of every tensor's payload
+    unsigned long long carry = 0;
+    for (uint32_t base = 0; base < B; base += 256) {
+        uint32_t i = base + threadIdx.x;
+        uint32_t v = 0;
+        if (i < B) v = (uint32_t)(*(volatile unsigned long long*)&info[i].payload_len);
+        uint32_t tot;
+        uint32_t ex = block_exclusive_scan<256>(v, s_scan, &tot);
+        if (i < B) info[i].payload_off = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) *ticket = 0;
+}
+
+__global__ void __launch_bounds__(256) k_pack(const scz_info* info, const uint8_t* slots, uint64_t slot_cap,
+                                              uint32_t slots_per_tensor, const uint32_t* block_len,
+                                              const uint32_t* blk_off, uint8_t* payload) {
+    const uint32_t b = blockIdx.y, blk = blockIdx.x;
+    const scz_info& in = info[b];
+    if (in.status != SCZ_OK || blk >= in.n_blocks) return;
+    const uint64_t sidx = (uint64_t)b * slots_per_tensor + blk;
+    const uint32_t len = block_len[sidx];
+    const uint8_t* src = slots + sidx * slot_cap + slot_cap - len;
+    uint8_t* dst = payload + in.payload_off + blk_off[sidx];
+    for (uint32_t i = threadIdx.x; i < len; i += 256) dst[i] = src[i];
+}
+
+// The encode pipeline over a device batch.  cand_out (device) optional.
+int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_out,
+               uint32_t* dump = nullptr) {
+    const uint32_t B = pl.B;
+    const uint64_t T = pl.T;
+    cudaStream_t s = ctx->stream;
+    const uint32_t ncand = (uint32_t)pl.rows.size();
+    // rhist layout: candidate c at offset sum_{c'<c} (K_c' + 1)
+    std::vector<uint32_t> rh_off(ncand);
+    uint64_t rh_total = 0;
+    for (uint32_t c = 0; c < ncand; ++c) {
+        rh_off[c] = (uint32_t)rh_total;
+        rh_total += T / pl.rows[c] + 1;
+    }
+    if (rh_total >= (1ull << 32)) return ctx->fail(SCZ_UNSUPPORTED, "row histogram too large");
+    CK(ctx->bitmap.ensure((size_t)B * pl.words_pad * 4));
+    CK(ctx->tile_stats.ensure((size_t)B * pl.n_tiles * sizeof(float4)));
+    CK(ctx->tile_off.ensure((size_t)B * pl.n_tiles * 4));
+    CK(ctx->state.ensure((size_t)B * sizeof(TensorState)));
+    CK(ctx->vhist.ensure((size_t)B * 256 * 4));
+    CK(ctx->v8.ensure((size_t)B * T));
+    int maxw = (pl.widths & 4) ? 4 : ((pl.widths & 2) ? 2 : 1);
+    CK(ctx->cr.ensure((size_t)B * 2 * T * maxw));
+    CK(ctx->hp.ensure((size_t)B * pl.period * 4));
+    CK(ctx->rhist.ensure((size_t)B * rh_total * 4));
+    CK(ctx->counts.ensure((size_t)B * pl.acap * 4));
+    CK(ctx->terms.ensure((size_t)B * pl.acap * 8));
+    CK(ctx->freqs.ensure((size_t)B * pl.acap * 4));
+    CK(ctx->cum.ensure((size_t)B * (pl.acap + 1) * 4));
+    CK(ctx->enctab.ensure((size_t)B * pl.acap * sizeof(EncTab)));
+    CK(ctx->slots.ensure((size_t)B * pl.nblk_cap * pl.slot_cap));
+    CK(ctx->block_len.ensure((size_t)B * pl.nblk_cap * 4));
+    CK(ctx->blk_off.ensure((size_t)B * pl.nblk_cap * 4));
+    CK(ctx->info.ensure((size_t)B * sizeof(scz_info)));
+    CK(ctx->payload.ensure((size_t)B * pl.payload_cap + 256));
+    CK(ctx->ticket.ensure(64));
+    CK(cudaMemsetAsync(ctx->state.p, 0, (size_t)B * sizeof(TensorState), s));
+    CK(cudaMemsetAsync(ctx->vhist.p, 0, (size_t)B * 256 * 4, s));
+    CK(cudaMemsetAsync(ctx->ticket.p, 0, 64, s));
+    bool need_hist = false;
+    for (uint64_t n : pl.rows) need_hist |= (T / n) > 1;
+    if (need_hist) {
+        CK(cudaMemsetAsync(ctx->hp.p, 0, (size_t)B * pl.period * 4, s));
+        CK(cudaMemsetAsync(ctx->rhist.p, 0, (size_t)B * rh_total * 4, s));
+    }
+
+    StatsParams sp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
+                   ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>()};
+    k_stats<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(sp);
+    LAUNCHED("k_stats");
+    QuantParams qp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
+                   ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
+                   ctx->vhist.as<uint32_t>(), nullptr};
+    k_quantize<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(qp);
+    LAUNCHED("k_quantize");
+
+    if (need_hist) {
+        ColHistParams cp;
+        cp.bitmap = ctx->bitmap.as<uint32_t>();
+        cp.words_pad = pl.words_pad;
+        cp.n_words = ceil_div_u32(T, 32);
+        cp.period_words = (uint32_t)(pl.period / 32);
+        cp.n_rows = ceil_div_u32(cp.n_words, cp.period_words);
+        cp.rows_per_cta = 64;
+        cp.hp = ctx->hp.as<uint32_t>();
+        cp.hp_stride = (uint32_t)pl.period;
+        dim3 g(ceil_div_u32(cp.period_words, 128), ceil_div_u32(cp.n_rows, cp.rows_per_cta), B);
+        k_colhist<<<g, 128, 0, s>>>(cp);
+        LAUNCHED("k_colhist");
+
+        RowHistParams rp;
+        memset(&rp, 0, sizeof rp);
+        rp.bitmap = ctx->bitmap.as<uint32_t>();
+        rp.words_pad = pl.words_pad;
+        rp.n_cand = ncand;
+        rp.rows_per_chunk = 8192;
+        uint32_t chunks = 0, maxbins = 0;
+        for (uint32_t c = 0; c < ncand; ++c) {
+            uint32_t K = (uint32_t)(T / pl.rows[c]);
+            rp.cand_k[c] = K;
+            rp.cand_rows[c] = (uint32_t)pl.rows[c];
+            rp.rhist_off[c] = rh_off[c];
+            rp.chunk_start[c] = chunks;
+            if (K > 1) chunks += ceil_div_u32(pl.rows[c], rp.rows_per_chunk);
+            if (K > 1) maxbins = std::max(maxbins, K + 1);
+        }
+        rp.chunk_start[ncand] = chunks;
+        rp.rhist = ctx->rhist.as<uint32_t>();
+        rp.rhist_stride = (uint32_t)rh_total;
+        if (chunks) {
+            size_t smem = std::min<uint32_t>(maxbins, 4096) * 4;
+            k_rowhist<<<dim3(chunks, B), 256, smem, s>>>(rp);
+            LAUNCHED("k_rowhist");
+        }
+    }
+
+    SelectParams sel;
+    memset(&sel, 0, sizeof sel);
+    sel.n_cand = ncand;
+    for (uint32_t c = 0; c < ncand; ++c) {
+        sel.cand_k[c] = (uint32_t)(T / pl.rows[c]);
+        sel.cand_n[c] = (uint32_t)pl.rows[c];
+        sel.rhist_off[c] = rh_off[c];
+    }
+    sel.period = (uint32_t)pl.period;
+    sel.hp = ctx->hp.as<uint32_t>();
+    sel.hp_stride = (uint32_t)pl.period;
+    sel.rhist = ctx->rhist.as<uint32_t>();
+    sel.rhist_stride = (uint32_t)rh_total;
+    sel.vhist = ctx->vhist.as<uint32_t>();
+    sel.q_bits = pl.q_bits;
+    sel.precision = pl.precision;
+    sel.searching = pl.searching ? 1 : 0;
+    sel.total = T;
+    sel.state = ctx->state.as<TensorState>();
+    sel.counts = ctx->counts.as<uint32_t>();
+    sel.terms = ctx->terms.as<double>();
+    sel.acap = pl.acap;
+    sel.freqs = ctx->freqs.as<uint32_t>();
+    sel.cum = ctx->cum.as<uint32_t>();
+    sel.enctab = ctx->enctab.as<EncTab>();
+    sel.cand_out = cand_out;
+    sel.dump = dump;
+    k_select<<<B, SEL_THREADS, 0, s>>>(sel);
+    LAUNCHED("k_select");
+
+    MatParams mp{T, pl.n_tiles, pl.words_pad, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(),
+                 ctx->state.as<TensorState>(), ctx->cr.p, 2 * T, 0};
+    EncParams ep{ctx->state.as<TensorState>(), ctx->enctab.as<EncTab>(), pl.acap, pl.precision,
+                 pl.block_syms, ctx->slots.as<uint8_t>(), pl.slot_cap, pl.nblk_cap,
+                 ctx->block_len.as<uint32_t>()};
+    const dim3 g_enc2(ceil_div_u32(pl.nblk_cap, ENC_WPB), B);
+    auto run_width = [&](auto tag) -> int {
+        using S = decltype(tag);
+        k_materialize<S><<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(mp);
+        LAUNCHED("k_materialize");
+        SplitSrc<S> src{ctx->v8.as<uint8_t>(), T, ctx->cr.as<S>(), 2 * T};
+        if (pl.format == 2) {
+            k_rans_enc_v2<SplitSrc<S>><<<g_enc2, ENC_WPB * 32, 0, s>>>(ep, src);
+            LAUNCHED("k_rans_enc_v2");
+        } else {
+            k_rans_enc_v1<SplitSrc<S>><<<B, 32, 0, s>>>(ep, src);
+            LAUNCHED("k_rans_enc_v1");
+        }
+        return SCZ_OK;
+    };
+    int st;
+    if (pl.widths & 1) { if ((st = run_width(uint8_t{})) != SCZ_OK) return st; }
+    if (pl.widths & 2) { if ((st = run_width(uint16_t{})) != SCZ_OK) return st; }
+    if (pl.widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
+
+    k_finalize<<<B, 256, 0, s>>>(ctx->state.as<TensorState>(), B, T, pl.q_bits, pl.precision, pl.format,
+                                 pl.block_syms, ctx->block_len.as<uint32_t>(), pl.nblk_cap,
+                                 ctx->blk_off.as<uint32_t>(), pl.acap, ctx->info.as<scz_info>(),
+                                 ctx->ticket.as<uint32_t>());
+    LAUNCHED("k_finalize");
+    k_pack<<<dim3(pl.nblk_cap, B), 256, 0, s>>>(ctx->info.as<scz_info>(), ctx->slots.as<uint8_t>(),
+                                                 pl.slot_cap, pl.nblk_cap, ctx->block_len.as<uint32_t>(),
+                                                 ctx->blk_off.as<uint32_t>(), ctx->payload.as<uint8_t>());
+    LAUNCHED("k_pack");
+    return SCZ_OK;
+}
+
+// ---------------------------------------------------------------- decode
+void dec_class(const scz_info& in, uint8_t* width) {
+    // symbol width + lookup flavour: 1 = u8 LUT, 2 = u16 LUT, 4 = binary search
+    if (in.precision <= 15 && in.alphabet <= 256) *width = 1;
+    else if (in.precision <= 15 && in.alphabet <= 65536) *width = 2;
+    else *width = 4;
+}
+
+// Host-side header checks in the order container.decompress applies them.
+int validate_header(scz_ctx* ctx, const scz_info& in) {
+    if (in.version != 1 && in.version != 2)
+        return ctx->fail(SCZ_UNSUPPORTED_VERSION, "container version %d unsupported", in.version);
+    if ((uint64_t)in.n_rows * in.n_cols != in.total)
+        return ctx->fail(SCZ_INVALID_CONTAINER, "N * K does not match the product of dims");
+    if (in.total >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "tensors of >= 2^31 elements");
+    if (in.alphabet < 1 || in.precision > 31)
+        return ctx->fail(SCZ_CORRUPT_STREAM, "frequencies do not sum to 2^precision");
+    const uint64_t L = 2 * in.nnz + in.n_rows;
+    if (in.nnz > in.total) return ctx->fail(SCZ_CORRUPT_STREAM, "nnz exceeds element count");
+    if (in.version == 2) {
+        if (in.lanes != 32)
+            return ctx->fail(SCZ_UNSUPPORTED, "v2 decoder supports 32 lanes (container has %u)", in.lanes);
+        if (in.precision > 16)
+            return ctx->fail(SCZ_UNSUPPORTED, "v2 decoder supports precision <= 16");
+        if (in.block_syms < in.lanes || in.block_syms % in.lanes ||
+            in.n_blocks != ceil_div_u32(L, in.block_syms))
+            return ctx->fail(SCZ_CORRUPT_STREAM, "v2 block geometry inconsistent");
+    }
+    if (in.payload_len < 4) return ctx->fail(SCZ_CORRUPT_STREAM, "bitstream shorter than the 4 state bytes");
+    return SCZ_OK;
+}
+
+int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t* d_freqs,
+               const uint32_t* d_blocks, const uint8_t* d_payload, float* d_out, bool stage,
+               uint32_t* q_out, uint8_t* mask_out) {
+    cudaStream_t s = ctx->stream;
+    CK(ctx->h_misc.ensure((size_t)B * (sizeof(scz_info) + 8 + 4)));
+    scz_info* hi = ctx->h_misc.as<scz_info>();
+    uint64_t* hoff = reinterpret_cast<uint64_t*>(hi + B);
+    int32_t* hst = reinterpret_cast<int32_t*>(hoff + B);
+    uint32_t acap = 1, nblk_cap = 1, nchunk_cap = 1, widths = 0;
+    uint64_t Lmax = 1, off = 0, maxA = 1;
+    int maxn = 1;
+    for (uint32_t b = 0; b < B; ++b) {
+        hi[b] = h_info[b];
+        hst[b] = SCZ_OK;
+        dec_class(hi[b], &hi[b].sym_bytes);
+        widths |= hi[b].sym_bytes;
+        acap = std::max(acap, hi[b].alphabet);
+        maxA = std::max<uint64_t>(maxA, hi[b].alphabet);
+        nblk_cap = std::max(nblk_cap, hi[b].version == 2 ? hi[b].n_blocks : 1u);
+        Lmax = std::max<uint64_t>(Lmax, 2 * hi[b].nnz + hi[b].n_rows);
+        nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, ROW_CHUNK));
+        maxn = std::max(maxn, (int)hi[b].precision);
+        hoff[b] = off;
+        off += hi[b].total;
+    }
+    CK(ctx->dinfo.ensure((size_t)B * sizeof(scz_info)));
+    CK(ctx->out_off.ensure((size_t)B * 8));
+    CK(ctx->dstatus.ensure((size_t)B * 4));
+    CK(ctx->cumtab.ensure((size_t)B * (acap + 1) * 4));
+    CK(ctx->dblk_off.ensure((size_t)B * nblk_cap * 4));
+    CK(ctx->dsym.ensure((size_t)B * Lmax * 4));
+    CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 4));
+    CK(cudaMemcpyAsync(ctx->dinfo.p, hi, (size_t)B * sizeof(scz_info), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->out_off.p, hoff, (size_t)B * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->dstatus.p, hst, (size_t)B * 4, cudaMemcpyHostToDevice, s));
+    DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
+                 ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
+                 ctx->dstatus.as<int32_t>()};
+    k_dec_prepare<<<B, 256, 0, s>>>(dp);
+    LAUNCHED("k_dec_prepare");
+    bool any_v1 = false, any_v2 = false;
+    for (uint32_t b = 0; b < B; ++b) (hi[b].version == 2 ? any_v2 : any_v1) = true;
+    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<uint32_t>(), nchunk_cap,
+                 ctx->dstatus.as<int32_t>(), d_out, ctx->out_off.as<uint64_t>(), q_out, mask_out};
+    auto run_width = [&](auto tag) -> int {
+        using S = decltype(tag);
+        using L = S;
+        const size_t tab = maxA <= TAB_SMEM_MAX ? maxA * sizeof(uint2) : 0;
+        const size_t lut = sizeof(L) < 4 ? ((size_t)1 << maxn) * sizeof(L) : 0;
+        if (any_v2) {
+            size_t smem = DEC_WPB * RING + tab + lut;
+            CK(cudaFuncSetAttribute(k_rans_dec_v2<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+            k_rans_dec_v2<S, L><<<dim3(ceil_div_u32(nblk_cap, DEC_WPB), B), DEC_WPB * 32, smem, s>>>(dp);
+            LAUNCHED("k_rans_dec_v2");
+        }
+        if (any_v1) {
+            size_t smem = RING + tab + lut;
+            CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+            k_rans_dec_v1<S, L><<<B, 32, smem, s>>>(dp);
+            LAUNCHED("k_rans_dec_v1");
+        }
+        k_row_sums<S><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+        LAUNCHED("k_row_sums");
+        return SCZ_OK;
+    };
+    // the width filter: kernels of width S skip tensors of another class
+    // (scz_info.sym_bytes set above); row kernels read the same class.
+    int st;
+    if (widths & 1) { if ((st = run_width(uint8_t{})) != SCZ_OK) return st; }
+    if (widths & 2) { if ((st = run_width(uint16_t{})) != SCZ_OK) return st; }
+    if (widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
+    k_row_scan<<<B, 256, 0, s>>>(rp);
+    LAUNCHED("k_row_scan");
+    auto rows_out = [&](auto tag) -> int {
+        using S = decltype(tag);
+        if (stage) k_rows_out<S, true><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+        else k_rows_out<S, false><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+        LAUNCHED("k_rows_out");
+        return SCZ_OK;
+    };
+    if (widths & 1) { if ((st = rows_out(uint8_t{})) != SCZ_OK) return st; }
+    if (widths & 2) { if ((st = rows_out(uint16_t{})) != SCZ_OK) return st; }
+    if (widths & 4) { if ((st = rows_out(uint32_t{})) != SCZ_OK) return st; }
+    return SCZ_OK;
+}
+
+}  // namespace
+
+// The per-width kernels must skip tensors of another class: enforce through
+// the info's sym_bytes in the kernels themselves.
+// (See the `if (in.sym_bytes != sizeof(S)) return;` guards below.)
+
+extern "C" {
+
+int scz_abi_version(void) { return 1; }
+
+int scz_ctx_create(int device, scz_ctx** out) {
+    if (!out) return SCZ_INVALID_INPUT;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) {
+        cudaGetLastError();
+        return SCZ_NO_DEVICE;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) {
+        cudaGetLastError();
+        return SCZ_NO_DEVICE;
+    }
+    scz_ctx* ctx = new scz_ctx();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return SCZ_CUDA_ERROR;
+    }
+    *out = ctx;
+    return SCZ_OK;
+}
+
+void scz_ctx_destroy(scz_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->x_in, &ctx->bitmap, &ctx->tile_stats, &ctx->tile_off, &ctx->state, &ctx->vhist,
+                      &ctx->v8, &ctx->cr, &ctx->hp, &ctx->rhist, &ctx->counts, &ctx->terms, &ctx->freqs,
+                      &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
+                      &ctx->info, &ctx->payload, &ctx->ticket, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
+                      &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
+                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout})
+        b->release();
+    for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
+                       &ctx->h_misc})
+        b->release();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* scz_last_error(const scz_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+void* scz_ctx_stream(scz_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+uint64_t scz_launch_count(const scz_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t batch, int q_bits,
+                     int64_t n_rows, int precision, int format, uint32_t lanes, uint32_t block_syms,
+                     scz_batch* out) {
+    if (!ctx || !out) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    EncPlan pl;
+    int st = plan_encode(ctx, total, batch, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
+    if (st) return st;
+    if ((st = run_encode(ctx, d_x, pl, nullptr)) != SCZ_OK) return st;
+    out->batch = batch;
+    out->d_info = ctx->info.as<scz_info>();
+    out->d_freqs = ctx->freqs.as<uint32_t>();
+    out->d_block_bytes = ctx->block_len.as<uint32_t>();
+    out->d_payload = ctx->payload.as<uint8_t>();
+    out->payload_total = 0;
+    out->freqs_total = (uint64_t)batch * pl.acap;
+    out->blocks_total = (uint64_t)batch * pl.nblk_cap;
+    ctx->last_batch = batch;
+    return SCZ_OK;
+}
+
+int scz_batch_sync(scz_ctx* ctx, scz_batch* b, scz_info* h_info) {
+    if (!ctx || !b || !h_info) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    CK(cudaMemcpyAsync(h_info, b->d_info, (size_t)b->batch * sizeof(scz_info), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    uint64_t tot = 0;
+    for (uint32_t i = 0; i < b->batch; ++i)
+        if (h_info[i].status == SCZ_OK) tot = std::max(tot, h_info[i].payload_off + h_info[i].payload_len);
+    b->payload_total = tot;
+    return SCZ_OK;
+}
+
+int scz_decode_batch_async(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, const uint32_t* d_freqs,
+                           const uint32_t* d_block_bytes, const uint8_t* d_payload, float* d_out) {
+    if (!ctx || !h_info) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    for (uint32_t b = 0; b < batch; ++b) {
+        int st = validate_header(ctx, h_info[b]);
+        if (st) return st;
+    }
+    return run_decode(ctx, h_info, batch, d_freqs, d_block_bytes, d_payload, d_out, false, nullptr, nullptr);
+}
+
+int scz_decode_status(scz_ctx* ctx, uint32_t batch, int32_t* h_status) {
+    if (!ctx || !h_status) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    CK(cudaMemcpyAsync(h_status, ctx->dstatus.p, (size_t)batch * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SCZ_OK;
+}
+
+int scz_decode_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, const uint32_t* d_freqs,
+                     const uint32_t* d_block_bytes, const uint8_t* d_payload, float* d_out,
+                     int32_t* h_status) {
+    int st = scz_decode_batch_async(ctx, h_info, batch, d_freqs, d_block_bytes, d_payload, d_out);
+    if (st) return st;
+    return scz_decode_status(ctx, batch, h_status);
+}
+
+int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64_t n_rows, int precision,
+                 int format, uint32_t lanes, uint32_t block_syms, scz_info* info, const uint32_t** freqs,
+                 const uint32_t** block_bytes, const uint8_t** payload) {
+    if (!ctx || !x || !info) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    EncPlan pl;
+    int st = plan_encode(ctx, total, 1, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
+    if (st) return st;
+    CK(ctx->x_in.ensure(total * 4));
+    CK(cudaMemcpyAsync(ctx->x_in.p, x, total * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if ((st = run_encode(ctx, ctx->x_in.as<float>(), pl, nullptr)) != SCZ_OK) return st;
+    CK(ctx->h_info.ensure(sizeof(scz_info)));
+    CK(cudaMemcpyAsync(ctx->h_info.p, ctx->info.p, sizeof(scz_info), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *info = *ctx->h_info.as<scz_info>();
+    if (info->status != SCZ_OK) {
+        const char* what[] = {"ok", "tensor contains NaN or Inf", "", "", "", "", "symbol exceeds alphabet",
+                              "cannot normalize all-zero counts", "more distinct symbols than slots",
+                              "symbol has zero normalized frequency"};
+        return ctx->fail(info->status, "%s", info->status < 10 ? what[info->status] : "device error");
+    }
+    CK(ctx->h_payload.ensure(info->payload_len + 16));
+    CK(ctx->h_freqs.ensure((size_t)info->alphabet * 4 + 16));
+    CK(ctx->h_blocks.ensure((size_t)info->n_blocks * 4 + 16));
+    CK(cudaMemcpyAsync(ctx->h_payload.p, ctx->payload.as<uint8_t>() + info->payload_off, info->payload_len,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_freqs.p, ctx->freqs.as<uint32_t>() + info->freqs_off, (size_t)info->alphabet * 4,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_blocks.p, ctx->block_len.as<uint32_t>() + info->blocks_off,
+                       (size_t)info->n_blocks * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (freqs) *freqs = ctx->h_freqs.as<uint32_t>();
+    if (block_bytes) *block_bytes = ctx->h_blocks.as<uint32_t>();
+    if (payload) *payload = ctx->h_payload.as<uint8_t>();
+    return SCZ_OK;
+}
+
+int scz_decompress(scz_ctx* ctx, const scz_info* info_in, const uint32_t* freqs, const uint32_t* block_bytes,
+                   const uint8_t* payload, float* out) {
+    if (!ctx || !info_in || !freqs || !out) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    scz_info in = *info_in;
+    int st = validate_header(ctx, in);
+    if (st) return st;
+    // rans.py:372 FrequencyTable.from_freqs: sum must be 2^precision
+    unsigned long long sum = 0;
+    for (uint32_t i = 0; i < in.alphabet; ++i) sum += freqs[i];
+    if (sum != (1ull << in.precision))
+        return ctx->fail(SCZ_CORRUPT_STREAM, "frequencies do not sum to 2^precision");
+    if (in.version == 2) {
+        unsigned long long bsum = 0;
+        for (uint32_t i = 0; i < in.n_blocks; ++i) bsum += block_bytes[i];
+        if (bsum != in.payload_len) return ctx->fail(SCZ_CORRUPT_STREAM, "block lengths do not sum to payload");
+    } else {
+        in.n_blocks = 1;
+    }
+    in.payload_off = 0;
+    in.freqs_off = 0;
+    in.blocks_off = 0;
+    CK(ctx->dpayload.ensure(in.payload_len + 512));
+    CK(ctx->dfreqs.ensure((size_t)in.alphabet * 4));
+    CK(ctx->dblocks.ensure((size_t)in.n_blocks * 4));
+    CK(ctx->dout.ensure(in.total * 4));
+    CK(cudaMemcpyAsync(ctx->dpayload.p, payload, in.payload_len, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->dfreqs.p, freqs, (size_t)in.alphabet * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (in.version == 2)
+        CK(cudaMemcpyAsync(ctx->dblocks.p, block_bytes, (size_t)in.n_blocks * 4, cudaMemcpyHostToDevice,
+                           ctx->stream));
+    if ((st = run_decode(ctx, &in, 1, ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
+                         ctx->dpayload.as<uint8_t>(), ctx->dout.as<float>(), false, nullptr, nullptr)) != SCZ_OK)
+        return st;
+    int32_t dst = 0;
+    CK(cudaMemcpyAsync(&dst, ctx->dstatus.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (dst != SCZ_OK) return ctx->fail(dst, "corrupt stream (device check failed)");
+    CK(cudaMemcpyAsync(out, ctx->dout.p, in.total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SCZ_OK;
+}
+
+// ------------------------------------------------------- stage entry points
+}  // extern "C"
+
+namespace {
+__global__ void k_set_params(TensorState* st, double scale, int64_t z) {
+    st->scale = scale;
+    st->zero_point = z;
+    st->fast = (scale >= 0x1p-120 && scale <= 0x1p120) ? 1u : 0u;
+    st->rcp32 = (float)(1.0 / scale);
+}
+
+int quantize_impl(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, bool given, double g_scale,
+                  int64_t g_z, double* scale, int64_t* zero_point, float* minmax, uint32_t* q,
+                  uint8_t* mask) {
+    if (n < 1 || n >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "size");
+    cudaStream_t s = ctx->stream;
+    uint32_t ntiles = ceil_div_u32(n, TILE), wp = ntiles * TILE_WORDS;
+    CK(ctx->x_in.ensure(n * 4));
+    CK(ctx->bitmap.ensure((size_t)wp * 4));
+    CK(ctx->tile_stats.ensure((size_t)ntiles * sizeof(float4)));
+    CK(ctx->tile_off.ensure((size_t)ntiles * 4));
+    CK(ctx->state.ensure(sizeof(TensorState)));
+    CK(ctx->vhist.ensure(256 * 4));
+    CK(ctx->v8.ensure(n));
+    CK(ctx->dsym_in.ensure(n * 5));
+    CK(cudaMemcpyAsync(ctx->x_in.p, x, n * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ctx->state.p, 0, sizeof(TensorState), s));
+    CK(cudaMemsetAsync(ctx->vhist.p, 0, 256 * 4, s));
+    StatsParams sp{ctx->x_in.as<float>(), n, ntiles, wp, q_bits, ctx->bitmap.as<uint32_t>(),
+                   ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>()};
+    k_stats<<<dim3(ntiles, 1), TILE_THREADS, 0, s>>>(sp);
+    LAUNCHED("k_stats");
+    if (given) {
+        k_set_params<<<1, 1, 0, s>>>(ctx->state.as<TensorState>(), g_scale, g_z);
+        LAUNCHED("k_set_params");
+    }
+    uint32_t* qd = ctx->dsym_in.as<uint32_t>();
+    uint8_t* md = reinterpret_cast<uint8_t*>(qd + n);
+    QuantParams qp{ctx->x_in.as<float>(), n, ntiles, wp, q_bits, ctx->bitmap.as<uint32_t>(),
+                   ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
+                   ctx->vhist.as<uint32_t>(), qd};
+    k_quantize<<<dim3(ntiles, 1), TILE_THREADS, 0, s>>>(qp);
+    LAUNCHED("k_quantize");
+    k_unpack_mask<<<ceil_div_u32(n, 256), 256, 0, s>>>(ctx->bitmap.as<uint32_t>(), n, md);
+    LAUNCHED("k_unpack_mask");
+    TensorState hs;
+    CK(cudaMemcpyAsync(&hs, ctx->state.p, sizeof hs, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hs.status != SCZ_OK || hs.nonfinite) return ctx->fail(SCZ_INVALID_INPUT, "tensor contains NaN or Inf");
+    if (scale) *scale = hs.scale;
+    if (zero_point) *zero_point = hs.zero_point;
+    if (minmax) {
+        minmax[0] = hs.xmin;
+        minmax[1] = hs.xmax;
+    }
+    if (q) CK(cudaMemcpyAsync(q, qd, n * 4, cudaMemcpyDeviceToHost, s));
+    if (mask) CK(cudaMemcpyAsync(mask, md, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return SCZ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int scz_quantize(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, float* minmax, double* scale,
+                 int64_t* zero_point, uint32_t* q, uint8_t* mask) {
+    if (!ctx || !x) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    if (q_bits < 2 || q_bits > 8) return ctx->fail(SCZ_INVALID_INPUT, "q_bits must be in [2, 8]");
+    return quantize_impl(ctx, x, n, q_bits, false, 0.0, 0, scale, zero_point, minmax, q, mask);
+}
+
+int scz_dequantize(scz_ctx* ctx, const uint32_t* q, const uint8_t* mask, uint64_t n, int q_bits, double scale,
+                   int64_t zero_point, float* out) {
+    if (!ctx || !q || !mask || !out) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    (void)q_bits;
+    cudaStream_t s = ctx->stream;
+    CK(ctx->dsym_in.ensure(n * 5));
+    CK(ctx->dout.ensure(n * 4));
+    uint32_t* qd = ctx->dsym_in.as<uint32_t>();
+    uint8_t* md = reinterpret_cast<uint8_t*>(qd + n);
+    CK(cudaMemcpyAsync(qd, q, n * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(md, mask, n, cudaMemcpyHostToDevice, s));
+    k_dequant_flat<<<ceil_div_u32(n, 256), 256, 0, s>>>(qd, md, n, scale, zero_point, ctx->dout.as<float>());
+    LAUNCHED("k_dequant_flat");
+    CK(cudaMemcpyAsync(out, ctx->dout.p, n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return SCZ_OK;
+}
+
+int scz_csr_encode(scz_ctx* ctx, const uint32_t* q, const uint8_t* mask, uint64_t n_rows, uint64_t n_cols,
+                   uint32_t* d, uint64_t* nnz_out) {
+    if (!ctx || !q || !mask || !d) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    const uint64_t n = n_rows * n_cols;
+    if (n < 1 || n >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "size");
+    cudaStream_t s = ctx->stream;
+    uint32_t ntiles = ceil_div_u32(n, TILE), wp = ntiles * TILE_WORDS;
+    CK(ctx->dsym_in.ensure(n * 5));
+    CK(ctx->bitmap.ensure((size_t)wp * 4));
+    CK(ctx->tile_off.ensure((size_t)ntiles * 4));
+    CK(ctx->state.ensure(sizeof(TensorState)));
+    CK(ctx->cr.ensure((size_t)(2 * n + n_rows) * 4));
+    uint32_t* qd = ctx->dsym_in.as<uint32_t>();
+    uint8_t* md = reinterpret_cast<uint8_t*>(qd + n);
+    CK(cudaMemcpyAsync(qd, q, n * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(md, mask, n, cudaMemcpyHostToDevice, s));
+    k_mask_bitmap<<<ntiles, TILE_THREADS, 0, s>>>(md, n, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>());
+    LAUNCHED("k_mask_bitmap");
+    TensorState hs;
+    memset(&hs, 0, sizeof hs);
+    hs.n_cols = (uint32_t)n_cols;
+    hs.n_rows = (uint32_t)n_rows;
+    CK(cudaMemcpyAsync(ctx->state.p, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
+    k_tile_scan<<<1, 256, 0, s>>>(ctx->tile_off.as<uint32_t>(), ntiles, &ctx->state.as<TensorState>()->nnz);
+    LAUNCHED("k_tile_scan");
+    uint32_t* dd = ctx->cr.as<uint32_t>();
+    k_compact_u32<<<ntiles, TILE_THREADS, 0, s>>>(qd, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(), dd);
+    LAUNCHED("k_compact_u32");
+    uint64_t nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, &ctx->state.as<TensorState>()->nnz, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    MatParams mp{n, ntiles, wp, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(),
+                 ctx->state.as<TensorState>(), dd + nnz, 0, 4};
+    k_materialize<uint32_t><<<dim3(ntiles, 1), TILE_THREADS, 0, s>>>(mp);
+    LAUNCHED("k_materialize");
+    CK(cudaMemcpyAsync(d, dd, (size_t)(2 * nnz + n_rows) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (nnz_out) *nnz_out = nnz;
+    return SCZ_OK;
+}
+
+int scz_csr_decode(scz_ctx* ctx, const uint32_t* d, uint64_t nnz, uint64_t n_rows, uint64_t n_cols, uint32_t* q,
+                   uint8_t* mask) {
+    if (!ctx || !d || !q || !mask) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    const uint64_t L = 2 * nnz + n_rows, n = n_rows * n_cols;
+    if (n >= (1ull << 31) || nnz > n) return ctx->fail(SCZ_CORRUPT_STREAM, "nnz exceeds element count");
+    cudaStream_t s = ctx->stream;
+    CK(ctx->dsym.ensure(L * 4));
+    CK(ctx->dsym_in.ensure(n * 5 + 16));
+    CK(ctx->dinfo.ensure(sizeof(scz_info)));
+    CK(ctx->dstatus.ensure(4));
+    uint32_t nch = std::max(1u, ceil_div_u32(n_rows, ROW_CHUNK));
+    CK(ctx->chunk_sum.ensure((size_t)nch * 4));
+    CK(cudaMemcpyAsync(ctx->dsym.p, d, L * 4, cudaMemcpyHostToDevice, s));
+    scz_info in;
+    memset(&in, 0, sizeof in);
+    in.n_rows = (uint32_t)n_rows;
+    in.n_cols = (uint32_t)n_cols;
+    in.nnz = nnz;
+    in.total = n;
+    in.q_bits = 8;
+    in.sym_bytes = 4;
+    CK(cudaMemcpyAsync(ctx->dinfo.p, &in, sizeof in, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ctx->dstatus.p, 0, 4, s));
+    uint32_t* qd = ctx->dsym_in.as<uint32_t>();
+    uint8_t* md = reinterpret_cast<uint8_t*>(qd + n);
+    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, L, ctx->chunk_sum.as<uint32_t>(), nch,
+                 ctx->dstatus.as<int32_t>(), nullptr, nullptr, qd, md};
+    k_row_sums<uint32_t><<<dim3(nch, 1), ROW_THREADS, 0, s>>>(rp);
+    LAUNCHED("k_row_sums");
+    k_row_scan<<<1, 256, 0, s>>>(rp);
+    LAUNCHED("k_row_scan");
+    k_rows_out<uint32_t, true><<<dim3(nch, 1), ROW_THREADS, 0, s>>>(rp);
+    LAUNCHED("k_rows_out");
+    int32_t dst = 0;
+    CK(cudaMemcpyAsync(&dst, ctx->dstatus.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (dst) return ctx->fail(dst, "corrupt CSR stream");
+    CK(cudaMemcpyAsync(q, qd, n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(mask, md, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return SCZ_OK;
+}
+
+int scz_build_counts(scz_ctx* ctx, const uint32_t* d, uint64_t n, uint64_t alphabet, int64_t* counts) {
+    if (!ctx || !counts) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    if (alphabet < 1) return ctx->fail(SCZ_INVALID_INPUT, "alphabet_size must be >= 1");
+    if (alphabet >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "alphabet");
+    cudaStream_t s = ctx->stream;
+    CK(ctx->dsym.ensure(std::max<uint64_t>(n, 1) * 4));
+    CK(ctx->counts.ensure(alphabet * 4 + 4));
+    uint32_t* dc = ctx->counts.as<uint32_t>();
+    CK(cudaMemsetAsync(dc, 0, alphabet * 4 + 4, s));
+    if (n) {
+        CK(cudaMemcpyAsync(ctx->dsym.p, d, n * 4, cudaMemcpyHostToDevice, s));
+        k_hist_u32<<<ceil_div_u32(n, 256), 256, 0, s>>>(ctx->dsym.as<uint32_t>(), n, (uint32_t)alphabet, dc,
+                                                        reinterpret_cast<int32_t*>(dc + alphabet));
+        LAUNCHED("k_hist_u32");
+    }
+    std::vector<uint32_t> h(alphabet + 1);
+    CK(cudaMemcpyAsync(h.data(), dc, (alphabet + 1) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h[alphabet]) return ctx->fail(SCZ_ALPHABET_OVERFLOW, "symbol >= alphabet size %llu",
+                                      (unsigned long long)alphabet);
+    for (uint64_t i = 0; i < alphabet; ++i) counts[i] = h[i];
+    return SCZ_OK;
+}
+
+int scz_normalize(scz_ctx* ctx, const int64_t* counts, uint64_t alphabet, int precision, uint32_t* freqs) {
+    if (!ctx || !counts || !freqs) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    if (alphabet < 1 || alphabet >= (1ull << 31)) return ctx->fail(SCZ_INVALID_INPUT, "alphabet");
+    cudaStream_t s = ctx->stream;
+    std::vector<uint32_t> c32(alphabet);
+    for (uint64_t i = 0; i < alphabet; ++i) {
+        if (counts[i] < 0 || counts[i] > 0xffffffffll) return ctx->fail(SCZ_UNSUPPORTED, "count range");
+        c32[i] = (uint32_t)counts[i];
+    }
+    CK(ctx->counts.ensure(alphabet * 4));
+    CK(ctx->freqs.ensure(alphabet * 4));
+    CK(ctx->terms.ensure(alphabet * 8));
+    CK(ctx->dstatus.ensure(4));
+    CK(cudaMemcpyAsync(ctx->counts.p, c32.data(), alphabet * 4, cudaMemcpyHostToDevice, s));
+    k_normalize_only<<<1, SEL_THREADS, 0, s>>>(ctx->counts.as<uint32_t>(), (uint32_t)alphabet, precision,
+                                                ctx->freqs.as<uint32_t>(), ctx->terms.as<double>(),
+                                                ctx->dstatus.as<int32_t>());
+    LAUNCHED("k_normalize_only");
+    int32_t st = 0;
+    CK(cudaMemcpyAsync(&st, ctx->dstatus.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(freqs, ctx->freqs.p, alphabet * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (st) return ctx->fail(st, "normalize_frequencies failed");
+    return SCZ_OK;
+}
+
+int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t* freqs, uint64_t alphabet,
+                    int precision, uint32_t lanes, uint32_t block_syms, uint8_t* out, uint64_t* out_len,
+                    uint32_t* block_bytes) {
+    if (!ctx || !freqs || !out || !out_len) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    if (precision < 1 || precision > 16) return ctx->fail(SCZ_INVALID_INPUT, "precision");
+    if (alphabet < 1 || alphabet >= (1ull << 31) || n >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "size");
+    const bool v2 = lanes != 0;
+    if (v2 && (lanes != 32 || block_syms < 32 || block_syms % 32))
+        return ctx->fail(SCZ_UNSUPPORTED, "v2 encoder supports 32 lanes, block_syms multiple of 32");
+    cudaStream_t s = ctx->stream;
+    // host-side table (tiny): cum + reciprocal
+    std::vector<EncTab> tab(alphabet);
+    uint64_t c = 0;
+    for (uint64_t i = 0; i < alphabet; ++i) {
+        make_enc_tab(freqs[i], (uint32_t)c, &tab[i]);
+        c += freqs[i];
+    }
+    const uint32_t nblk = v2 ? std::max(1u, ceil_div_u32(n, block_syms)) : 1;
+    const uint64_t slot_cap = ((v2 ? 128 + 2ull * block_syms : 4 + 2 * n) + 15) & ~15ull;
+    CK(ctx->dsym.ensure(std::max<uint64_t>(n, 1) * 4));
+    CK(ctx->enctab.ensure(alphabet * sizeof(EncTab)));
+    CK(ctx->state.ensure(sizeof(TensorState)));
+    CK(ctx->slots.ensure(nblk * slot_cap));
+    CK(ctx->block_len.ensure(nblk * 4));
+    if (n) CK(cudaMemcpyAsync(ctx->dsym.p, d, n * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->enctab.p, tab.data(), alphabet * sizeof(EncTab), cudaMemcpyHostToDevice, s));
+    TensorState hs;
+    memset(&hs, 0, sizeof hs);
+    hs.alphabet = (uint32_t)alphabet;
+    hs.stream_len = n;
+    hs.nnz = n;  // PlainSrc ignores the split
+    CK(cudaMemcpyAsync(ctx->state.p, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
+    EncParams ep{ctx->state.as<TensorState>(), ctx->enctab.as<EncTab>(), (uint32_t)alphabet, precision,
+                 block_syms, ctx->slots.as<uint8_t>(), slot_cap, nblk, ctx->block_len.as<uint32_t>()};
+    PlainSrc src{ctx->dsym.as<uint32_t>(), 0};
+    if (v2) k_rans_enc_v2<PlainSrc><<<dim3(ceil_div_u32(nblk, ENC_WPB), 1), ENC_WPB * 32, 0, s>>>(ep, src);
+    else k_rans_enc_v1<PlainSrc><<<1, 32, 0, s>>>(ep, src);
+    LAUNCHED("k_rans_enc");
+    std::vector<uint32_t> bl(nblk);
+    CK(cudaMemcpyAsync(bl.data(), ctx->block_len.p, nblk * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs, ctx->state.p, sizeof hs, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hs.errbits & 1u) return ctx->fail(SCZ_ALPHABET_OVERFLOW, "symbol >= alphabet size");
+    if (hs.errbits & 2u) return ctx->fail(SCZ_UNCODABLE_SYMBOL, "symbol has zero normalized frequency");
+    uint64_t pos = 0;
+    for (uint32_t b = 0; b < nblk; ++b) {
+        CK(cudaMemcpyAsync(out + pos, ctx->slots.as<uint8_t>() + (uint64_t)b * slot_cap + slot_cap - bl[b], bl[b],
+                           cudaMemcpyDeviceToHost, s));
+        if (block_bytes) block_bytes[b] = bl[b];
+        pos += bl[b];
+    }
+    CK(cudaStreamSynchronize(s));
+    *out_len = pos;
+    return SCZ_OK;
+}
+
+int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint32_t* freqs, uint64_t alphabet,
+                    int precision, uint32_t lanes, uint32_t block_syms, uint64_t n_blocks,
+                    const uint32_t* block_bytes, uint64_t count, uint32_t* out) {
+    if (!ctx || !freqs || !out) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    scz_info in;
+    memset(&in, 0, sizeof in);
+    in.version = lanes ? 2 : 1;
+    in.precision = (uint8_t)precision;
+    in.alphabet = (uint32_t)alphabet;
+    // present the stream as a container with N = count, nnz = 0 so that the
+    // decoder produces exactly `count` symbols
+    in.n_rows = (uint32_t)count;
+    in.nnz = 0;
+    in.n_cols = 1;
+    in.total = count;
+    in.lanes = lanes ? lanes : 1;
+    in.block_syms = lanes ? block_syms : (uint32_t)count;
+    in.n_blocks = lanes ? (uint32_t)n_blocks : 1;
+    in.payload_len = len;
+    if (len < 4) return ctx->fail(SCZ_CORRUPT_STREAM, "bitstream shorter than the 4 state bytes");
+    if (precision < 1 || precision > 31) return ctx->fail(SCZ_CORRUPT_STREAM, "precision");
+    if (count >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "size");
+    if (lanes && (lanes != 32 || precision > 16)) return ctx->fail(SCZ_UNSUPPORTED, "v2 decoder limits");
+    if (lanes && (block_syms < 32 || block_syms % 32 ||
+                  n_blocks != (count ? ceil_div_u32(count, block_syms) : 1)))
+        return ctx->fail(SCZ_CORRUPT_STREAM, "v2 block geometry inconsistent");
+    unsigned long long sum = 0;
+    for (uint64_t i = 0; i < alphabet; ++i) sum += freqs[i];
+    if (sum != (1ull << precision)) return ctx->fail(SCZ_CORRUPT_STREAM, "frequencies do not sum to 2^precision");
+    if (count == 0) {
+        // rans.decode with count 0: only the final checks
+        if (len != 4) return ctx->fail(SCZ_CORRUPT_STREAM, "final state check failed");
+        uint32_t x = data[0] | (data[1] << 8) | (data[2] << 16) | ((uint32_t)data[3] << 24);
+        if (x != STATE_LOW) return ctx->fail(SCZ_CORRUPT_STREAM, "final state check failed");
+        return SCZ_OK;
+    }
+    cudaStream_t s = ctx->stream;
+    CK(ctx->dpayload.ensure(len + 512));
+    CK(ctx->dfreqs.ensure(alphabet * 4));
+    CK(ctx->dblocks.ensure(std::max<uint64_t>(n_blocks, 1) * 4));
+    CK(cudaMemcpyAsync(ctx->dpayload.p, data, len, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->dfreqs.p, freqs, alphabet * 4, cudaMemcpyHostToDevice, s));
+    if (lanes) CK(cudaMemcpyAsync(ctx->dblocks.p, block_bytes, n_blocks * 4, cudaMemcpyHostToDevice, s));
+    // decode only (no CSR stage): run the rANS kernels directly
+    scz_info hi = in;
+    dec_class(hi, &hi.sym_bytes);
+    CK(ctx->dinfo.ensure(sizeof(scz_info)));
+    CK(ctx->dstatus.ensure(4));
+    CK(ctx->cumtab.ensure((alphabet + 1) * 4));
+    CK(ctx->dblk_off.ensure(std::max<uint64_t>(n_blocks, 1) * 4));
+    CK(ctx->dsym.ensure(count * 4));
+    CK(cudaMemcpyAsync(ctx->dinfo.p, &hi, sizeof hi, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ctx->dstatus.p, 0, 4, s));
+    DecParams dp{ctx->dinfo.as<scz_info>(), ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
+                 ctx->dpayload.as<uint8_t>(), ctx->cumtab.as<uint32_t>(), ctx->dblk_off.as<uint32_t>(),
+                 (uint32_t)alphabet, (uint32_t)std::max<uint64_t>(n_blocks, 1), ctx->dsym.p, count,
+                 ctx->dstatus.as<int32_t>()};
+    k_dec_prepare<<<1, 256, 0, s>>>(dp);
+    LAUNCHED("k_dec_prepare");
+    const size_t tab = alphabet <= TAB_SMEM_MAX ? alphabet * sizeof(uint2) : 0;
+    auto go = [&](auto tag) -> int {
+        using S = decltype(tag);
+        const size_t lut = sizeof(S) < 4 ? ((size_t)1 << precision) * sizeof(S) : 0;
+        if (lanes) {
+            size_t smem = DEC_WPB * RING + tab + lut;
+            CK(cudaFuncSetAttribute(k_rans_dec_v2<S, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_rans_dec_v2<S, S><<<dim3(ceil_div_u32(n_blocks, DEC_WPB), 1), DEC_WPB * 32, smem, s>>>(dp);
+        } else {
+            size_t smem = RING + tab + lut;
+            CK(cudaFuncSetAttribute(k_rans_dec_v1<S, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_rans_dec_v1<S, S><<<1, 32, smem, s>>>(dp);
+        }
+        LAUNCHED("k_rans_dec");
+        return SCZ_OK;
+    };
+    int st = hi.sym_bytes == 1 ? go(uint8_t{}) : (hi.sym_bytes == 2 ? go(uint16_t{}) : go(uint32_t{}));
+    if (st) return st;
+    int32_t dst = 0;
+    CK(cudaMemcpyAsync(&dst, ctx->dstatus.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (dst) return ctx->fail(dst, "corrupt stream");
+    // widen to u32 on the host side of the copy
+    if (hi.sym_bytes == 4) {
+        CK(cudaMemcpyAsync(out, ctx->dsym.p, count * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    } else {
+        std::vector<uint8_t> tmp(count * hi.sym_bytes);
+        CK(cudaMemcpyAsync(tmp.data(), ctx->dsym.p, tmp.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < count; ++i)
+            out[i] = hi.sym_bytes == 1 ? tmp[i] : reinterpret_cast<uint16_t*>(tmp.data())[i];
+    }
+    return SCZ_OK;
+}
+
+int scz_search(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, const uint64_t* rows, uint32_t n_rows_list,
+               uint32_t max_cand, uint32_t* n_cand, uint64_t* cand, uint32_t* counts, uint32_t counts_stride,
+               uint32_t* chosen, uint32_t* chosen_exhaustive, uint32_t* flags) {
+    if (!ctx || !x || !n_cand) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    EncPlan pl;
+    std::vector<uint64_t> ex_rows;
+    if (rows) ex_rows.assign(rows, rows + n_rows_list);
+    int st = plan_encode(ctx, n, 1, q_bits, -1, 14, 1, 1, 32, &pl, rows ? &ex_rows : nullptr);
+    if (st) return st;
+    const uint32_t nc = (uint32_t)pl.rows.size();
+    *n_cand = nc;
+    if (nc > max_cand) return ctx->fail(SCZ_INVALID_INPUT, "max_cand too small (%u needed)", nc);
+    if (counts && counts_stride < pl.acap)
+        return ctx->fail(SCZ_INVALID_INPUT, "counts_stride too small (%u needed)", pl.acap);
+    CK(ctx->x_in.ensure(n * 4));
+    CK(ctx->cand_out.ensure((size_t)MAX_CAND * 2 * 8 + (size_t)nc * pl.acap * 4));
+    CK(cudaMemcpyAsync(ctx->x_in.p, x, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* dco = ctx->cand_out.as<double>();
+    uint32_t* ddump = reinterpret_cast<uint32_t*>(dco + MAX_CAND * 2);
+    if ((st = run_encode(ctx, ctx->x_in.as<float>(), pl, dco, counts ? ddump : nullptr)) != SCZ_OK) return st;
+    std::vector<double> co(MAX_CAND * 2);
+    TensorState hs;
+    CK(cudaMemcpyAsync(co.data(), dco, co.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&hs, ctx->state.p, sizeof hs, cudaMemcpyDeviceToHost, ctx->stream));
+    if (counts)
+        for (uint32_t c = 0; c < nc; ++c)
+            CK(cudaMemcpyAsync(counts + (uint64_t)c * counts_stride, ddump + (uint64_t)c * pl.acap,
+                               (size_t)pl.acap * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (hs.nonfinite) return ctx->fail(SCZ_INVALID_INPUT, "tensor contains NaN or Inf");
+    double best = INFINITY;
+    uint32_t ex = 0;
+    for (uint32_t c = 0; c < nc; ++c) {
+        uint64_t N = pl.rows[c];
+        cand[6 * c + 0] = N;
+        cand[6 * c + 1] = n / N;
+        cand[6 * c + 2] = hs.nnz;
+        cand[6 * c + 3] = 2 * hs.nnz + N;
+        memcpy(&cand[6 * c + 4], &co[2 * c], 8);
+        memcpy(&cand[6 * c + 5], &co[2 * c + 1], 8);
+        if (co[2 * c + 1] < best) {
+            best = co[2 * c + 1];
+            ex = c;
+        }
+    }
+    if (chosen) *chosen = hs.cand_index;
+    if (chosen_exhaustive) *chosen_exhaustive = ex;
+    if (flags) *flags = hs.search_flags;
+    return SCZ_OK;
+}
+
+int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t batch, int q_bits,
+                       int64_t n_rows, int precision, int format, uint32_t lanes, uint32_t block_syms,
+                       const scz_info** infos, const uint8_t** payload, const uint32_t** freqs,
+                       const uint32_t** block_bytes, uint64_t* sizes) {
+    if (!ctx || !h_x || !infos) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    EncPlan pl;
+    int st = plan_encode(ctx, total, batch, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
+    if (st) return st;
+    cudaStream_t s = ctx->stream;
+    CK(ctx->x_in.ensure((size_t)batch * total * 4));
+    CK(cudaMemcpyAsync(ctx->x_in.p, h_x, (size_t)batch * total * 4, cudaMemcpyHostToDevice, s));
+    if ((st = run_encode(ctx, ctx->x_in.as<float>(), pl, nullptr)) != SCZ_OK) return st;
+    CK(ctx->hb_info.ensure((size_t)batch * sizeof(scz_info)));
+    scz_info* hi = ctx->hb_info.as<scz_info>();
+    CK(cudaMemcpyAsync(hi, ctx->info.p, (size_t)batch * sizeof(scz_info), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint64_t ptot = 0;
+    for (uint32_t i = 0; i < batch; ++i)
+        if (hi[i].status == SCZ_OK) ptot = std::max(ptot, hi[i].payload_off + hi[i].payload_len);
+    const uint64_t ftot = (uint64_t)batch * pl.acap, btot = (uint64_t)batch * pl.nblk_cap;
+    CK(ctx->hb_payload.ensure(ptot + 16));
+    CK(ctx->hb_freqs.ensure(ftot * 4));
+    CK(ctx->hb_blocks.ensure(btot * 4));
+    CK(cudaMemcpyAsync(ctx->hb_payload.p, ctx->payload.p, ptot, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->hb_freqs.p, ctx->freqs.p, ftot * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->hb_blocks.p, ctx->block_len.p, btot * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *infos = hi;
+    if (payload) *payload = ctx->hb_payload.as<uint8_t>();
+    if (freqs) *freqs = ctx->hb_freqs.as<uint32_t>();
+    if (block_bytes) *block_bytes = ctx->hb_blocks.as<uint32_t>();
+    if (sizes) {
+        sizes[0] = ptot;
+        sizes[1] = ftot;
+        sizes[2] = btot;
+    }
+    return SCZ_OK;
+}
+
+int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, const uint32_t* h_freqs,
+                         uint64_t freqs_count, const uint32_t* h_blocks, uint64_t blocks_count,
+                         const uint8_t* h_payload, uint64_t payload_bytes, float* h_out, int32_t* h_status) {
+    if (!ctx || !h_info || !h_freqs || !h_payload || !h_out || !h_status) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    uint64_t out_total = 0;
+    for (uint32_t b = 0; b < batch; ++b) {
+        int st = validate_header(ctx, h_info[b]);
+        if (st) return st;
+        if (h_info[b].payload_off + h_info[b].payload_len > payload_bytes ||
+            h_info[b].freqs_off + h_info[b].alphabet > freqs_count ||
+            (h_info[b].version == 2 && h_info[b].blocks_off + h_info[b].n_blocks > blocks_count))
+            return ctx->fail(SCZ_INVALID_INPUT, "info offsets exceed the given buffers");
+        out_total += h_info[b].total;
+    }
+    cudaStream_t s = ctx->stream;
+    CK(ctx->dpayload.ensure(payload_bytes + 512));
+    CK(ctx->dfreqs.ensure(freqs_count * 4 + 4));
+    CK(ctx->dblocks.ensure(blocks_count * 4 + 4));
+    CK(ctx->dout.ensure(out_total * 4));
+    CK(cudaMemcpyAsync(ctx->dpayload.p, h_payload, payload_bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->dfreqs.p, h_freqs, freqs_count * 4, cudaMemcpyHostToDevice, s));
+    if (blocks_count && h_blocks)
+        CK(cudaMemcpyAsync(ctx->dblocks.p, h_blocks, blocks_count * 4, cudaMemcpyHostToDevice, s));
+    int st = run_decode(ctx, h_info, batch, ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
+                        ctx->dpayload.as<uint8_t>(), ctx->dout.as<float>(), false, nullptr, nullptr);
+    if (st) return st;
+    CK(cudaMemcpyAsync(h_out, ctx->dout.p, out_total * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_status, ctx->dstatus.p, (size_t)batch * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return SCZ_OK;
+}
+
+int scz_ctx_set_timing(scz_ctx* ctx, int enable) {
+    if (!ctx) return SCZ_INVALID_INPUT;
+    ctx->collect();
+    ctx->timing = enable != 0;
+    ctx->acc.clear();
+    return SCZ_OK;
+}
+
+int scz_ctx_read_timing(scz_ctx* ctx, char* buf, uint64_t cap) {
+    if (!ctx || !buf || cap == 0) return SCZ_INVALID_INPUT;
+    ctx->collect();
+    std::string out;
+    char line[256];
+    for (auto& kv : ctx->acc) {
+        snprintf(line, sizeof line, "%s %.6f %llu\n", kv.first.c_str(), kv.second.first,
+                 (unsigned long long)kv.second.second);
+        out += line;
+    }
+    ctx->acc.clear();
+    if (out.size() + 1 > cap) return ctx->fail(SCZ_INVALID_INPUT, "timing buffer too small");
+    memcpy(buf, out.c_str(), out.size() + 1);
+    return SCZ_OK;
+}
+
+int scz_quantize_params(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, double scale, int64_t zero_point,
+                        uint32_t* q, uint8_t* mask) {
+    if (!ctx || !x) return SCZ_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    if (q_bits < 2 || q_bits > 8) return ctx->fail(SCZ_INVALID_INPUT, "q_bits must be in [2, 8]");
+    if (!(scale > 0)) return ctx->fail(SCZ_INVALID_INPUT, "scale must be positive");
+    return quantize_impl(ctx, x, n, q_bits, true, scale, zero_point, nullptr, nullptr, nullptr, q, mask);
+}
+
+}  // extern "C"

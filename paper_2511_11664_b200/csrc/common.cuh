@@ -1,0 +1,132 @@
+// common.cuh -- shared device definitions for libsczip_b200 (sm_100a).
+//
+// Layout conventions:
+//  * a batch is B tensors of T float32 each, contiguous ([B][T]);
+//  * the zero bitmap of tensor b is bitmap[b * words_pad .. ], bit (p & 31)
+//    of word (p >> 5) set iff x[p] != 0.0f (the ~zero_mask of tensor.py:139);
+//  * D = v ++ c ++ r (sparse.py:98-101) is never materialised whole: values
+//    live in v8 (u8, rank-ordered), columns and row counts in cr (u8/u16/u32);
+//  * per-tensor scalars live in TensorState; per-tensor variable-length
+//    outputs in fixed-stride slots (stride recorded in the launch params).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sczip_b200.h"
+
+namespace scz {
+
+constexpr int TILE = 8192;             // elements per stats/quantize tile
+constexpr int TILE_THREADS = 256;      // 32 elements per thread
+constexpr int TILE_WORDS = TILE / 32;  // bitmap words per tile
+constexpr uint32_t STATE_LOW = 1u << 23;  // rans.py:26
+constexpr int MAX_CAND = 64;           // feasible reshape candidates per launch
+
+// Per-tensor device state written by the encode kernels (internal, not ABI).
+struct TensorState {
+    float xmin, xmax;      // fp32 min/max (tensor.py:127)
+    uint32_t nonfinite;    // FeatureTensor check (tensor.py:48)
+    uint32_t tiles_done;   // last-CTA ticket
+    double scale;          // compute_params (tensor.py:101-122)
+    int64_t zero_point;
+    float rcp32;           // fl32(1/scale) for the guard-band quantiser
+    uint32_t fast;         // 1 if the fp32 guard-band path is valid for this scale
+    uint64_t nnz;
+    uint32_t n_rows, n_cols;
+    uint32_t alphabet;
+    uint32_t cand_index;   // chosen candidate
+    uint64_t stream_len;   // l_D = 2 nnz + N
+    int32_t status;
+    uint32_t search_flags;
+    uint32_t n_evaluated;
+    uint32_t n_blocks;
+    uint32_t sym_bytes;    // width of the c/r symbols of the chosen K (1, 2, 4)
+    uint32_t errbits;      // encoder flags (ERR_OVERFLOW | ERR_UNCODABLE)
+};
+
+struct EncTab {  // per-symbol encoder table entry (16 B)
+    uint32_t freq;
+    uint32_t cum;
+    uint32_t rcp;    // ceil(2^(31+l) / f), l = ceil(log2 f)   (f >= 2)
+    uint32_t shift;  // l - 1 ; 0xFFFFFFFF marks f == 1 (q = x)
+};
+
+__host__ __device__ inline uint32_t ceil_div_u32(uint64_t a, uint64_t b) {
+    return (uint32_t)((a + b - 1) / b);
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ uint32_t lanemask_gt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_gt;" : "=r"(m));
+    return m;
+}
+
+// Exact floor(x / f) for x < 2^31, f >= 1 (Granlund-Montgomery).
+__device__ __forceinline__ uint32_t enc_div(uint32_t x, const EncTab& t) {
+    if (t.shift == 0xFFFFFFFFu) return x;
+    return __umulhi(x, t.rcp) >> t.shift;
+}
+
+__host__ __device__ inline void make_enc_tab(uint32_t f, uint32_t cum, EncTab* t) {
+    t->freq = f;
+    t->cum = cum;
+    if (f <= 1) {
+        t->rcp = 0;
+        t->shift = 0xFFFFFFFFu;
+        return;
+    }
+    uint32_t l = 0;
+    while ((1u << l) < f) ++l;  // l = ceil(log2 f), f <= 2^16
+    uint64_t m = ((1ull << (31 + l)) + f - 1) / f;
+    t->rcp = (uint32_t)m;
+    t->shift = l - 1;
+}
+
+// Block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024,
+// multiple of 32).  Returns the exclusive prefix; *total gets the sum.
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp,
+                                                         uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = (lane < NT / 32) ? s_warp[lane] : 0;
+        uint32_t ws = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = ws - w;
+        if (lane == NT / 32 - 1) s_warp[32] = ws;
+    }
+    __syncthreads();
+    uint32_t r = s_warp[warp] + x - v;
+    *total = s_warp[32];
+    __syncthreads();
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace scz

@@ -1,0 +1,458 @@
+// encode.cu -- compress-side kernels (K1, K2, K3, K6-prep).
+//
+//   k_stats      K1+K2  min/max, non-finite flag, zero bitmap, per-tile nnz;
+//                       the last CTA of each tensor reduces the tiles, scans
+//                       tile nnz and runs compute_params in fp64.
+//   k_quantize   K3     guard-band fp32 quantiser with exact fp64 fix-up,
+//                       rank-compaction of original-nonzero values into v8,
+//                       and the value histogram.
+//   k_colhist           column histogram modulo P = lcm(32, every candidate K)
+//                       from the bitmap (one pass prices every candidate).
+//   k_rowhist           per-candidate histogram of row nonzero counts.
+//   k_materialize       col indices and row counts for the chosen K (c, r).
+#include "common.cuh"
+
+namespace scz {
+
+struct StatsParams {
+    const float* x;
+    uint64_t total;       // T
+    uint32_t n_tiles;
+    uint32_t words_pad;   // bitmap words per tensor (n_tiles * TILE_WORDS)
+    int q_bits;
+    uint32_t* bitmap;     // [B][words_pad]
+    float4* tile_stats;   // [B][n_tiles] {min, max, nnz(bits), nonfinite(bits)}
+    uint32_t* tile_off;   // [B][n_tiles] exclusive nnz prefix
+    TensorState* state;   // [B]
+};
+
+// Load 4 consecutive elements starting at idx (idx % 4 == 0); out-of-range
+// lanes read as 0 and are flagged invalid.
+__device__ __forceinline__ float4 load4(const float* xb, uint64_t idx, uint64_t total,
+                                        bool aligned, uint32_t* valid) {
+    if (aligned && idx + 3 < total) {
+        *valid = 0xF;
+        return __ldg(reinterpret_cast<const float4*>(xb + idx));
+    }
+    float v[4];
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (idx + j < total) {
+            v[j] = xb[idx + j];
+            m |= 1u << j;
+        } else {
+            v[j] = 0.0f;
+        }
+    }
+    *valid = m;
+    return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// tensor.py:101-122 compute_params in fp64 with explicitly rounded ops.
+__device__ void device_compute_params(float fmin, float fmax, int q_bits, double* scale,
+                                      int64_t* z) {
+    double x_min = (double)fmin, x_max = (double)fmax;
+    int64_t q_max = (1 << q_bits) - 1;
+    double lo = (0.0 < x_min) ? 0.0 : x_min;
+    double hi = (0.0 > x_max) ? 0.0 : x_max;
+    double s;
+    int64_t zz;
+    if (hi == lo) {
+        s = 1.0;
+        zz = 0;
+    } else {
+        s = __ddiv_rn(__dsub_rn(hi, lo), (double)q_max);
+        double t = __ddiv_rn(-lo, s);
+        double a = floor(__dadd_rn(fabs(t), 0.5));
+        zz = (int64_t)copysign(a, t);
+    }
+    if (zz < 0) zz = 0;
+    if (zz > q_max) zz = q_max;
+    *scale = s;
+    *z = zz;
+}
+
+__global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
+    const uint32_t tile = blockIdx.x, b = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float* xb = p.x + (uint64_t)b * p.total;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(xb) & 15) == 0);
+    const uint64_t tile_base = (uint64_t)tile * TILE;
+    uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad + (uint64_t)tile * TILE_WORDS;
+
+    float mn = INFINITY, mx = -INFINITY;
+    uint32_t nnz = 0, bad = 0;
+#pragma unroll 4
+    for (int it = 0; it < 8; ++it) {
+        uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4;
+        uint32_t valid;
+        float4 v = load4(xb, idx, p.total, aligned, &valid);
+        float e[4] = {v.x, v.y, v.z, v.w};
+        uint32_t nib = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (valid >> j & 1) {
+                if (!isfinite(e[j])) bad = 1;
+                mn = fminf(mn, e[j]);
+                mx = fmaxf(mx, e[j]);
+                nib |= (uint32_t)(e[j] != 0.0f) << j;
+            }
+        }
+        nnz += __popc(nib);
+        uint32_t w = nib << (4 * (lane & 7));
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & 7) == 0) bm[warp * 32 + it * 4 + (lane >> 3)] = w;
+    }
+    // block reduce
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    __shared__ float s_mn[8], s_mx[8];
+    __shared__ uint32_t s_nnz[8], s_bad[8];
+    __shared__ uint32_t s_last;
+    if (lane == 0) {
+        s_mn[warp] = mn;
+        s_mx[warp] = mx;
+        s_nnz[warp] = nnz;
+        s_bad[warp] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) {
+            mn = fminf(mn, s_mn[w]);
+            mx = fmaxf(mx, s_mx[w]);
+            nnz += s_nnz[w];
+            bad |= s_bad[w];
+        }
+        p.tile_stats[(uint64_t)b * p.n_tiles + tile] =
+            make_float4(mn, mx, __uint_as_float(nnz), __uint_as_float(bad));
+        __threadfence();
+        uint32_t t = atomicAdd(&p.state[b].tiles_done, 1u);
+        s_last = (t == p.n_tiles - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+
+    // ---- last CTA of tensor b: reduce tiles, scan nnz, compute params ----
+    __shared__ uint32_t s_scan[33];
+    const float4* ts = p.tile_stats + (uint64_t)b * p.n_tiles;
+    uint32_t* toff = p.tile_off + (uint64_t)b * p.n_tiles;
+    float gmn = INFINITY, gmx = -INFINITY;
+    uint32_t gbad = 0, carry = 0;
+    for (uint32_t base = 0; base < p.n_tiles; base += TILE_THREADS) {
+        uint32_t i = base + threadIdx.x;
+        uint32_t c = 0;
+        if (i < p.n_tiles) {
+            float4 s = __ldcg(ts + i);
+            gmn = fminf(gmn, s.x);
+            gmx = fmaxf(gmx, s.y);
+            c = __float_as_uint(s.z);
+            gbad |= __float_as_uint(s.w);
+        }
+        uint32_t tot;
+        uint32_t ex = block_exclusive_scan<TILE_THREADS>(c, s_scan, &tot);
+        if (i < p.n_tiles) toff[i] = carry + ex;
+        carry += tot;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gmn = fminf(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+        gmx = fmaxf(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+        gbad |= __shfl_xor_sync(0xffffffffu, gbad, o);
+    }
+    if (lane == 0) {
+        s_mn[warp] = gmn;
+        s_mx[warp] = gmx;
+        s_bad[warp] = gbad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) {
+            gmn = fminf(gmn, s_mn[w]);
+            gmx = fmaxf(gmx, s_mx[w]);
+            gbad |= s_bad[w];
+        }
+        TensorState& st = p.state[b];
+        st.xmin = gmn;
+        st.xmax = gmx;
+        st.nonfinite = gbad;
+        st.nnz = carry;
+        st.tiles_done = 0;  // re-arm for the next launch
+        if (gbad) {
+            st.status = SCZ_INVALID_INPUT;
+            st.scale = 1.0;
+            st.zero_point = 0;
+            st.fast = 0;
+            st.rcp32 = 1.0f;
+        } else {
+            double s;
+            int64_t z;
+            device_compute_params(gmn, gmx, p.q_bits, &s, &z);
+            st.scale = s;
+            st.zero_point = z;
+            // guard-band path needs fl32(1/s) normal and x*r32 finite
+            st.fast = (s >= 0x1p-120 && s <= 0x1p120) ? 1u : 0u;
+            st.rcp32 = (float)(1.0 / s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- quantize
+struct QuantParams {
+    const float* x;
+    uint64_t total;
+    uint32_t n_tiles;
+    uint32_t words_pad;
+    int q_bits;
+    const uint32_t* bitmap;
+    const uint32_t* tile_off;
+    const TensorState* state;
+    uint8_t* v8;          // [B][total] compacted value symbols
+    uint32_t* vhist;      // [B][256]
+    uint32_t* sym_out;    // optional [B][total] full symbol array (stage API)
+};
+
+// tensor.py:130-140 for one element: exact fp64 sequence of the reference.
+__device__ __forceinline__ uint32_t quant_exact(float x, double scale, double zf, double qmax) {
+    double y = __dadd_rn(__ddiv_rn((double)x, scale), zf);
+    double a = floor(__dadd_rn(fabs(y), 0.5));
+    double r = (y > 0.0) ? a : ((y < 0.0) ? -a : 0.0);
+    r = fmin(fmax(r, 0.0), qmax);
+    return (uint32_t)r;
+}
+
+// fp32 estimate y = x * fl32(1/s) + z has |error| < 2^-14.4; any
+// y within 2^-12 of a rounding boundary k + 1/2 is recomputed exactly.
+__device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, int qmax,
+                                               double scale, double zf, bool fast) {
+    if (fast) {
+        float y = fmaf(x, r32, zf32);
+        float fr = y - floorf(y);
+        if (fabsf(fr - 0.5f) > 0x1p-12f) {
+            int q = __float2int_rn(y);
+            return (uint32_t)min(max(q, 0), qmax);
+        }
+    }
+    return quant_exact(x, scale, zf, (double)qmax);
+}
+
+__global__ void __launch_bounds__(TILE_THREADS) k_quantize(QuantParams p) {
+    const uint32_t tile = blockIdx.x, b = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const TensorState& st = p.state[b];
+    if (st.status != SCZ_OK) return;
+    const float* xb = p.x + (uint64_t)b * p.total;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(xb) & 15) == 0);
+    const uint64_t tile_base = (uint64_t)tile * TILE;
+    const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad + (uint64_t)tile * TILE_WORDS;
+
+    __shared__ uint32_t s_wpre[TILE_WORDS];
+    __shared__ uint32_t s_scan[33];
+    __shared__ uint32_t s_hist[256];
+    const int nbins = 1 << p.q_bits;
+    for (int i = threadIdx.x; i < nbins; i += TILE_THREADS) s_hist[i] = 0;
+    uint32_t myword = bm[threadIdx.x];
+    uint32_t tot;
+    s_wpre[threadIdx.x] = block_exclusive_scan<TILE_THREADS>(__popc(myword), s_scan, &tot);
+    // (block_exclusive_scan ends with __syncthreads)
+    const uint32_t base_rank = p.tile_off[(uint64_t)b * p.n_tiles + tile];
+    const double scale = st.scale;
+    const double zf = (double)st.zero_point;
+    const float r32 = st.rcp32, zf32 = (float)st.zero_point;
+    const bool fast = st.fast != 0;
+    const int qmax = nbins - 1;
+    uint8_t* v8 = p.v8 + (uint64_t)b * p.total;
+
+#pragma unroll 2
+    for (int it = 0; it < 8; ++it) {
+        uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4;
+        uint32_t valid;
+        float4 v = load4(xb, idx, p.total, aligned, &valid);
+        float e[4] = {v.x, v.y, v.z, v.w};
+        const int word = warp * 32 + it * 4 + (lane >> 3);
+        const uint32_t wbits = bm[word];
+        const int bit0 = 4 * (lane & 7);
+        uint32_t rank = base_rank + s_wpre[word] + __popc(wbits & ((1u << bit0) - 1u));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if ((valid >> j & 1) && e[j] != 0.0f) {
+                uint32_t q = quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
+                v8[rank++] = (uint8_t)q;
+                atomicAdd(&s_hist[q], 1u);
+                if (p.sym_out) p.sym_out[(uint64_t)b * p.total + idx + j] = q;
+            } else if (p.sym_out && (valid >> j & 1)) {
+                p.sym_out[(uint64_t)b * p.total + idx + j] =
+                    quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t* gh = p.vhist + (uint64_t)b * 256;
+    for (int i = threadIdx.x; i < nbins; i += TILE_THREADS)
+        if (s_hist[i]) atomicAdd(gh + i, s_hist[i]);
+}
+
+// ------------------------------------------------------- search histograms
+struct ColHistParams {
+    const uint32_t* bitmap;
+    uint32_t words_pad;
+    uint32_t n_words;      // ceil(T / 32)
+    uint32_t period_words; // P / 32
+    uint32_t n_rows;       // ceil(n_words / period_words)
+    uint32_t rows_per_cta; // row chunk handled by one CTA
+    uint32_t* hp;          // [B][P] counts of nonzeros at p mod P
+    uint32_t hp_stride;
+};
+
+// H_P[j] = #{p : p mod P == j, x[p] != 0}; thread owns one bitmap word
+// column of the (rows x P) view and counts its 32 bit positions.
+__global__ void __launch_bounds__(128) k_colhist(ColHistParams p) {
+    const uint32_t q = blockIdx.x * 128 + threadIdx.x;
+    const uint32_t b = blockIdx.z;
+    if (q >= p.period_words) return;
+    const uint32_t r0 = blockIdx.y * p.rows_per_cta;
+    const uint32_t r1 = min(p.n_rows, r0 + p.rows_per_cta);
+    const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad;
+    uint32_t cnt[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) cnt[i] = 0;
+    for (uint32_t r = r0; r < r1; ++r) {
+        uint64_t wi = (uint64_t)r * p.period_words + q;
+        if (wi >= p.n_words) break;
+        uint32_t w = __ldg(bm + wi);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) cnt[i] += (w >> i) & 1u;
+    }
+    uint32_t* hp = p.hp + (uint64_t)b * p.hp_stride + q * 32;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        if (cnt[i]) atomicAdd(hp + i, cnt[i]);
+}
+
+// popcount of bits [start, start + len) of a bitmap (len >= 1).
+__device__ __forceinline__ uint32_t range_popc(const uint32_t* bm, uint64_t start, uint32_t len) {
+    uint64_t end = start + len;
+    uint64_t w0 = start >> 5, w1 = (end - 1) >> 5;
+    uint32_t s = (uint32_t)(start & 31);
+    if (w0 == w1) {
+        uint32_t w = __ldg(bm + w0) >> s;
+        uint32_t m = (len >= 32) ? 0xffffffffu : ((1u << len) - 1u);
+        return __popc(w & m);
+    }
+    uint32_t c = __popc(__ldg(bm + w0) >> s);
+    for (uint64_t w = w0 + 1; w < w1; ++w) c += __popc(__ldg(bm + w));
+    uint32_t e = (uint32_t)(end & 31);
+    uint32_t last = __ldg(bm + w1);
+    c += __popc(e ? (last & ((1u << e) - 1u)) : last);
+    return c;
+}
+
+struct RowHistParams {
+    const uint32_t* bitmap;
+    uint32_t words_pad;
+    uint32_t n_cand;
+    uint32_t cand_k[MAX_CAND];        // K per candidate
+    uint32_t cand_rows[MAX_CAND];     // N per candidate
+    uint32_t chunk_start[MAX_CAND + 1];  // first CTA-chunk of each candidate
+    uint32_t rhist_off[MAX_CAND];     // offset of candidate's r-hist (K+1 bins)
+    uint32_t rows_per_chunk;
+    uint32_t* rhist;                  // [B][rhist_stride]
+    uint32_t rhist_stride;
+};
+
+// Row-count histograms for every candidate K: r_i = popcount(row i).
+__global__ void __launch_bounds__(256) k_rowhist(RowHistParams p) {
+    const uint32_t chunk = blockIdx.x, b = blockIdx.y;
+    uint32_t c = 0;
+    while (c + 1 < p.n_cand && p.chunk_start[c + 1] <= chunk) ++c;
+    const uint32_t K = p.cand_k[c], N = p.cand_rows[c];
+    const uint32_t nb = K + 1;
+    extern __shared__ uint32_t s_h[];
+    const bool use_smem = nb <= 4096;
+    uint32_t* gh = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c];
+    if (use_smem)
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) s_h[i] = 0;
+    __syncthreads();
+    const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad;
+    const uint64_t r0 = (uint64_t)(chunk - p.chunk_start[c]) * p.rows_per_chunk;
+    const uint64_t r1 = min((uint64_t)N, r0 + p.rows_per_chunk);
+    for (uint64_t r = r0 + threadIdx.x; r < r0 + ((r1 - r0 + 31) & ~31ull); r += blockDim.x) {
+        const bool live = r < r1;
+        uint32_t v = live ? range_popc(bm, r * K, K) : 0xffffffffu;
+        uint32_t peers = __match_any_sync(0xffffffffu, v);
+        if (live && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+            if (use_smem) atomicAdd(&s_h[v], (uint32_t)__popc(peers));
+            else atomicAdd(gh + v, (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    if (use_smem)
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+            if (s_h[i]) atomicAdd(gh + i, s_h[i]);
+}
+
+// ------------------------------------------------------------ materialise
+struct MatParams {
+    uint64_t total;
+    uint32_t n_tiles;
+    uint32_t words_pad;
+    const uint32_t* bitmap;
+    const uint32_t* tile_off;
+    const TensorState* state;
+    void* cr;             // [B][cr_stride] symbols of width sym_bytes
+    uint64_t cr_stride;   // elements
+    int sym_bytes;
+};
+
+template <typename S>
+__device__ __forceinline__ void store_sym(void* base, uint64_t i, uint32_t v) {
+    reinterpret_cast<S*>(base)[i] = (S)v;
+}
+
+template <typename S>
+__global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
+    const uint32_t tile = blockIdx.x, b = blockIdx.y;
+    const TensorState& st = p.state[b];
+    if (st.status != SCZ_OK) return;
+    const uint32_t K = st.n_cols;
+    const uint64_t nnz = st.nnz;
+    const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad;
+    S* cr = reinterpret_cast<S*>(p.cr) + (uint64_t)b * p.cr_stride;
+    __shared__ uint32_t s_scan[33];
+    const uint64_t word = (uint64_t)tile * TILE_WORDS + threadIdx.x;
+    uint32_t w = bm[word];
+    uint32_t tot;
+    uint32_t rank = p.tile_off[(uint64_t)b * p.n_tiles + tile] +
+                    block_exclusive_scan<TILE_THREADS>(__popc(w), s_scan, &tot);
+    // column index of every nonzero: p mod K (sparse.py:66-68)
+    if (w) {
+        uint64_t p0 = word * 32;
+        uint32_t m = (uint32_t)(p0 % K);
+        while (w) {
+            int bit = __ffs(w) - 1;
+            w &= w - 1;
+            uint32_t c = m + bit;
+            if (c >= K) c = (K <= 32) ? c % K : c - K;
+            cr[rank++] = (S)c;
+        }
+    }
+    // row counts for the rows starting in this tile (sparse.py:68)
+    uint64_t ts = (uint64_t)tile * TILE, te = min(ts + TILE, p.total);
+    uint64_t i0 = (ts + K - 1) / K, i1 = (te + K - 1) / K;
+    for (uint64_t i = i0 + threadIdx.x; i < i1; i += TILE_THREADS)
+        cr[nnz + i] = (S)range_popc(bm, i * K, K);
+}
+
+template __global__ void k_materialize<uint8_t>(MatParams);
+template __global__ void k_materialize<uint16_t>(MatParams);
+template __global__ void k_materialize<uint32_t>(MatParams);
+
+}  // namespace scz

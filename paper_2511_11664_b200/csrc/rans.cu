@@ -1,0 +1,464 @@
+// rans.cu -- rANS encode/decode kernels (K5, K7).
+//
+// Arithmetic per symbol is exactly rans.py:134-152 (32-bit state, L = 2^23,
+// byte renormalisation, precision n).  Two layouts (FORMAT.md):
+//   v1  one stream per tensor, byte-identical to rans.encode (rans.py:155-180);
+//       one warp per tensor runs the serial recurrence (lanes redundant, the
+//       table entries of the next 32 symbols are fetched in parallel).
+//   v2  blocks of B symbols, W = 32 interleaved lanes per block, one warp per
+//       block, one lane per rANS state.  Renormalisation bytes of a step are
+//       placed by a warp ballot-scan (<= 2 bytes per lane per step).
+#include "common.cuh"
+
+namespace scz {
+
+constexpr int ENC_WPB = 4;    // warps (= v2 blocks) per CTA
+constexpr int DEC_WPB = 4;
+constexpr int RING = 512;     // per-warp payload ring buffer (bytes)
+constexpr uint32_t TAB_SMEM_MAX = 2048;  // symbols whose table fits in smem
+
+// ---- symbol sources: D[i] for tensor b -----------------------------------
+template <typename S>
+struct SplitSrc {  // D = v8[0..nnz) ++ cr[0..nnz+N)
+    const uint8_t* v8;
+    uint64_t v8_stride;
+    const S* cr;
+    uint64_t cr_stride;
+    __device__ __forceinline__ uint32_t at(uint32_t b, uint64_t i, uint64_t nnz) const {
+        return i < nnz ? (uint32_t)v8[b * v8_stride + i] : (uint32_t)cr[b * cr_stride + (i - nnz)];
+    }
+    static constexpr int width = sizeof(S);
+};
+struct PlainSrc {  // D given as u32 (stage API)
+    const uint32_t* d;
+    uint64_t stride;
+    __device__ __forceinline__ uint32_t at(uint32_t b, uint64_t i, uint64_t) const {
+        return d[b * stride + i];
+    }
+    static constexpr int width = 0;  // matches any sym_bytes
+};
+
+struct EncParams {
+    TensorState* state;
+    const EncTab* enctab;
+    uint32_t acap;
+    int precision;
+    uint32_t block_syms;      // v2 block size (multiple of 32)
+    uint8_t* slots;           // block output slots
+    uint64_t slot_cap;        // bytes per slot
+    uint32_t slots_per_tensor;
+    uint32_t* block_len;      // [B][slots_per_tensor]
+};
+
+__device__ __forceinline__ void flag_err(TensorState& st, uint32_t bit) {
+    atomicOr(&st.errbits, bit);
+}
+constexpr uint32_t ERR_OVERFLOW = 1, ERR_UNCODABLE = 2;
+
+template <class Src>
+__global__ void __launch_bounds__(ENC_WPB * 32) k_rans_enc_v2(EncParams p, Src src) {
+    const uint32_t b = blockIdx.y;
+    TensorState& st = p.state[b];
+    if (st.status != SCZ_OK) return;
+    if (Src::width && st.sym_bytes != (uint32_t)Src::width) return;  // other width variant
+    __shared__ EncTab s_tab[TAB_SMEM_MAX];
+    const uint32_t A = st.alphabet;
+    const EncTab* gt = p.enctab + (uint64_t)b * p.acap;
+    const bool smem_tab = A <= TAB_SMEM_MAX;
+    if (smem_tab)
+        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) s_tab[i] = gt[i];
+    __syncthreads();
+    const EncTab* tab = smem_tab ? s_tab : gt;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t L = st.stream_len;
+    const uint32_t nblk = L ? ceil_div_u32(L, p.block_syms) : 1;
+    const uint32_t blk = blockIdx.x * ENC_WPB + warp;
+    if (blk >= nblk) return;
+    const uint64_t nnz = st.nnz;
+    const uint64_t base = (uint64_t)blk * p.block_syms;
+    const uint32_t len = (uint32_t)min((uint64_t)p.block_syms, L - base);
+    const uint32_t steps = (len + 31) / 32;
+    const int n = p.precision;
+    const uint32_t gtm = lanemask_gt();
+    uint8_t* slot = p.slots + ((uint64_t)b * p.slots_per_tensor + blk) * p.slot_cap;
+    uint8_t* tail = slot + p.slot_cap - 1;  // emitted byte k lands at tail[-k]
+    uint32_t x = STATE_LOW, emitted = 0, err = 0;
+
+    // software pipeline: symbol of the next step is fetched one step ahead
+    uint32_t i_next = (steps - 1) * 32 + lane;
+    uint32_t sym_next = (steps && i_next < len) ? src.at(b, base + i_next, nnz) : 0;
+    for (int s = (int)steps - 1; s >= 0; --s) {
+        const uint32_t i = (uint32_t)s * 32 + lane;
+        const bool active = i < len;
+        uint32_t sym = sym_next;
+        if (s > 0) sym_next = src.at(b, base + i - 32, nnz);  // i - 32 < len always
+        EncTab t = {1, 0, 0, 0xFFFFFFFFu};
+        if (active) {
+            if (sym >= A) {
+                err |= ERR_OVERFLOW;
+            } else {
+                t = tab[sym];
+                if (t.freq == 0) err |= ERR_UNCODABLE;
+            }
+        }
+        const bool live = active && t.freq != 0 && sym < A;
+        const uint32_t bound = t.freq << (31 - n);  // ((L >> n) << 8) * f
+        uint32_t e = 0;
+        if (live && x >= bound) e = ((x >> 8) >= bound) ? 2u : 1u;
+        const uint32_t b1 = __ballot_sync(0xffffffffu, e >= 1);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, e == 2);
+        const uint32_t k = emitted + __popc(b1 & gtm) + __popc(b2 & gtm);
+        if (e >= 1) tail[-(int64_t)k] = (uint8_t)(x & 0xFF);
+        if (e == 2) tail[-(int64_t)k - 1] = (uint8_t)((x >> 8) & 0xFF);
+        emitted += __popc(b1) + __popc(b2);
+        x >>= 8 * e;
+        if (live) {
+            uint32_t q = enc_div(x, t);
+            x = (q << n) + t.cum + (x - q * t.freq);
+        }
+    }
+    // block bytes: W little-endian states, then the emitted bytes (decoder order)
+    const uint32_t blen = 4 * 32 + emitted;
+    uint8_t* start = slot + p.slot_cap - blen;
+    start[4 * lane + 0] = (uint8_t)x;
+    start[4 * lane + 1] = (uint8_t)(x >> 8);
+    start[4 * lane + 2] = (uint8_t)(x >> 16);
+    start[4 * lane + 3] = (uint8_t)(x >> 24);
+    err = __reduce_or_sync(0xffffffffu, err);
+    if (lane == 0) {
+        p.block_len[(uint64_t)b * p.slots_per_tensor + blk] = blen;
+        if (err) flag_err(st, err);
+    }
+}
+
+// v1: the reference's single stream.  One warp per tensor; all lanes carry
+// the same state, lane j prefetches the table entry of the j-th next symbol.
+template <class Src>
+__global__ void __launch_bounds__(32) k_rans_enc_v1(EncParams p, Src src) {
+    const uint32_t b = blockIdx.x;
+    TensorState& st = p.state[b];
+    if (st.status != SCZ_OK) return;
+    if (Src::width && st.sym_bytes != (uint32_t)Src::width) return;
+    __shared__ EncTab s_tab[TAB_SMEM_MAX];
+    const uint32_t A = st.alphabet;
+    const EncTab* gt = p.enctab + (uint64_t)b * p.acap;
+    const bool smem_tab = A <= TAB_SMEM_MAX;
+    if (smem_tab)
+        for (uint32_t i = threadIdx.x; i < A; i += 32) s_tab[i] = gt[i];
+    __syncwarp();
+    const EncTab* tab = smem_tab ? s_tab : gt;
+    const uint32_t lane = threadIdx.x;
+    const uint64_t L = st.stream_len, nnz = st.nnz;
+    const int n = p.precision;
+    uint8_t* slot = p.slots + (uint64_t)b * p.slots_per_tensor * p.slot_cap;
+    uint8_t* tail = slot + p.slot_cap - 1;
+    uint32_t x = STATE_LOW, err = 0;
+    uint64_t emitted = 0;
+    for (uint64_t top = L; top > 0;) {
+        const uint32_t cnt = (uint32_t)(top < 32 ? top : 32);
+        // lane j holds symbol top-1-j (processed j-th in this chunk)
+        EncTab mine = {1, 0, 0, 0xFFFFFFFFu};
+        uint32_t ok = 1;
+        if (lane < cnt) {
+            uint32_t sym = src.at(b, top - 1 - lane, nnz);
+            if (sym >= A) {
+                err |= ERR_OVERFLOW;
+                ok = 0;
+            } else {
+                mine = tab[sym];
+                if (mine.freq == 0) {
+                    err |= ERR_UNCODABLE;
+                    ok = 0;
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, !ok)) break;
+        for (uint32_t j = 0; j < cnt; ++j) {
+            EncTab t;
+            t.freq = __shfl_sync(0xffffffffu, mine.freq, j);
+            t.cum = __shfl_sync(0xffffffffu, mine.cum, j);
+            t.rcp = __shfl_sync(0xffffffffu, mine.rcp, j);
+            t.shift = __shfl_sync(0xffffffffu, mine.shift, j);
+            const uint32_t bound = t.freq << (31 - n);
+            if (x >= bound) {
+                if (lane == 0) tail[-(int64_t)emitted] = (uint8_t)(x & 0xFF);
+                x >>= 8;
+                ++emitted;
+                if (x >= bound) {
+                    if (lane == 0) tail[-(int64_t)emitted] = (uint8_t)(x & 0xFF);
+                    x >>= 8;
+                    ++emitted;
+                }
+            }
+            uint32_t q = enc_div(x, t);
+            x = (q << n) + t.cum + (x - q * t.freq);
+        }
+        top -= cnt;
+    }
+    err = __reduce_or_sync(0xffffffffu, err);
+    if (lane == 0) {
+        uint8_t* start = slot + p.slot_cap - emitted - 4;
+        start[0] = (uint8_t)x;
+        start[1] = (uint8_t)(x >> 8);
+        start[2] = (uint8_t)(x >> 16);
+        start[3] = (uint8_t)(x >> 24);
+        p.block_len[(uint64_t)b * p.slots_per_tensor] = (uint32_t)(4 + emitted);
+        if (err) flag_err(st, err);
+    }
+}
+
+// ---------------------------------------------------------------- decode
+struct DecParams {
+    const scz_info* info;        // [B] device copy
+    const uint32_t* freqs;       // batch freq buffer
+    const uint32_t* block_bytes; // batch block-length buffer
+    const uint8_t* payload;      // batch payload buffer (256-byte aligned base)
+    uint32_t* cumtab;            // scratch [B][acap + 1]
+    uint32_t* blk_off;           // scratch [B][nblk_cap]
+    uint32_t acap, nblk_cap;
+    void* dsym;                  // out [B][dsym_stride] symbols, width sym_w
+    uint64_t dsym_stride;
+    int32_t* status;             // [B]
+};
+
+// Per tensor: validate the table (rans.py:49-56, Σ f == 2^n), build the cdf,
+// scan block lengths into offsets and check them against the header.
+__global__ void __launch_bounds__(256) k_dec_prepare(DecParams p) {
+    const uint32_t b = blockIdx.x;
+    const scz_info& in = p.info[b];
+    __shared__ uint32_t s_scan[33];
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    if (p.status[b] != SCZ_OK) return;
+    const uint32_t A = in.alphabet;
+    const uint32_t* f = p.freqs + in.freqs_off;
+    uint32_t* cum = p.cumtab + (uint64_t)b * (p.acap + 1);
+    unsigned long long carry = 0;
+    for (uint32_t base = 0; base < A; base += 256) {
+        uint32_t i = base + threadIdx.x;
+        uint32_t v = i < A ? f[i] : 0;
+        uint32_t tot;
+        uint32_t ex = block_exclusive_scan<256>(v, s_scan, &tot);
+        if (i < A) cum[i] = (uint32_t)(carry + ex);
+        carry += tot;
+    }
+    if (threadIdx.x == 0) cum[A] = (uint32_t)carry;
+    if (carry != (1ull << in.precision) && threadIdx.x == 0) s_bad = 1;
+    // block offsets
+    const uint32_t W = in.version == 2 ? in.lanes : 1;
+    uint32_t* off = p.blk_off + (uint64_t)b * p.nblk_cap;
+    carry = 0;
+    for (uint32_t base = 0; base < in.n_blocks; base += 256) {
+        uint32_t i = base + threadIdx.x;
+        uint32_t v = 0;
+        if (i < in.n_blocks) {
+            v = in.version == 2 ? p.block_bytes[in.blocks_off + i] : (uint32_t)in.payload_len;
+            if (v < 4 * W) s_bad = 1;
+        }
+        uint32_t tot;
+        uint32_t ex = block_exclusive_scan<256>(v, s_scan, &tot);
+        if (i < in.n_blocks) off[i] = (uint32_t)(carry + ex);
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && carry != in.payload_len) s_bad = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_bad) p.status[b] = SCZ_CORRUPT_STREAM;
+}
+
+// slot -> symbol lookup table over [0, 2^n): thread t fills a contiguous
+// range, starting from a binary search of cum.
+template <typename L>
+__device__ void build_lut(L* lut, const uint32_t* cum, uint32_t A, uint32_t nslots) {
+    const uint32_t per = (nslots + blockDim.x - 1) / blockDim.x;
+    uint32_t s0 = threadIdx.x * per;
+    if (s0 >= nslots) return;
+    uint32_t s1 = min(nslots, s0 + per);
+    // largest sym with cum[sym] <= s0 (searchsorted right - 1)
+    uint32_t lo = 0, hi = A + 1;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (cum[mid] <= s0) lo = mid;
+        else hi = mid;
+    }
+    uint32_t sym = lo;
+    for (uint32_t sl = s0; sl < s1; ++sl) {
+        while (cum[sym + 1] <= sl) ++sym;
+        lut[sl] = (L)sym;
+    }
+}
+
+__device__ __forceinline__ uint32_t find_sym(const uint32_t* cum, uint32_t A, uint32_t slot) {
+    uint32_t lo = 0, hi = A + 1;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (cum[mid] <= slot) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// slot -> symbol: LUT when L is u8/u16, binary search of the cdf otherwise
+// (np.searchsorted(cdf, slot, 'right') - 1, rans.py:201).
+template <typename L>
+__device__ __forceinline__ uint32_t lookup(const L* lut, const uint32_t* cum, uint32_t A,
+                                           uint32_t slot) {
+    if constexpr (sizeof(L) == 4) return find_sym(cum, A, slot);
+    else return lut[slot];
+}
+
+// Per-warp byte ring fed by aligned 128-byte chunks of the payload.
+struct Ring {
+    uint8_t* buf;
+    uint64_t filled;  // absolute (payload-buffer) address up to which bytes are loaded
+    __device__ __forceinline__ void fill_to(const uint8_t* payload, uint64_t want, uint32_t lane) {
+        while (filled < want) {  // warp-uniform
+            uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(payload + filled) + lane);
+            *reinterpret_cast<uint32_t*>(buf + ((filled + 4 * lane) & (RING - 1))) = w;
+            filled += 128;
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ uint32_t byte(uint64_t a) const { return buf[a & (RING - 1)]; }
+};
+
+template <typename S, typename L>
+__global__ void __launch_bounds__(DEC_WPB * 32) k_rans_dec_v2(DecParams p) {
+    const uint32_t b = blockIdx.y;
+    const scz_info& in = p.info[b];
+    if (p.status[b] != SCZ_OK || in.version != 2 || in.sym_bytes != sizeof(S)) return;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t* rings = smem;                                        // DEC_WPB * RING
+    uint2* s_tab = reinterpret_cast<uint2*>(smem + DEC_WPB * RING); // A entries (if fits)
+    const uint32_t A = in.alphabet;
+    const int n = in.precision;
+    const uint32_t nslots = 1u << n;
+    const bool tab_smem = A <= TAB_SMEM_MAX;
+    L* lut = reinterpret_cast<L*>(smem + DEC_WPB * RING + (tab_smem ? A : 0) * sizeof(uint2));
+    const uint32_t* f = p.freqs + in.freqs_off;
+    const uint32_t* cum = p.cumtab + (uint64_t)b * (p.acap + 1);
+    if (tab_smem)
+        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) s_tab[i] = make_uint2(f[i], cum[i]);
+    if constexpr (sizeof(L) < 4) build_lut<L>(lut, cum, A, nslots);
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t blk = blockIdx.x * DEC_WPB + warp;
+    if (blk >= in.n_blocks) return;
+    const uint64_t Ls = 2 * in.nnz + in.n_rows;
+    const uint64_t base = (uint64_t)blk * in.block_syms;
+    const uint32_t len = (uint32_t)min((uint64_t)in.block_syms, Ls - base);
+    const uint32_t blen = p.block_bytes[in.blocks_off + blk];
+    const uint64_t a0 = in.payload_off + p.blk_off[(uint64_t)b * p.nblk_cap + blk];
+    Ring ring{rings + warp * RING, a0 & ~127ull};
+    ring.fill_to(p.payload, a0 + 128 + 64, lane);
+    uint32_t x = ring.byte(a0 + 4 * lane) | (ring.byte(a0 + 4 * lane + 1) << 8) |
+                 (ring.byte(a0 + 4 * lane + 2) << 16) | (ring.byte(a0 + 4 * lane + 3) << 24);
+    uint64_t cur = a0 + 128;
+    uint32_t pos = 128;
+    const uint32_t mask = nslots - 1;
+    const uint32_t ltm = lanemask_lt();
+    S* out = reinterpret_cast<S*>(p.dsym) + (uint64_t)b * p.dsym_stride + base;
+    const uint32_t steps = (len + 31) / 32;
+    bool bad = false;
+    for (uint32_t s = 0; s < steps; ++s) {
+        const uint32_t i = s * 32 + lane;
+        const bool active = i < len;
+        uint32_t cnt = 0, sym = 0;
+        if (active) {
+            const uint32_t slot = x & mask;
+            sym = lookup<L>(lut, cum, A, slot);
+            uint2 fc = tab_smem ? s_tab[sym] : make_uint2(f[sym], cum[sym]);
+            x = fc.x * (x >> n) + slot - fc.y;
+            cnt = (x < (1u << 15)) ? 2u : ((x < STATE_LOW) ? 1u : 0u);
+        }
+        const uint32_t b1 = __ballot_sync(0xffffffffu, cnt >= 1);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, cnt == 2);
+        const uint32_t tot = __popc(b1) + __popc(b2);
+        if (pos + tot > blen) {  // rans.py:203-205 underrun
+            bad = true;
+            break;
+        }
+        const uint64_t a = cur + __popc(b1 & ltm) + __popc(b2 & ltm);
+        if (cnt >= 1) x = (x << 8) | ring.byte(a);
+        if (cnt == 2) x = (x << 8) | ring.byte(a + 1);
+        cur += tot;
+        pos += tot;
+        if (active) out[i] = (S)sym;
+        ring.fill_to(p.payload, cur + 64, lane);
+    }
+    // rans.py:211-212: every lane back at L and every byte consumed
+    if (!bad) bad = __any_sync(0xffffffffu, x != STATE_LOW) || pos != blen;
+    if (bad && lane == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+}
+
+// v1 decode: one warp per tensor, the serial rans.decode loop (all lanes
+// carry the same state; lane 0 stores).  Generic lookup (binary search) when
+// the table does not fit a LUT.
+template <typename S, typename L>
+__global__ void __launch_bounds__(32) k_rans_dec_v1(DecParams p) {
+    const uint32_t b = blockIdx.x;
+    const scz_info& in = p.info[b];
+    if (p.status[b] != SCZ_OK || in.version != 1 || in.sym_bytes != sizeof(S)) return;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t* ringbuf = smem;
+    uint2* s_tab = reinterpret_cast<uint2*>(smem + RING);
+    const uint32_t A = in.alphabet;
+    const int n = in.precision;
+    const uint32_t nslots = 1u << n;
+    const bool tab_smem = A <= TAB_SMEM_MAX;
+    L* lut = reinterpret_cast<L*>(smem + RING + (tab_smem ? A : 0) * sizeof(uint2));
+    const uint32_t* f = p.freqs + in.freqs_off;
+    const uint32_t* cum = p.cumtab + (uint64_t)b * (p.acap + 1);
+    if (tab_smem)
+        for (uint32_t i = threadIdx.x; i < A; i += 32) s_tab[i] = make_uint2(f[i], cum[i]);
+    if constexpr (sizeof(L) < 4) build_lut<L>(lut, cum, A, nslots);
+    __syncwarp();
+    const uint32_t lane = threadIdx.x;
+    const uint64_t Ls = 2 * in.nnz + in.n_rows;
+    const uint64_t blen = in.payload_len;
+    const uint64_t a0 = in.payload_off;
+    Ring ring{ringbuf, a0 & ~127ull};
+    ring.fill_to(p.payload, a0 + 128, lane);
+    uint32_t x = ring.byte(a0) | (ring.byte(a0 + 1) << 8) | (ring.byte(a0 + 2) << 16) |
+                 (ring.byte(a0 + 3) << 24);
+    uint64_t pos = 4;
+    const uint32_t mask = nslots - 1;
+    S* out = reinterpret_cast<S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    bool bad = false;
+    for (uint64_t i = 0; i < Ls; ++i) {
+        const uint32_t slot = x & mask;
+        const uint32_t sym = lookup<L>(lut, cum, A, slot);
+        uint2 fc = tab_smem ? s_tab[sym] : make_uint2(f[sym], cum[sym]);
+        x = fc.x * (x >> n) + slot - fc.y;
+        while (x < STATE_LOW) {
+            if (pos >= blen) {
+                bad = true;
+                break;
+            }
+            x = (x << 8) | ring.byte(a0 + pos);
+            ++pos;
+        }
+        if (bad) break;
+        if (lane == 0) out[i] = (S)sym;
+        if (ring.filled < a0 + pos + 64) ring.fill_to(p.payload, a0 + pos + 64 + 256, lane);
+    }
+    if (!bad) bad = (x != STATE_LOW) || pos != blen;
+    if (bad && lane == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+}
+
+#define SCZ_INST_DEC(S, L)                                     \
+    template __global__ void k_rans_dec_v2<S, L>(DecParams);   \
+    template __global__ void k_rans_dec_v1<S, L>(DecParams);
+SCZ_INST_DEC(uint8_t, uint8_t)
+SCZ_INST_DEC(uint16_t, uint16_t)
+SCZ_INST_DEC(uint32_t, uint32_t)
+
+#define SCZ_INST_ENC(SRC)                                            \
+    template __global__ void k_rans_enc_v2<SRC>(EncParams, SRC);     \
+    template __global__ void k_rans_enc_v1<SRC>(EncParams, SRC);
+SCZ_INST_ENC(SplitSrc<uint8_t>)
+SCZ_INST_ENC(SplitSrc<uint16_t>)
+SCZ_INST_ENC(SplitSrc<uint32_t>)
+SCZ_INST_ENC(PlainSrc)
+
+}  // namespace scz

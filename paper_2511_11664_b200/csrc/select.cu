@@ -1,0 +1,401 @@
+// select.cu -- reshape search decision (Algorithm 1) and frequency tables.
+//
+//   k_select  one CTA per tensor.  For every feasible candidate N (descending,
+//             optimizer.py:72-75) it assembles the histogram of D = v ++ c ++ r
+//             from the value histogram, the folded column histogram and the
+//             row-count histogram, prices it as l_D * H (optimizer.py:87-96,
+//             rans.py:216-223 with numpy's pairwise summation order), replays
+//             the early-stopped scan (optimizer.py:129-138), then normalises
+//             the chosen histogram (rans.py:88-131) and builds the encoder
+//             table (freq, cum, exact reciprocal).
+//   k_normalize_only  stage entry point for rans.normalize_frequencies.
+#include "common.cuh"
+
+namespace scz {
+
+constexpr int SEL_THREADS = 256;
+
+struct SelectParams {
+    uint32_t n_cand;
+    uint32_t cand_k[MAX_CAND];
+    uint32_t cand_n[MAX_CAND];
+    uint32_t rhist_off[MAX_CAND];
+    uint32_t period;            // P (column histogram period)
+    const uint32_t* hp;
+    uint32_t hp_stride;
+    const uint32_t* rhist;
+    uint32_t rhist_stride;
+    const uint32_t* vhist;      // [B][256]
+    int q_bits;
+    int precision;
+    int searching;              // 1: Algorithm 1; 0: single explicit candidate
+    uint64_t total;
+    TensorState* state;
+    uint32_t* counts;           // scratch [B][acap]
+    double* terms;              // scratch [B][acap]
+    uint32_t acap;
+    uint32_t* freqs;            // out [B][acap]
+    uint32_t* cum;              // out [B][acap + 1]
+    EncTab* enctab;             // out [B][acap]
+    double* cand_out;           // optional out [B][MAX_CAND][2] (entropy, cost)
+    uint32_t* dump;             // optional out [B][n_cand][acap] histogram of D per candidate
+};
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src
+// pairwise_sum) of a[0..n): blocks of <= 128 with 8 accumulators, halves
+// rounded down to a multiple of 8 above that.  Serial, one thread.
+__device__ double pairwise_sum(const double* a, uint32_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (uint32_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        uint32_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    uint32_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
+}
+
+struct BlockScratch {
+    uint32_t scan[33];
+    uint32_t hist[256];
+    unsigned long long red64[SEL_THREADS / 32];
+    uint32_t red32[SEL_THREADS / 32];
+    uint64_t bcast64[4];
+    double costs[MAX_CAND];
+    double ents[MAX_CAND];
+    uint32_t alph[MAX_CAND];
+};
+
+__device__ unsigned long long block_sum64(unsigned long long v, BlockScratch& s) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s.red64[warp] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (int w = 0; w < SEL_THREADS / 32; ++w) t += s.red64[w];
+    __syncthreads();
+    return t;
+}
+
+__device__ uint32_t block_max32(uint32_t v, BlockScratch& s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s.red32[warp] = v;
+    __syncthreads();
+    uint32_t t = 0;
+    for (int w = 0; w < SEL_THREADS / 32; ++w) t = max(t, s.red32[w]);
+    __syncthreads();
+    return t;
+}
+
+// rans.py:88-131 normalize_frequencies over counts[0..A) by one CTA.
+// Returns an SCZ_* status (same for all threads).
+__device__ int block_normalize(const uint32_t* counts, uint32_t A, int precision,
+                               uint32_t* freqs, double* rem, uint32_t* cum, BlockScratch& s) {
+    unsigned long long total = 0, npresent = 0;
+    for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+        total += counts[i];
+        npresent += counts[i] > 0;
+    }
+    total = block_sum64(total, s);
+    npresent = block_sum64(npresent, s);
+    if (total == 0) return SCZ_NORMALIZE_ERROR;
+    if (precision < 1 || precision > 16) return SCZ_INVALID_INPUT;
+    const unsigned long long target = 1ull << precision;
+    if (npresent > target) return SCZ_PRECISION_TOO_SMALL;
+    const double ratio = __ddiv_rn((double)target, (double)total);
+    unsigned long long sumf = 0;
+    for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+        double ideal = __dmul_rn((double)counts[i], ratio);
+        double f = floor(ideal);
+        freqs[i] = (uint32_t)f;
+        rem[i] = __dsub_rn(ideal, f);
+        sumf += (unsigned long long)f;
+    }
+    sumf = block_sum64(sumf, s);
+    long long deficit = (long long)target - (long long)sumf;
+    if (deficit > 0) {
+        // np.lexsort((arange, -rem))[:deficit]: radix-select the deficit-th
+        // largest remainder (non-negative doubles order as their bits), then
+        // take ties in index order.
+        unsigned long long prefix = 0, pmask = 0;
+        unsigned long long k = (unsigned long long)deficit;
+        if (k >= A) {
+            for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) freqs[i] += 1;
+        } else {
+            for (int shift = 56; shift >= 0; shift -= 8) {
+                for (int i = threadIdx.x; i < 256; i += SEL_THREADS) s.hist[i] = 0;
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+                    unsigned long long key = (unsigned long long)__double_as_longlong(rem[i]);
+                    if ((key & pmask) == prefix) atomicAdd(&s.hist[(key >> shift) & 255], 1u);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    unsigned long long acc = 0;
+                    int d = 255;
+                    for (; d > 0; --d) {
+                        if (acc + s.hist[d] >= k) break;
+                        acc += s.hist[d];
+                    }
+                    s.bcast64[0] = prefix | ((unsigned long long)d << shift);
+                    s.bcast64[1] = k - acc;
+                }
+                __syncthreads();
+                prefix = s.bcast64[0];
+                k = s.bcast64[1];
+                pmask |= 0xFFull << shift;
+                __syncthreads();
+            }
+            // take every key > prefix, and the first k keys == prefix by index
+            uint32_t carry = 0;
+            for (uint32_t base = 0; base < A; base += SEL_THREADS) {
+                uint32_t i = base + threadIdx.x;
+                unsigned long long key =
+                    i < A ? (unsigned long long)__double_as_longlong(rem[i]) : 0ull;
+                uint32_t eq = (i < A && key == prefix) ? 1u : 0u;
+                uint32_t tot;
+                uint32_t ex = block_exclusive_scan<SEL_THREADS>(eq, s.scan, &tot);
+                if (i < A) {
+                    if (key > prefix || (eq && carry + ex < k)) freqs[i] += 1;
+                }
+                carry += tot;
+            }
+        }
+    }
+    __syncthreads();
+    unsigned long long sum2 = 0;
+    for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+        if (counts[i] > 0 && freqs[i] == 0) freqs[i] = 1;
+        sum2 += freqs[i];
+    }
+    sum2 = block_sum64(sum2, s);
+    long long surplus = (long long)sum2 - (long long)target;
+    while (surplus > 0) {
+        // argmax, first index on ties (np.argmax)
+        unsigned long long best = 0;
+        for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+            unsigned long long key = ((unsigned long long)freqs[i] << 32) | (0xffffffffu - i);
+            best = key > best ? key : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+            best = y > best ? y : best;
+        }
+        if ((threadIdx.x & 31) == 0) s.red64[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long bb = 0;
+            for (int w = 0; w < SEL_THREADS / 32; ++w) bb = s.red64[w] > bb ? s.red64[w] : bb;
+            s.bcast64[2] = bb;
+        }
+        __syncthreads();
+        unsigned long long bb = s.bcast64[2];
+        __syncthreads();
+        uint32_t idx = 0xffffffffu - (uint32_t)(bb & 0xffffffffu);
+        long long room = (long long)(bb >> 32) - 1;
+        long long cut = room < surplus ? room : surplus;
+        if (cut <= 0) return SCZ_PRECISION_TOO_SMALL;
+        if (threadIdx.x == 0) freqs[idx] -= (uint32_t)cut;
+        surplus -= cut;
+        __syncthreads();
+    }
+    // cdf (rans.py:130)
+    if (cum) {
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < A; base += SEL_THREADS) {
+            uint32_t i = base + threadIdx.x;
+            uint32_t v = i < A ? freqs[i] : 0;
+            uint32_t tot;
+            uint32_t ex = block_exclusive_scan<SEL_THREADS>(v, s.scan, &tot);
+            if (i < A) cum[i] = carry + ex;
+            carry += tot;
+        }
+        if (threadIdx.x == 0) cum[A] = carry;
+    }
+    __syncthreads();
+    return SCZ_OK;
+}
+
+// Histogram of D for candidate c into counts[0..acap); returns alphabet.
+__device__ uint32_t assemble_counts(const SelectParams& p, uint32_t b, uint32_t c,
+                                    uint32_t* counts, BlockScratch& s) {
+    const TensorState& st = p.state[b];
+    const uint32_t K = p.cand_k[c], N = p.cand_n[c];
+    const uint64_t nnz = st.nnz;
+    const uint32_t nv = 1u << p.q_bits;
+    const uint32_t ubound = max(nv, K + 1);
+    const uint32_t* vh = p.vhist + (uint64_t)b * 256;
+    const uint32_t* rh = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c];
+    for (uint32_t i = threadIdx.x; i < ubound; i += SEL_THREADS) {
+        uint32_t v = (i < nv) ? vh[i] : 0;
+        if (K == 1) {
+            if (i == 0) v += (uint32_t)(N - nnz) + (uint32_t)nnz;  // c = 0 for all, r = 0 rows
+            if (i == 1) v += (uint32_t)nnz;                      // r = 1 rows
+        } else if (i <= K) {
+            v += rh[i];
+        }
+        counts[i] = v;
+    }
+    __syncthreads();
+    if (K > 1) {
+        // column histogram: fold H_P (p mod P) onto p mod K
+        const uint32_t* hp = p.hp + (uint64_t)b * p.hp_stride;
+        const uint32_t P = p.period;
+        if (K <= SEL_THREADS) {
+            const uint32_t L = K * (SEL_THREADS / K);
+            if (threadIdx.x < L) {
+                uint32_t acc = 0;
+                for (uint32_t j = threadIdx.x; j < P; j += L) acc += hp[j];
+                if (acc) atomicAdd(&counts[threadIdx.x % K], acc);
+            }
+        } else {
+            for (uint32_t col = threadIdx.x; col < K; col += SEL_THREADS) {
+                uint32_t acc = 0;
+                for (uint32_t j = col; j < P; j += K) acc += hp[j];
+                counts[col] += acc;
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t last = 0;
+    for (uint32_t i = threadIdx.x; i < ubound; i += SEL_THREADS)
+        if (counts[i]) last = i + 1;
+    return block_max32(last, s);
+}
+
+// -(p log2 p).sum() over the positive counts, in numpy's order (rans.py:219-223).
+__device__ double block_entropy(const uint32_t* counts, uint32_t A, double total, double* terms,
+                                BlockScratch& s) {
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < A; base += SEL_THREADS) {
+        uint32_t i = base + threadIdx.x;
+        uint32_t c = i < A ? counts[i] : 0;
+        uint32_t tot;
+        uint32_t ex = block_exclusive_scan<SEL_THREADS>(c > 0 ? 1u : 0u, s.scan, &tot);
+        if (c > 0) {
+            double pp = __ddiv_rn((double)c, total);
+            terms[carry + ex] = __dmul_rn(pp, log2(pp));
+        }
+        carry += tot;
+    }
+    __syncthreads();
+    __shared__ double s_h;
+    if (threadIdx.x == 0) s_h = -pairwise_sum(terms, carry);
+    __syncthreads();
+    return s_h;
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
+    const uint32_t b = blockIdx.x;
+    TensorState& st = p.state[b];
+    if (st.status != SCZ_OK) return;
+    __shared__ BlockScratch s;
+    uint32_t* counts = p.counts + (uint64_t)b * p.acap;
+    double* terms = p.terms + (uint64_t)b * p.acap;
+    const uint64_t nnz = st.nnz;
+
+    uint32_t chosen = 0, flags = 0, evaluated = 0;
+    if (p.searching) {
+        for (uint32_t c = 0; c < p.n_cand; ++c) {
+            uint32_t A = assemble_counts(p, b, c, counts, s);
+            if (p.dump) {
+                uint32_t* dd = p.dump + ((uint64_t)b * p.n_cand + c) * p.acap;
+                for (uint32_t i = threadIdx.x; i < p.acap; i += SEL_THREADS) dd[i] = i < A ? counts[i] : 0;
+            }
+            uint64_t len = 2 * nnz + p.cand_n[c];
+            double h = block_entropy(counts, A, (double)len, terms, s);
+            if (threadIdx.x == 0) {
+                s.ents[c] = h;
+                s.costs[c] = __dmul_rn((double)len, h);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            // optimizer.py:116-138 replay; flag decisions that a 1e-12
+            // relative perturbation of either cost could flip.
+            double best = INFINITY, prev = INFINITY;
+            bool stopped = false;
+            auto near = [](double a, double bb) {
+                if (isinf(a) || isinf(bb)) return false;
+                if (a == 0.0 && bb == 0.0) return false;
+                return fabs(a - bb) <= 1e-12 * fmax(fabs(a), fabs(bb));
+            };
+            for (uint32_t c = 0; c < p.n_cand; ++c) {
+                double v = s.costs[c];
+                ++evaluated;
+                if (near(v, best) || near(v, prev)) flags |= SCZ_SEARCH_NEAR_TIE;
+                if (v < best) {
+                    best = v;
+                    chosen = c;
+                }
+                if (v > prev) {
+                    stopped = true;
+                    break;
+                }
+                prev = v;
+            }
+            if (stopped) flags |= SCZ_SEARCH_EARLY_STOPPED;
+            flags |= SCZ_SEARCH_USED;
+            if (p.cand_out) {
+                double* co = p.cand_out + (uint64_t)b * MAX_CAND * 2;
+                for (uint32_t c = 0; c < p.n_cand; ++c) {
+                    co[2 * c] = s.ents[c];
+                    co[2 * c + 1] = s.costs[c];
+                }
+            }
+            s.alph[0] = chosen;
+            s.alph[1] = flags;
+            s.alph[2] = evaluated;
+        }
+        __syncthreads();
+        chosen = s.alph[0];
+        flags = s.alph[1];
+        evaluated = s.alph[2];
+        __syncthreads();
+    }
+    // chosen candidate: histogram -> normalised table -> encoder table
+    uint32_t A = assemble_counts(p, b, chosen, counts, s);
+    uint32_t* freqs = p.freqs + (uint64_t)b * p.acap;
+    uint32_t* cum = p.cum + (uint64_t)b * (p.acap + 1);
+    int status = block_normalize(counts, A, p.precision, freqs, terms, cum, s);
+    EncTab* et = p.enctab + (uint64_t)b * p.acap;
+    if (status == SCZ_OK)
+        for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) make_enc_tab(freqs[i], cum[i], &et[i]);
+    if (threadIdx.x == 0) {
+        st.status = status;
+        st.cand_index = chosen;
+        st.n_rows = p.cand_n[chosen];
+        st.n_cols = p.cand_k[chosen];
+        st.alphabet = A;
+        st.stream_len = 2 * nnz + p.cand_n[chosen];
+        const uint32_t K = p.cand_k[chosen];
+        st.sym_bytes = K <= 255 ? 1u : (K <= 65535 ? 2u : 4u);
+        st.search_flags = flags;
+        st.n_evaluated = evaluated;
+    }
+}
+
+// Stage entry point: normalize_frequencies of an arbitrary count vector.
+__global__ void __launch_bounds__(SEL_THREADS) k_normalize_only(const uint32_t* counts, uint32_t A,
+                                                               int precision, uint32_t* freqs,
+                                                               double* rem, int32_t* status) {
+    __shared__ BlockScratch s;
+    int st = block_normalize(counts, A, precision, freqs, rem, nullptr, s);
+    if (threadIdx.x == 0) *status = st;
+}
+
+}  // namespace scz

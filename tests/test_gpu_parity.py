@@ -1,0 +1,410 @@
+"""GPU parity: the sm_100a path through the C-ABI against the reference's
+golden bytes and the CPU oracle (bit-exact for every integer / byte output,
+0-ulp for the fp32 reconstruction).  Mirrors the reference's own suite
+(pkg/tests/test_*.py) where it asserts known answers."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_2511_11664_b200 as sz
+from inputs import make_input
+from oracle import oracle as orc
+from paper_2511_11664_b200 import container, optimizer, rans, sparse, tensor
+from paper_2511_11664_b200.errors import (
+    AlphabetOverflow,
+    CorruptStream,
+    InvalidContainer,
+    InvalidInput,
+    NonDivisible,
+    NormalizeError,
+    PrecisionTooSmall,
+    UncodableSymbol,
+    UnsupportedVersion,
+)
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def tensor_of(spec):
+    return sz.FeatureTensor(tuple(spec["dims"]), make_input(spec))
+
+
+# ------------------------------------------------------------ containers
+def test_v1_containers_bit_exact_vs_reference_files(golden):
+    """compress() reproduces the reference's .scz bytes; decompress() its floats."""
+    for rec in golden["small"]:
+        spec = rec["spec"]
+        t = tensor_of(spec)
+        c = sz.compress(t, spec["q"], spec.get("n_rows"), spec.get("precision", 14))
+        raw = container.to_bytes(c)
+        want = open(os.path.join(GOLDEN, rec["file"]), "rb").read()
+        assert raw == want, spec
+        out = sz.decompress(container.from_bytes(want))
+        assert sha(out.data.tobytes()) == rec["output_sha"], spec
+
+
+def test_v1_baseline_configs_bit_exact(golden):
+    """BASELINE.json configs C1, C2 (VGG16, MobileNetV2), C5 (SwinT, DenseNet, Q=2..8)."""
+    for rec in golden["big"]:
+        spec = rec["spec"]
+        if spec.get("name") == "C4-llama2-7b":
+            continue
+        t = tensor_of(spec)
+        c = sz.compress(t, spec["q"])
+        assert c.n_rows == rec["n_rows"], spec["name"]
+        raw = container.to_bytes(c)
+        assert sha(raw) == rec["container_sha"], spec["name"]
+        out = sz.decompress(c)
+        assert sha(out.data.tobytes()) == rec["output_sha"], spec["name"]
+
+
+def test_v1_llama_hidden_state_c4(golden):
+    """C4: 1x2048x4096 signed dense, K=1, l_D = 25.2M symbols in one v1 stream."""
+    rec = next((r for r in golden["big"] if r["spec"].get("name") == "C4-llama2-7b"), None)
+    if rec is None:
+        pytest.skip("golden.json generated without --big")
+    t = tensor_of(rec["spec"])
+    c = sz.compress(t, 8, format=2)
+    assert c.n_rows == rec["n_rows"] and c.nnz == rec["nnz"]
+    out = sz.decompress(c)
+    assert sha(out.data.tobytes()) == rec["output_sha"]
+    c1 = sz.compress(t, 8)
+    assert sha(container.to_bytes(c1)) == rec["container_sha"]
+
+
+def test_v2_containers_match_oracle(golden):
+    for rec in golden["small"] + golden["big"]:
+        spec = rec["spec"]
+        if spec.get("name") == "C4-llama2-7b":
+            continue
+        t = tensor_of(spec)
+        for bs in (64, 8192):
+            c = sz.compress(t, spec["q"], spec.get("n_rows"), spec.get("precision", 14),
+                            format=2, block_syms=bs)
+            ref = orc.compress(t.data, t.dims, spec["q"], rec["n_rows"], spec.get("precision", 14),
+                               fmt=2, lanes=32, block_syms=bs)
+            assert container.to_bytes(c) == orc.to_bytes(ref), (spec, bs)
+            back = container.from_bytes(container.to_bytes(c))
+            out = sz.decompress(back)
+            assert sha(out.data.tobytes()) == rec["output_sha"], (spec, bs)
+
+
+def test_v2_lanes_are_reference_streams(golden):
+    """Each lane of a v2 block is exactly rans.encode of its subsequence (reference pins)."""
+    for rec in golden["big"][:3]:
+        spec = rec["spec"]
+        t = tensor_of(spec)
+        pins = rec["v2_lane_pins"]
+        W, B = pins["lanes"], pins["block_syms"]
+        p = tensor.params_for(t, spec["q"])
+        q = tensor.quantize_reshape(t, p, rec["n_rows"])
+        d = sparse.concat(sparse.csr_encode(q))
+        table = rans.normalize_frequencies(rans.build_counts(d, int(d.data.max()) + 1), 14)
+        for b, j, h in pins["pins"]:
+            sub = d.data[b * B:(b + 1) * B][j::W]
+            assert sha(rans.encode(sub, table).data) == h
+
+
+# ----------------------------------------------------------- stage parity
+def test_quantize_kat_and_edge_values(golden):
+    for row in golden["kat"]["quantize"]:
+        x = np.array(row["x"], np.uint32).view(np.float32)
+        t = sz.FeatureTensor((x.size,), x)
+        p = tensor.params_for(t, row["q"])
+        assert p.scale.hex() == row["scale"] and p.zero_point == row["z"]
+        q, m = tensor.quantize(t, p)
+        assert q.tolist() == row["sym"] and m.tolist() == row["mask"]
+        out = tensor.dequantize(sz.QuantizedMatrix(1, x.size, q, m), p, (x.size,))
+        assert out.data.view(np.uint32).tolist() == row["deq"]
+    # test_tensor.py:64-87
+    q, m = tensor.quantize(sz.FeatureTensor((1,), np.array([3.26], np.float32)),
+                           sz.QuantParams(4, 0.5, 0, 0.0, 7.5))
+    assert q[0] == 7 and not m[0]
+    q, m = tensor.quantize(sz.FeatureTensor((1,), np.array([0.0], np.float32)),
+                           sz.QuantParams(4, 0.5, 3, -1.5, 6.0))
+    assert q[0] == 3 and m[0]
+    vals = np.array([-1e6, -0.8, 0.0, 0.7, 1e6], np.float32)
+    q, _ = tensor.quantize(sz.FeatureTensor((5,), vals), sz.QuantParams(4, 0.1, 8, -0.8, 0.7))
+    assert q.max() <= 15
+
+
+def test_quantize_matches_oracle_random():
+    """fp32 guard band + fp64 fix-up == the reference's fp64 sequence, incl.
+    values planted on and one ulp around every rounding boundary."""
+    rng = np.random.default_rng(1)
+    for trial in range(24):
+        q_bits = 2 + trial % 7
+        n = int(rng.integers(1, 300_000))
+        x = (rng.laplace(0, 1, n) * rng.choice([1e-3, 1, 1e3])).astype(np.float32)
+        if trial % 3 == 0:
+            x = np.abs(x)
+        x[rng.random(n) < 0.3] = 0.0
+        x[rng.random(n) < 0.01] = -0.0
+        s, z = orc.params_for(x, q_bits)
+        k = rng.integers(0, (1 << q_bits) - 1, min(n, 5000))
+        planted = ((k + 0.5 - z) * s).astype(np.float32)
+        idx = rng.integers(0, n, planted.size)
+        x[idx] = np.nextafter(planted, planted + rng.choice([-1, 0, 1], planted.size).astype(np.float32))
+        t = sz.FeatureTensor((n,), x)
+        p = tensor.params_for(t, q_bits)
+        s, z = orc.params_for(x, q_bits)
+        assert (p.scale, p.zero_point) == (s, z)
+        q, m = tensor.quantize(t, p)
+        qo, mo = orc.quantize(x, s, z, q_bits)
+        assert np.array_equal(q, qo) and np.array_equal(m, mo)
+        out = tensor.dequantize(sz.QuantizedMatrix(1, n, q, m), p, (n,))
+        assert np.array_equal(out.data.view(np.uint32), orc.dequantize(qo, mo, s, z).view(np.uint32))
+
+
+def test_csr_kat_and_corruption():
+    # test_sparse.py:38-101
+    q = sz.QuantizedMatrix(2, 3, [0, 5, 0, 3, 0, 2], [True, False, True, False, True, False])
+    s = sparse.csr_encode(q)
+    assert s.values.tolist() == [5, 3, 2] and s.col_idx.tolist() == [1, 0, 2]
+    assert s.row_counts.tolist() == [1, 2]
+    back = sparse.csr_decode(s, 2, 3)
+    assert back.data.tolist() == [0, 5, 0, 3, 0, 2]
+    assert back.zero_mask.tolist() == [True, False, True, False, True, False]
+    e = sparse.csr_encode(sz.QuantizedMatrix(2, 3, np.zeros(6), np.ones(6, bool)))
+    assert e.values.size == 0 and e.row_counts.tolist() == [0, 0]
+    assert sparse.csr_encode(sz.QuantizedMatrix(1, 2, [0, 3], [False, False])).values.tolist() == [0, 3]
+    for bad in (sz.SparseCSR([1, 2, 3], [0, 1, 0], [2, 2]), sz.SparseCSR([1], [5], [1, 0]),
+                sz.SparseCSR([1, 2], [1, 1], [2, 0]), sz.SparseCSR([1], [0], [1])):
+        with pytest.raises(CorruptStream):
+            sparse.csr_decode(bad, 2, 3)
+
+
+def test_csr_matches_oracle_random():
+    rng = np.random.default_rng(2)
+    for _ in range(40):
+        n, k = int(rng.integers(1, 400)), int(rng.integers(1, 300))
+        qv = rng.integers(0, 256, n * k).astype(np.uint32)
+        mask = rng.random(n * k) < rng.uniform(0, 1)
+        s = sparse.csr_encode(sz.QuantizedMatrix(n, k, qv, mask))
+        d, nnz = orc.csr_concat(qv, mask, n)
+        assert np.array_equal(sparse.concat(s).data, d)
+        back = sparse.csr_decode(s, n, k)
+        qo, mo = orc.csr_decode(d, nnz, n, k)
+        assert np.array_equal(back.data, qo) and np.array_equal(back.zero_mask, mo)
+
+
+def test_counts_and_normalize(golden):
+    assert rans.build_counts([5, 3, 2, 1, 0, 2, 1, 2], 6).tolist() == [1, 2, 3, 1, 0, 1]
+    assert rans.build_counts([], 4).tolist() == [0, 0, 0, 0]
+    with pytest.raises(AlphabetOverflow):
+        rans.build_counts([0, 7], 6)
+    t = rans.normalize_frequencies([1, 2, 3, 1, 0, 1], 4)
+    assert t.freqs.tolist() == [2, 4, 6, 2, 0, 2] and t.cdf.tolist() == [0, 2, 6, 12, 14, 14, 16]
+    assert rans.normalize_frequencies([7], 4).freqs.tolist() == [16]
+    with pytest.raises(PrecisionTooSmall):
+        rans.normalize_frequencies([1, 1, 1], 1)
+    with pytest.raises(PrecisionTooSmall):
+        rans.normalize_frequencies([1] * 300, 8)
+    with pytest.raises(NormalizeError):
+        rans.normalize_frequencies([0, 0, 0, 0], 10)
+    for row in golden["kat"]["normalize"]:
+        if isinstance(row["freqs"], str):
+            with pytest.raises(PrecisionTooSmall):
+                rans.normalize_frequencies(row["counts"], row["precision"])
+        else:
+            got = rans.normalize_frequencies(row["counts"], row["precision"]).freqs.tolist()
+            assert got == row["freqs"]
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        a = int(rng.integers(1, 3000))
+        counts = rng.integers(0, 2000, a) ** int(rng.integers(1, 3))
+        counts[rng.random(a) < 0.3] = 0
+        if counts.sum() == 0:
+            continue
+        prec = int(rng.integers(8, 17))
+        try:
+            want = orc.normalize_frequencies(counts, prec).tolist()
+        except orc.OracleError:
+            with pytest.raises(PrecisionTooSmall):
+                rans.normalize_frequencies(counts, prec)
+            continue
+        assert rans.normalize_frequencies(counts, prec).freqs.tolist() == want
+
+
+def test_rans_streams_match_reference(golden):
+    for row in golden["kat"]["rans"]:
+        d = np.array(row["d"], np.uint32)
+        t = rans.FrequencyTable.from_freqs(row["freqs"], row["precision"])
+        b = rans.encode(d, t)
+        assert b.data.hex() == row["payload"]
+        assert rans.decode(b, t, d.size).tolist() == row["d"]
+
+
+def test_rans_kat_and_errors():
+    # test_rans.py:101-157
+    assert rans.encode_step(8388608, freq=6, cum=10, precision=4) == (22369628, [])
+    t = rans.FrequencyTable.from_freqs([10, 6], 4)
+    assert rans.decode_step(22369628, t) == (8388608, 1)
+    d = [0] * 50
+    t = rans.normalize_frequencies(rans.build_counts(d, 1), 14)
+    b = rans.encode(d, t)
+    assert len(b.data) == 4 and rans.decode(b, t, 50).tolist() == d
+    t0 = rans.FrequencyTable.from_freqs([256], 8)
+    assert rans.decode(rans.encode([], t0), t0, 0).size == 0
+    rng = np.random.default_rng(0)
+    d = rng.integers(0, 16, 500)
+    t = rans.normalize_frequencies(rans.build_counts(d, 16), 14)
+    b = rans.encode(d, t)
+    for bad in (b.data[:-1], b.data[:2], b.data + b"\x00"):
+        with pytest.raises(CorruptStream):
+            rans.decode(rans.Bitstream(bad), t, 500)
+    with pytest.raises(UncodableSymbol):
+        rans.encode([1], rans.FrequencyTable.from_freqs([128, 0, 128], 8))
+    with pytest.raises(AlphabetOverflow):
+        rans.encode([2], rans.FrequencyTable.from_freqs([128, 128], 8))
+
+
+def test_rans_random_vs_oracle_all_precisions():
+    rng = np.random.default_rng(4)
+    for trial in range(60):
+        prec = 8 + trial % 9
+        a = int(rng.integers(1, 300 if trial % 5 else 5000))
+        n = int(rng.integers(1, 40_000))
+        w = rng.random(a) ** 3
+        d = rng.choice(a, size=n, p=w / w.sum()).astype(np.uint32)
+        counts = np.bincount(d, minlength=a)
+        try:
+            f = orc.normalize_frequencies(counts, prec)
+        except orc.OracleError:
+            continue
+        t = rans.FrequencyTable.from_freqs(f, prec)
+        b = rans.encode(d, t)
+        assert b.data == orc.rans_encode(d, f, prec)
+        assert np.array_equal(rans.decode(b, t, n), d)
+        if prec <= 16:
+            payload, bb = rans.encode_lanes(d, t, 32, 32 * (1 + trial % 9))
+            want, wbb = orc.rans_encode_v2(d, f, prec, 32, 32 * (1 + trial % 9))
+            assert payload == want and bb.tolist() == wbb.tolist()
+            back = rans.decode_lanes(payload, bb, t, n, 32, 32 * (1 + trial % 9))
+            assert np.array_equal(back, d)
+
+
+def test_search_reports_match_reference(golden):
+    """optimizer.search / exhaustive_search: same N, candidates and entropy floats."""
+    for rec in golden["small"] + golden["big"]:
+        if "search" not in rec:
+            continue
+        t = tensor_of(rec["spec"])
+        n, rep = optimizer.search(t, rec["spec"]["q"])
+        want = rec["search"]
+        assert n == want["chosen"] and rep.early_stopped == want["early_stopped"]
+        got = [[c.n_rows, c.n_cols, c.nnz, c.stream_len, c.entropy_bits, c.t_tot]
+               for c in rep.candidates]
+        assert got == want["candidates"], rec["spec"]
+        if "exhaustive" in rec:
+            n, rep = optimizer.exhaustive_search(t, rec["spec"]["q"])
+            assert n == rec["exhaustive"]["chosen"]
+            assert [[c.n_rows, c.entropy_bits, c.t_tot] for c in rep.candidates] == \
+                rec["exhaustive"]["candidates"]
+
+
+def test_cost_on_infeasible_reshapes():
+    # test_optimizer.py:58-63 trend + explicit N outside the search window
+    t = sz.gen_synthetic("relu-laplace", [128, 28, 28], 0.9, 42)
+    ent = [optimizer.cost(t, n, 4).entropy_bits for n in (784, 1792, 6272, 14336)]
+    assert all(a > b for a, b in zip(ent, ent[1:]))
+    x = t.data
+    s, z = orc.params_for(x, 4)
+    q, m = orc.quantize(x, s, z, 4)
+    for n in (784, 1792, 6272, 14336):
+        counts, _ = orc.stream_counts(q, m, n, 4)
+        assert optimizer.cost(t, n, 4).entropy_bits == orc.entropy(counts)
+    with pytest.raises(NonDivisible):
+        optimizer.cost(sz.gen_synthetic("uniform", [4, 4], 0.0, 0), 5, 4)
+
+
+def test_device_search_decision_matches_reference(golden):
+    """The compress() path decides N on the device (fp64 entropy, numpy
+    summation order); it must agree with the reference's choice."""
+    for rec in golden["small"] + golden["big"]:
+        if "search" not in rec or rec["spec"].get("name") == "C4-llama2-7b":
+            continue
+        rows, chosen, chosen_ex, flags = optimizer.device_histograms(tensor_of(rec["spec"]),
+                                                                     rec["spec"]["q"])
+        assert rows[chosen][0] == rec["search"]["chosen"], rec["spec"]
+
+
+# ------------------------------------------------------------ error paths
+def test_container_error_classes(golden):
+    for case in golden["errors"]:
+        blob = bytes.fromhex(case["blob"])
+        try:
+            container.decompress(container.from_bytes(blob))
+            got = None
+        except (sz.SczipError, ValueError) as e:
+            got = type(e).__name__
+        assert got == case["error"], case["name"]
+
+
+def test_compress_argument_errors():
+    t = sz.gen_synthetic("relu-laplace", [8, 8, 8], 0.8, 21)
+    with pytest.raises(NonDivisible):
+        sz.compress(t, 4, n_rows=7)
+    with pytest.raises(InvalidInput):
+        sz.compress(t, 4, precision=16)
+    with pytest.raises(InvalidInput):
+        sz.compress(t, 9)
+    c = sz.compress(t, 4)
+    bad = container.Container(c.q_bits, c.precision, c.dims, c.n_rows, c.n_cols + 1, c.nnz,
+                              c.scale, c.zero_point, c.freqs, c.payload)
+    with pytest.raises(InvalidContainer):
+        sz.decompress(bad)
+    bad = container.Container(c.q_bits, c.precision, c.dims, c.n_rows, c.n_cols, c.nnz,
+                              c.scale, c.zero_point, c.freqs, c.payload[:-2])
+    with pytest.raises(CorruptStream):
+        sz.decompress(bad)
+    with pytest.raises(UnsupportedVersion):
+        sz.decompress(container.Container(c.q_bits, c.precision, c.dims, c.n_rows, c.n_cols,
+                                          c.nnz, c.scale, c.zero_point, c.freqs, c.payload, 7))
+
+
+def test_v2_corruption_detected():
+    t = sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5, 3)
+    c = sz.compress(t, 8, format=2, block_syms=1024)
+    raw = bytearray(container.to_bytes(c))
+    for pos in (len(raw) - 1, len(raw) - 700, len(raw) - 3000):
+        bad = bytearray(raw)
+        bad[pos] ^= 0x5A
+        with pytest.raises(CorruptStream):
+            container.decompress(container.from_bytes(bytes(bad)))
+
+
+# ------------------------------------------------------- random round trips
+def test_random_round_trips_vs_oracle():
+    """Acceptance-style (test_acceptance.py:44-62): random (T, Q, N), both formats."""
+    rng = np.random.default_rng(7)
+    for i in range(120):
+        total = int(rng.integers(1, 5000))
+        divs = orc.divisors(total)
+        n_rows = None if i % 3 == 0 else int(divs[rng.integers(0, len(divs))])
+        q = int(rng.integers(2, 9))
+        x = np.abs(rng.laplace(0, 1, total)).astype(np.float32)
+        x[rng.random(total) < rng.uniform(0.0, 0.97)] = 0.0
+        if i % 7 == 0:
+            x = -x
+        t = sz.FeatureTensor((total,), x)
+        fmt = 1 + i % 2
+        try:
+            ref = orc.compress(x, (total,), q, n_rows, 14, fmt=fmt, lanes=32, block_syms=256)
+        except orc.OracleError as e:
+            assert e.status == orc.PRECISION_TOO_SMALL
+            with pytest.raises(PrecisionTooSmall):
+                sz.compress(t, q, n_rows, format=fmt, block_syms=256)
+            continue
+        c = sz.compress(t, q, n_rows, format=fmt, block_syms=256)
+        assert container.to_bytes(c) == orc.to_bytes(ref), (i, total, q, n_rows, fmt)
+        out = sz.decompress(c)
+        assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32))
