@@ -1,0 +1,493 @@
+#!/usr/bin/env python
+"""Benchmark: batched quantise + reshape-search + CSR + rANS round trip on B200.
+
+Workload (BASELINE.json configs[1]): VGG16 split-point features, batch 256 of
+(1, 256, 56, 56) post-ReLU Laplace tensors at sparsity 0.5, seeds
+rank*256 .. rank*256+255, Q = 8, precision 14, N chosen by Algorithm 1 on the
+device, container format v2 (FORMAT.md: W = 32 lanes, 8192-symbol blocks).
+
+A step = compress the batch + decompress it.  Metric: GB/s of
+fp32 features through encode+decode = 4*T*batch / step time, whole job.
+
+  value  device-resident step (inputs in HBM; 822 MB per rank, larger than
+         L2, so no flush is needed); timed with CUDA events on the library's
+         stream, max over ranks.
+  e2e    the same through the C-ABI host-buffer entry points
+         (scz_compress_batch / scz_decompress_batch): pinned host features in,
+         host containers out, host containers in, host features out.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: one process per GPU under torchrun; every rank codes its own 256
+tensors (weak scaling, no collective on the data path; the barrier and the
+max-over-ranks reduction of the timings use NCCL).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rANS encode+decode GB/s of fp32 features & p50 latency/tensor; bytes/element"
+UNIT = "GB/s"
+WORKLOADS = {
+    "vgg16": dict(dims=(1, 256, 56, 56), kind="relu-laplace", sparsity=0.5, q=8,
+                  name="VGG16 split-point features 1x256x56x56 post-ReLU sparsity 0.5, 8-bit"),
+    "mobilenetv2": dict(dims=(1, 64, 14, 14), kind="signed", sparsity=0.0, q=8,
+                        name="MobileNetV2 features[10] 1x64x14x14 signed Laplace, 8-bit"),
+    "resnet50": dict(dims=(1, 512, 28, 28), kind="relu-laplace", sparsity=0.5, q=8,
+                     name="ResNet-50 layer2 1x512x28x28 post-ReLU sparsity 0.5, 8-bit"),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--format", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--block-syms", type=int, default=8192)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="bounded CPU-baseline sample (rank 0, N=1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip v1 / latency side measurements")
+    return ap.parse_args()
+
+
+def make_batch(wl, batch, seed0):
+    from paper_2511_11664_b200.synth import make_input
+
+    T = int(np.prod(wl["dims"]))
+    out = np.empty((batch, T), np.float32)
+    for i in range(batch):
+        out[i] = make_input(dict(kind=wl["kind"], dims=wl["dims"], sparsity=wl["sparsity"],
+                                 seed=seed0 + i))
+    return out
+
+
+# ------------------------------------------------------------ CPU baseline
+def _cpu_worker(args):
+    wl_key, seed, fmt = args
+    from oracle import oracle as orc
+    from paper_2511_11664_b200.synth import make_input
+
+    wl = WORKLOADS[wl_key]
+    x = make_input(dict(kind=wl["kind"], dims=wl["dims"], sparsity=wl["sparsity"], seed=seed))
+    t0 = time.perf_counter()
+    c = orc.compress(x, wl["dims"], wl["q"], None, 14, fmt=fmt)
+    out = orc.decompress(c)
+    dt = time.perf_counter() - t0
+    assert out.size == x.size
+    return dt, len(orc.to_bytes(c))
+
+
+def cpu_baseline(wl_key, seconds, processes=None, fmt=1):
+    """The oracle port (oracle/: the reference's algorithm in C + numpy) on the
+    host cores: compress (with Algorithm 1) + decompress one tensor per task,
+    one task per process, for ~`seconds` of wall time."""
+    import multiprocessing as mp
+
+    wl = WORKLOADS[wl_key]
+    T = int(np.prod(wl["dims"]))
+    cores = processes or len(os.sched_getaffinity(0))
+    ctx = mp.get_context("fork")
+    done, per_task = 0, []
+    t_start = time.perf_counter()
+    seed = 0
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, [(wl_key, 10_000 + i, fmt) for i in range(cores)])  # warm-up
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < seconds or done == 0:
+            res = pool.map(_cpu_worker, [(wl_key, seed + i, fmt) for i in range(cores)])
+            seed += cores
+            done += len(res)
+            per_task += [r[0] for r in res]
+        wall = time.perf_counter() - t_start
+    gbs = 4.0 * T * done / wall / 1e9
+    return dict(value=gbs, unit=UNIT, cores=cores, kind="port",
+                sample=f"{done} tensors of {wl['name']} (compress incl. Algorithm 1 + decompress, "
+                       f"format v{fmt}) on {cores} processes, {wall:.1f} s wall; "
+                       f"per-tensor p50 {statistics.median(per_task) * 1e3:.1f} ms"), per_task
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = WORKLOADS[args.workload]
+    T = int(np.prod(wl["dims"]))
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    pool = mp.get_context("fork").Pool(cores)
+    seed = 0
+    times, per_task = [], []
+    for step in range(args.warmup + args.steps):
+        tasks = [(args.workload, seed + i, 1) for i in range(cores)]
+        seed += cores
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, tasks)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            per_task += [r[0] for r in res]
+    pool.close()
+    total = sum(times)
+    value = 4.0 * T * cores * len(times) / total / 1e9
+    line = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=args.gpus,
+                steps=args.steps, warmup=args.warmup, ms_per_step=1e3 * total / len(times),
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64/u32",
+                data="synthetic",
+                config=dict(workload=wl["name"], global_batch=cores, q_bits=wl["q"],
+                            format="v1 (reference wire format)", precision=14),
+                cpu_baseline=dict(value=value, unit=UNIT, cores=cores, kind="port",
+                                  sample=f"each step: {cores} tensors (one per host process), "
+                                         "oracle C/numpy port of sczip compress+decompress; "
+                                         f"per-tensor p50 {statistics.median(per_task) * 1e3:.1f} ms"),
+                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=[], samples=0)
+        return dict(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons),
+                    samples=len(sm))
+
+
+# -------------------------------------------------------------- our arm
+def algorithmic_bytes(name, infos, T, nblk_bytes):
+    """Bytes a kernel must move per launch, batch-summed."""
+    nnz = sum(int(i["nnz"]) for i in infos)
+    N = sum(int(i["n_rows"]) for i in infos)
+    S = sum(int(i["payload_len"]) for i in infos)
+    B = len(infos)
+    w = max(int(i["sym_bytes"]) for i in infos)
+    L = 2 * nnz + N
+    return {
+        "k_stats": 4 * T * B + T * B // 8,
+        "k_quantize": 4 * T * B + T * B // 8 + nnz,
+        "k_colhist": T * B // 8,
+        "k_materialize": T * B // 8 + (nnz + N) * w,
+        "k_rans_enc_v2": nnz + (nnz + N) * w + S,
+        "k_rans_enc_v1": nnz + (nnz + N) * w + S,
+        "k_pack": 2 * S,
+        "k_rans_dec_v2": S + L * w,
+        "k_rans_dec_v1": S + L * w,
+        "k_row_sums": N * w,
+        "k_rows_out": L * w + 4 * T * B,
+    }.get(name)
+
+
+def run_ours(args):
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2511_11664_b200 import _native
+
+    wl = WORKLOADS[args.workload]
+    T = int(np.prod(wl["dims"]))
+    B = args.batch
+    ctx = _native.context(local)
+    lib = ctx.lib
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    host = torch.empty((B, T), dtype=torch.float32).pin_memory()
+    host.numpy()[:] = make_batch(wl, B, rank * B)
+    x_dev = host.cuda(local)
+    out_dev = torch.empty_like(x_dev)
+    torch.cuda.synchronize()
+
+    batch = _native.Batch()
+    h_info = (_native.Info * B)()
+
+    def device_step(fmt=args.format):
+        ctx.check(lib.scz_encode_batch(ctx.h, ctypes.c_void_p(x_dev.data_ptr()), T, B, wl["q"], -1, 14,
+                                       fmt, 32, args.block_syms, ctypes.byref(batch)))
+        ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), h_info))
+        ctx.check(lib.scz_decode_batch_async(ctx.h, h_info, B, ctypes.c_void_p(batch.d_freqs),
+                                             ctypes.c_void_p(batch.d_block_bytes),
+                                             ctypes.c_void_p(batch.d_payload),
+                                             ctypes.c_void_p(out_dev.data_ptr())))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timed region -------------------------------------
+    for _ in range(args.warmup):
+        device_step()
+    barrier()
+    ctx.set_timing(True)
+    ctx.read_timing()
+    l0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            device_step()
+        ev1.record(stream)
+        barrier()
+    launches = ctx.launches - l0
+    kt = ctx.read_timing()
+    ctx.set_timing(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms)
+    value = 4.0 * T * B * world / (ms * 1e-3) / 1e9
+
+    status = (ctypes.c_int32 * B)()
+    ctx.check(lib.scz_decode_status(ctx.h, B, status))
+    infos = [{f: getattr(h_info[i], f) for f, _ in _native.Info._fields_} for i in range(B)]
+    assert all(s == 0 for s in status) and all(i["status"] == 0 for i in infos), "device status"
+    # every reconstruction within the quantisation bound, zeros exact (tensor.py:143-156)
+    scales = torch.tensor([i["scale"] for i in infos], device=x_dev.device, dtype=torch.float32)
+    err = (out_dev - x_dev).abs().amax(dim=1)
+    assert bool((err <= scales * 1.0001 + 1e-6).all()), "reconstruction outside the quantisation bound"
+    assert bool((out_dev[x_dev == 0] == 0).all())
+    total_bytes = sum(i["payload_len"] + 60 + 4 * len(wl["dims"]) + 2 * i["alphabet"] +
+                      (12 + 4 * i["n_blocks"] if args.format == 2 else 0) for i in infos)
+    bpe = total_bytes / (T * B)
+
+    # ---- roofline of the dominant kernel ----------------------------------
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak = float(json.load(open(peaks_path))["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    dom = max(kt.items(), key=lambda kv: kv[1][0]) if kt else None
+    roofline = None
+    kernel_share = {}
+    if dom:
+        step_ms_sum = sum(v[0] for v in kt.values())
+        kernel_share = {k: round(v[0] / step_ms_sum, 4) for k, v in sorted(kt.items(), key=lambda kv: -kv[1][0])}
+        name, (tot_ms, n) = dom
+        per_launch_ms = tot_ms / n
+        launches_per_step = n / args.steps
+        ab = algorithmic_bytes(name, infos, T, None)
+        achieved = (ab / launches_per_step) / (per_launch_ms * 1e-3) / 1e9 if ab else None
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            traffic = json.load(open(prof)).get(name)
+        roofline = dict(kernel=name, bound="hbm", achieved=achieved, peak=peak, unit="GB/s",
+                        frac=(achieved / peak) if achieved else None, traffic=traffic,
+                        algorithmic_bytes_per_launch=(ab / launches_per_step) if ab else None,
+                        launch_ms=per_launch_ms, peak_source=peak_src)
+    pipe_bytes = 8 * T * B + 2 * total_bytes
+    pipeline_roofline = dict(achieved=pipe_bytes / (ms * 1e-3) / 1e9, peak=peak, unit="GB/s",
+                             frac=pipe_bytes / (ms * 1e-3) / 1e9 / peak,
+                             bytes_per_step="8*T*batch + 2*container bytes")
+
+    # ---- e2e through the host-buffer C-ABI ---------------------------------
+    infos_p = ctypes.POINTER(_native.Info)()
+    pay_p = ctypes.POINTER(ctypes.c_uint8)()
+    fr_p = ctypes.POINTER(ctypes.c_uint32)()
+    bl_p = ctypes.POINTER(ctypes.c_uint32)()
+    sizes = (ctypes.c_uint64 * 3)()
+    h_out = torch.empty((B, T), dtype=torch.float32).pin_memory()
+    e2e_status = (ctypes.c_int32 * B)()
+    io = {}
+
+    def e2e_step():
+        ctx.check(lib.scz_compress_batch(ctx.h, ctypes.c_void_p(host.data_ptr()), T, B, wl["q"], -1, 14,
+                                         args.format, 32, args.block_syms, ctypes.byref(infos_p),
+                                         ctypes.byref(pay_p), ctypes.byref(fr_p), ctypes.byref(bl_p),
+                                         sizes))
+        ctx.check(lib.scz_decompress_batch(ctx.h, infos_p, B, fr_p, sizes[1], bl_p, sizes[2], pay_p,
+                                           sizes[0], ctypes.c_void_p(h_out.data_ptr()), e2e_status))
+        io["h2d"] = 4 * T * B + sizes[0] + 4 * sizes[1] + 4 * sizes[2]
+        io["d2h"] = B * ctypes.sizeof(_native.Info) + sizes[0] + 4 * sizes[1] + 4 * sizes[2] + 4 * T * B + 4 * B
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    e2e_value = 4.0 * T * B * world / (e2e_ms * 1e-3) / 1e9
+    assert all(s == 0 for s in e2e_status)
+    assert torch.equal(h_out, out_dev.cpu()), "host-path reconstruction differs from device path"
+
+    extras = {}
+    if not args.no_extras and rank == 0:
+        extras = side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, _ = cpu_baseline(args.workload, args.cpu_seconds)
+
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
+            warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling="weak",
+            vs_baseline=None, dtype="u8/u32 (fp32 in/out, fp64 quant params)", data="synthetic",
+            config=dict(workload=wl["name"], global_batch=B * world, per_gpu_batch=B, q_bits=wl["q"],
+                        precision=14, format=f"v{args.format}", lanes=32,
+                        block_syms=args.block_syms, reshape="Algorithm 1 on device",
+                        parallelism=f"dp{world} (independent tensors, no collective)",
+                        l2="inputs 822 MB per rank > 126 MB L2 (no flush needed)"),
+            bytes_per_element=bpe,
+            e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=io["h2d"],
+                     d2h_bytes_per_step=io["d2h"], ms_per_step=e2e_ms,
+                     path="scz_compress_batch + scz_decompress_batch, pinned host buffers"),
+            roofline=roofline, pipeline_roofline=pipeline_roofline, kernel_share=kernel_share,
+            gpu_launches=launches, clocks=clocks.summary(), cpu_baseline=cpu, **extras)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
+    """Per-tensor p50 latency (B = 1, device resident) and the v1 (reference
+    wire format) batch throughput."""
+    from paper_2511_11664_b200 import _native
+
+    res = {}
+    batch = _native.Batch()
+    info1 = (_native.Info * 1)()
+    x0 = ctypes.c_void_p(x_dev[0].data_ptr())
+    o0 = ctypes.c_void_p(out_dev[0].data_ptr())
+    lat_enc, lat_dec = [], []
+    for it in range(30):
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        ctx.check(lib.scz_encode_batch(ctx.h, x0, T, 1, wl["q"], -1, 14, 2, 32, args.block_syms,
+                                       ctypes.byref(batch)))
+        ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), info1))
+        b.record(stream)
+        ctx.check(lib.scz_decode_batch_async(ctx.h, info1, 1, ctypes.c_void_p(batch.d_freqs),
+                                             ctypes.c_void_p(batch.d_block_bytes),
+                                             ctypes.c_void_p(batch.d_payload), o0))
+        c.record(stream)
+        c.synchronize()
+        if it >= 5:
+            lat_enc.append(a.elapsed_time(b) * 1e3)
+            lat_dec.append(b.elapsed_time(c) * 1e3)
+    res["latency_us_p50"] = dict(
+        encode=statistics.median(lat_enc), decode=statistics.median(lat_dec),
+        encode_plus_decode=statistics.median([e + d for e, d in zip(lat_enc, lat_dec)]),
+        tensor=str(wl["dims"]), format="v2", note="device-resident, includes the info D2H sync")
+    # v1: the reference's single-stream format, one warp per tensor
+    B = x_dev.shape[0]
+    h_info = (_native.Info * B)()
+    for it in range(3):
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.check(lib.scz_encode_batch(ctx.h, ctypes.c_void_p(x_dev.data_ptr()), T, B, wl["q"], -1, 14,
+                                       1, 32, args.block_syms, ctypes.byref(batch)))
+        ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), h_info))
+        ctx.check(lib.scz_decode_batch_async(ctx.h, h_info, B, ctypes.c_void_p(batch.d_freqs),
+                                             ctypes.c_void_p(batch.d_block_bytes),
+                                             ctypes.c_void_p(batch.d_payload),
+                                             ctypes.c_void_p(out_dev.data_ptr())))
+        c.record(stream)
+        c.synchronize()
+    v1_ms = a.elapsed_time(c)
+    res["v1_reference_format"] = dict(value=4.0 * T * B / (v1_ms * 1e-3) / 1e9, unit=UNIT,
+                                      ms_per_step=v1_ms, batch=B,
+                                      note="bit-exact reference wire format; serial stream per tensor")
+    return res
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -408,3 +408,19 @@ def test_random_round_trips_vs_oracle():
         assert container.to_bytes(c) == orc.to_bytes(ref), (i, total, q, n_rows, fmt)
         out = sz.decompress(c)
         assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32))
+
+
+def test_batch_api_matches_single_tensor_path():
+    """compress_many / decompress_many (one device pass) == per-tensor calls."""
+    ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
+    for fmt in (1, 2):
+        many = container.compress_many(ts, 8, format=fmt, block_syms=1024)
+        for t, c in zip(ts, many):
+            one = sz.compress(t, 8, format=fmt, block_syms=1024)
+            assert container.to_bytes(c) == container.to_bytes(one)
+        outs = container.decompress_many(many)
+        for t, c, o in zip(ts, many, outs):
+            assert np.array_equal(o.data.view(np.uint32), sz.decompress(c).data.view(np.uint32))
+    # explicit N, mixed corruption: the bad tensor raises, as decompress would
+    many = container.compress_many(ts[:3], 6, n_rows=50176 // 8, format=2, block_syms=512)
+    assert all(c.n_cols == 8 for c in many)
