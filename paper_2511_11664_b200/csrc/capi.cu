@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -15,6 +16,10 @@
 #include "encode.cu"
 #include "select.cu"
 #include "rans.cu"
+#include "front.cu"
+#include "rans_enc.cu"
+#include "rans_dec.cu"
+#include "rowhist.cu"
 #include "decode.cu"
 
 using namespace scz;
@@ -85,6 +90,27 @@ std::vector<uint64_t> candidate_rows(uint64_t total, int q_bits) {
     return out;
 }
 
+// launch names carry the symbol width so per-kernel timing separates the
+// (mostly empty) variants that skip tensors of another width class
+template <typename S>
+const char* wname(const char* base) {
+    static const char* const tab[][3] = {
+        {"k_materialize/u8", "k_materialize/u16", "k_materialize/u32"},
+        {"k_rans_enc_v2/u8", "k_rans_enc_v2/u16", "k_rans_enc_v2/u32"},
+        {"k_rans_enc_v1/u8", "k_rans_enc_v1/u16", "k_rans_enc_v1/u32"},
+        {"k_rans_dec_v2/u8", "k_rans_dec_v2/u16", "k_rans_dec_v2/u32"},
+        {"k_rans_dec_v1/u8", "k_rans_dec_v1/u16", "k_rans_dec_v1/u32"},
+        {"k_row_sums/u8", "k_row_sums/u16", "k_row_sums/u32"},
+        {"k_rows_out/u8", "k_rows_out/u16", "k_rows_out/u32"},
+    };
+    static const char* const bases[] = {"k_materialize", "k_rans_enc_v2", "k_rans_enc_v1", "k_rans_dec_v2",
+                                        "k_rans_dec_v1", "k_row_sums", "k_rows_out"};
+    const int w = sizeof(S) == 1 ? 0 : (sizeof(S) == 2 ? 1 : 2);
+    for (int i = 0; i < 7; ++i)
+        if (!strcmp(base, bases[i])) return tab[i][w];
+    return base;
+}
+
 uint64_t gcd64(uint64_t a, uint64_t b) {
     while (b) {
         uint64_t t = a % b;
@@ -114,6 +140,9 @@ struct scz_ctx {
     int32_t* h_status_async = nullptr;
     uint32_t last_batch = 0;
     HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
+    DevBuf ready;
+    uint32_t front_grid = 0;  // co-resident CTAs of k_front (0 = not queried)
+    bool use_front = getenv("SCZ_FUSED_FRONT") != nullptr;  // experimental (slower today)
 
     // Optional per-kernel timing with CUDA events on this stream: kernel i
     // spans [end event of the previous launch (or the API-entry mark), its
@@ -379,7 +408,20 @@ __global__ void __launch_bounds__(256) k_pack(const scz_info* info, const uint8_
     const uint32_t len = block_len[sidx];
     const uint8_t* src = slots + sidx * slot_cap + slot_cap - len;
     uint8_t* dst = payload + in.payload_off + blk_off[sidx];
-    for (uint32_t i = threadIdx.x; i < len; i += 256) dst[i] = src[i];
+    // bytes up to a 4-aligned destination, then funnel-shifted words, then the tail
+    uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
+    head = head < len ? head : len;
+    if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+    const uint8_t* s2 = src + head;
+    uint32_t* d2 = reinterpret_cast<uint32_t*>(dst + head);
+    const uint32_t nwords = (len - head) / 4;
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(s2) & 3) * 8;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s2) & ~(uintptr_t)3);
+    for (uint32_t w = threadIdx.x; w < nwords; w += 256) {
+        const uint32_t lo = sw[w];
+        d2[w] = sh ? __funnelshift_r(lo, sw[w + 1], sh) : lo;  // slots are padded: w+1 is readable
+    }
+    for (uint32_t i = head + 4 * nwords + threadIdx.x; i < len; i += 256) dst[i] = src[i];
 }
 
 // The encode pipeline over a device batch.  cand_out (device) optional.
@@ -397,12 +439,13 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         rh_total += T / pl.rows[c] + 1;
     }
     if (rh_total >= (1ull << 32)) return ctx->fail(SCZ_UNSUPPORTED, "row histogram too large");
-    CK(ctx->bitmap.ensure((size_t)B * pl.words_pad * 4));
+    CK(ctx->bitmap.ensure((size_t)B * pl.words_pad * 4 + 64));
     CK(ctx->tile_stats.ensure((size_t)B * pl.n_tiles * sizeof(float4)));
     CK(ctx->tile_off.ensure((size_t)B * pl.n_tiles * 4));
     CK(ctx->state.ensure((size_t)B * sizeof(TensorState)));
     CK(ctx->vhist.ensure((size_t)B * 256 * 4));
-    CK(ctx->v8.ensure((size_t)B * T));
+    const uint64_t dstride = (pl.L_max + 15) & ~15ull;  // D = v ++ c ++ r (u8 width)
+    CK(ctx->v8.ensure((size_t)B * dstride + 64));
     int maxw = (pl.widths & 4) ? 4 : ((pl.widths & 2) ? 2 : 1);
     CK(ctx->cr.ensure((size_t)B * 2 * T * maxw));
     CK(ctx->hp.ensure((size_t)B * pl.period * 4));
@@ -412,11 +455,11 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     CK(ctx->freqs.ensure((size_t)B * pl.acap * 4));
     CK(ctx->cum.ensure((size_t)B * (pl.acap + 1) * 4));
     CK(ctx->enctab.ensure((size_t)B * pl.acap * sizeof(EncTab)));
-    CK(ctx->slots.ensure((size_t)B * pl.nblk_cap * pl.slot_cap));
+    CK(ctx->slots.ensure((size_t)B * pl.nblk_cap * pl.slot_cap + 64));
     CK(ctx->block_len.ensure((size_t)B * pl.nblk_cap * 4));
     CK(ctx->blk_off.ensure((size_t)B * pl.nblk_cap * 4));
     CK(ctx->info.ensure((size_t)B * sizeof(scz_info)));
-    CK(ctx->payload.ensure((size_t)B * pl.payload_cap + 256));
+    CK(ctx->payload.ensure((size_t)B * pl.payload_cap + 4096));
     CK(ctx->ticket.ensure(64));
     CK(cudaMemsetAsync(ctx->state.p, 0, (size_t)B * sizeof(TensorState), s));
     CK(cudaMemsetAsync(ctx->vhist.p, 0, (size_t)B * 256 * 4, s));
@@ -428,15 +471,36 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         CK(cudaMemsetAsync(ctx->rhist.p, 0, (size_t)B * rh_total * 4, s));
     }
 
-    StatsParams sp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
-                   ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>()};
-    k_stats<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(sp);
-    LAUNCHED("k_stats");
-    QuantParams qp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
-                   ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
-                   ctx->vhist.as<uint32_t>(), nullptr};
-    k_quantize<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(qp);
-    LAUNCHED("k_quantize");
+    // K1+K2+K3: fused single-read front end when every tensor's tiles fit in
+    // one co-resident grid (cooperative launch), else stats then quantise.
+    if (ctx->front_grid == 0) {
+        int per_sm = 0, coop = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_front, TILE_THREADS, 0);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+        ctx->front_grid = coop ? (uint32_t)(per_sm * ctx->num_sms) : 1u;
+    }
+    const uint64_t items = (uint64_t)B * pl.n_tiles;
+    if (ctx->use_front && pl.n_tiles <= ctx->front_grid && ctx->front_grid > 1) {
+        CK(ctx->ready.ensure((size_t)B * 4));
+        CK(cudaMemsetAsync(ctx->ready.p, 0, (size_t)B * 4, s));
+        FrontParams fp{d_x, T, pl.n_tiles, pl.words_pad, B, pl.q_bits, ctx->bitmap.as<uint32_t>(),
+                       ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(),
+                       ctx->ready.as<uint32_t>(), ctx->v8.as<uint8_t>(), ctx->vhist.as<uint32_t>(), dstride};
+        void* args[] = {&fp};
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(items, ctx->front_grid);
+        CK(cudaLaunchCooperativeKernel((void*)k_front, dim3(grid), dim3(TILE_THREADS), args, 0, s));
+        LAUNCHED("k_front");
+    } else {
+        StatsParams sp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
+                       ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>()};
+        k_stats<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(sp);
+        LAUNCHED("k_stats");
+        QuantParams qp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
+                       ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
+                       ctx->vhist.as<uint32_t>(), nullptr, dstride};
+        k_quantize<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(qp);
+        LAUNCHED("k_quantize");
+    }
 
     if (need_hist) {
         ColHistParams cp;
@@ -452,12 +516,12 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         k_colhist<<<g, 128, 0, s>>>(cp);
         LAUNCHED("k_colhist");
 
-        RowHistParams rp;
+        RowHist2Params rp;
         memset(&rp, 0, sizeof rp);
         rp.bitmap = ctx->bitmap.as<uint32_t>();
         rp.words_pad = pl.words_pad;
+        rp.n_words = ceil_div_u32(T, 32);
         rp.n_cand = ncand;
-        rp.rows_per_chunk = 8192;
         uint32_t chunks = 0, maxbins = 0;
         for (uint32_t c = 0; c < ncand; ++c) {
             uint32_t K = (uint32_t)(T / pl.rows[c]);
@@ -465,16 +529,24 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
             rp.cand_rows[c] = (uint32_t)pl.rows[c];
             rp.rhist_off[c] = rh_off[c];
             rp.chunk_start[c] = chunks;
-            if (K > 1) chunks += ceil_div_u32(pl.rows[c], rp.rows_per_chunk);
-            if (K > 1) maxbins = std::max(maxbins, K + 1);
+            if (K == 2 || K == 4 || K == 8) {
+                rp.units_per_chunk[c] = RH_THREADS * 16;  // bitmap words
+                chunks += ceil_div_u32(rp.n_words, rp.units_per_chunk[c]);
+            } else if (K > 1) {
+                rp.units_per_chunk[c] = RH_THREADS * 32;  // rows
+                chunks += ceil_div_u32(pl.rows[c], rp.units_per_chunk[c]);
+                if (K + 1 > RH_PRIV_BINS) maxbins = std::max(maxbins, K + 1);
+            }
         }
         rp.chunk_start[ncand] = chunks;
         rp.rhist = ctx->rhist.as<uint32_t>();
         rp.rhist_stride = (uint32_t)rh_total;
         if (chunks) {
-            size_t smem = std::min<uint32_t>(maxbins, 4096) * 4;
-            k_rowhist<<<dim3(chunks, B), 256, smem, s>>>(rp);
+            size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
+            k_rowhist2<<<dim3(chunks, B), RH_THREADS, smem, s>>>(rp);
             LAUNCHED("k_rowhist");
+            k_rowhist_zero<<<B, 64, 0, s>>>(rp);
+            LAUNCHED("k_rowhist_zero");
         }
     }
 
@@ -505,28 +577,49 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     sel.enctab = ctx->enctab.as<EncTab>();
     sel.cand_out = cand_out;
     sel.dump = dump;
-    k_select<<<B, SEL_THREADS, 0, s>>>(sel);
+    const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)pl.period) : 0;
+    if (sel_smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
+    k_select<<<B, SEL_THREADS, sel_smem, s>>>(sel);
     LAUNCHED("k_select");
 
     MatParams mp{T, pl.n_tiles, pl.words_pad, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(),
-                 ctx->state.as<TensorState>(), ctx->cr.p, 2 * T, 0};
+                 ctx->state.as<TensorState>(), ctx->cr.p, 2 * T, 1, 0};
     EncParams ep{ctx->state.as<TensorState>(), ctx->enctab.as<EncTab>(), pl.acap, pl.precision,
                  pl.block_syms, ctx->slots.as<uint8_t>(), pl.slot_cap, pl.nblk_cap,
-                 ctx->block_len.as<uint32_t>()};
-    const dim3 g_enc2(ceil_div_u32(pl.nblk_cap, ENC_WPB), B);
+                 ctx->block_len.as<uint32_t>(), pl.acap};
+    const dim3 g_enc2(ceil_div_u32(pl.nblk_cap, ENC2_WPB), B);
+    const bool enc_smem_tab = pl.acap <= ENC_TAB_SMEM_MAX;
+    const size_t enc_smem = enc_smem_tab ? (size_t)pl.acap * sizeof(EncTab) : 0;
     auto run_width = [&](auto tag) -> int {
         using S = decltype(tag);
-        k_materialize<S><<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(mp);
-        LAUNCHED("k_materialize");
-        SplitSrc<S> src{ctx->v8.as<uint8_t>(), T, ctx->cr.as<S>(), 2 * T};
-        if (pl.format == 2) {
-            k_rans_enc_v2<SplitSrc<S>><<<g_enc2, ENC_WPB * 32, 0, s>>>(ep, src);
-            LAUNCHED("k_rans_enc_v2");
-        } else {
-            k_rans_enc_v1<SplitSrc<S>><<<B, 32, 0, s>>>(ep, src);
-            LAUNCHED("k_rans_enc_v1");
+        MatParams m2 = mp;
+        if (sizeof(S) == 1) {  // u8: c ++ r land right after v in the same buffer
+            m2.cr = ctx->v8.p;
+            m2.cr_stride = dstride;
+            m2.after_v = 1;
         }
-        return SCZ_OK;
+        k_materialize<S><<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(m2);
+        LAUNCHED(wname<S>("k_materialize"));
+        auto launch = [&](auto src) -> int {
+            using Src = decltype(src);
+            if (pl.format == 2) {
+                if (enc_smem_tab) {
+                    CK(cudaFuncSetAttribute(k_rans_enc_v2<Src, true, false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)enc_smem));
+                    k_rans_enc_v2<Src, true, false><<<g_enc2, ENC2_WPB * 32, enc_smem, s>>>(ep, src);
+                } else {
+                    k_rans_enc_v2<Src, false, false><<<g_enc2, ENC2_WPB * 32, 0, s>>>(ep, src);
+                }
+                LAUNCHED(wname<S>("k_rans_enc_v2"));
+            } else {
+                k_rans_enc_v1<Src><<<B, 32, 0, s>>>(ep, src);
+                LAUNCHED(wname<S>("k_rans_enc_v1"));
+            }
+            return SCZ_OK;
+        };
+        if constexpr (sizeof(S) == 1) return launch(Contig8Src{ctx->v8.as<uint8_t>(), dstride});
+        else return launch(SplitSrc<S>{ctx->v8.as<uint8_t>(), dstride, ctx->cr.as<S>(), 2 * T});
     };
     int st;
     if (pl.widths & 1) { if ((st = run_width(uint8_t{})) != SCZ_OK) return st; }
@@ -549,7 +642,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
 void dec_class(const scz_info& in, uint8_t* width) {
     // symbol width + lookup flavour: 1 = u8 LUT, 2 = u16 LUT, 4 = binary search
     if (in.precision <= 15 && in.alphabet <= 256) *width = 1;
-    else if (in.precision <= 15 && in.alphabet <= 65536) *width = 2;
+    else if (in.precision <= 15 && in.alphabet <= 4096) *width = 2;
     else *width = 4;
 }
 
@@ -597,7 +690,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         maxA = std::max<uint64_t>(maxA, hi[b].alphabet);
         nblk_cap = std::max(nblk_cap, hi[b].version == 2 ? hi[b].n_blocks : 1u);
         Lmax = std::max<uint64_t>(Lmax, 2 * hi[b].nnz + hi[b].n_rows);
-        nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, ROW_CHUNK));
+        nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, rows_per_chunk(hi[b].n_cols)));
         maxn = std::max(maxn, (int)hi[b].precision);
         hoff[b] = off;
         off += hi[b].total;
@@ -627,21 +720,21 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         const size_t tab = maxA <= TAB_SMEM_MAX ? maxA * sizeof(uint2) : 0;
         const size_t lut = sizeof(L) < 4 ? ((size_t)1 << maxn) * sizeof(L) : 0;
         if (any_v2) {
-            size_t smem = DEC_WPB * RING + tab + lut;
+            size_t smem = dec_v2_smem(sizeof(L), maxn, (uint32_t)maxA);
             CK(cudaFuncSetAttribute(k_rans_dec_v2<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-            k_rans_dec_v2<S, L><<<dim3(ceil_div_u32(nblk_cap, DEC_WPB), B), DEC_WPB * 32, smem, s>>>(dp);
-            LAUNCHED("k_rans_dec_v2");
+            k_rans_dec_v2<S, L><<<dim3(ceil_div_u32(nblk_cap, DEC2_WPB), B), DEC2_WPB * 32, smem, s>>>(dp);
+            LAUNCHED(wname<S>("k_rans_dec_v2"));
         }
         if (any_v1) {
             size_t smem = RING + tab + lut;
             CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
             k_rans_dec_v1<S, L><<<B, 32, smem, s>>>(dp);
-            LAUNCHED("k_rans_dec_v1");
+            LAUNCHED(wname<S>("k_rans_dec_v1"));
         }
         k_row_sums<S><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
-        LAUNCHED("k_row_sums");
+        LAUNCHED(wname<S>("k_row_sums"));
         return SCZ_OK;
     };
     // the width filter: kernels of width S skip tensors of another class
@@ -656,7 +749,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         using S = decltype(tag);
         if (stage) k_rows_out<S, true><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
         else k_rows_out<S, false><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
-        LAUNCHED("k_rows_out");
+        LAUNCHED(wname<S>("k_rows_out"));
         return SCZ_OK;
     };
     if (widths & 1) { if ((st = rows_out(uint8_t{})) != SCZ_OK) return st; }
@@ -710,7 +803,7 @@ void scz_ctx_destroy(scz_ctx* ctx) {
                       &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
                       &ctx->info, &ctx->payload, &ctx->ticket, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
                       &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
-                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout})
+                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready})
         b->release();
     for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
                        &ctx->h_misc})
@@ -847,7 +940,7 @@ int scz_decompress(scz_ctx* ctx, const scz_info* info_in, const uint32_t* freqs,
     in.payload_off = 0;
     in.freqs_off = 0;
     in.blocks_off = 0;
-    CK(ctx->dpayload.ensure(in.payload_len + 512));
+    CK(ctx->dpayload.ensure(in.payload_len + 4096));
     CK(ctx->dfreqs.ensure((size_t)in.alphabet * 4));
     CK(ctx->dblocks.ensure((size_t)in.n_blocks * 4));
     CK(ctx->dout.ensure(in.total * 4));
@@ -908,7 +1001,7 @@ int quantize_impl(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, bool giv
     uint8_t* md = reinterpret_cast<uint8_t*>(qd + n);
     QuantParams qp{ctx->x_in.as<float>(), n, ntiles, wp, q_bits, ctx->bitmap.as<uint32_t>(),
                    ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
-                   ctx->vhist.as<uint32_t>(), qd};
+                   ctx->vhist.as<uint32_t>(), qd, n};
     k_quantize<<<dim3(ntiles, 1), TILE_THREADS, 0, s>>>(qp);
     LAUNCHED("k_quantize");
     k_unpack_mask<<<ceil_div_u32(n, 256), 256, 0, s>>>(ctx->bitmap.as<uint32_t>(), n, md);
@@ -992,7 +1085,7 @@ int scz_csr_encode(scz_ctx* ctx, const uint32_t* q, const uint8_t* mask, uint64_
     CK(cudaMemcpyAsync(&nnz, &ctx->state.as<TensorState>()->nnz, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     MatParams mp{n, ntiles, wp, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(),
-                 ctx->state.as<TensorState>(), dd + nnz, 0, 4};
+                 ctx->state.as<TensorState>(), dd + nnz, 0, 0, 0};
     k_materialize<uint32_t><<<dim3(ntiles, 1), TILE_THREADS, 0, s>>>(mp);
     LAUNCHED("k_materialize");
     CK(cudaMemcpyAsync(d, dd, (size_t)(2 * nnz + n_rows) * 4, cudaMemcpyDeviceToHost, s));
@@ -1012,7 +1105,7 @@ int scz_csr_decode(scz_ctx* ctx, const uint32_t* d, uint64_t nnz, uint64_t n_row
     CK(ctx->dsym_in.ensure(n * 5 + 16));
     CK(ctx->dinfo.ensure(sizeof(scz_info)));
     CK(ctx->dstatus.ensure(4));
-    uint32_t nch = std::max(1u, ceil_div_u32(n_rows, ROW_CHUNK));
+    uint32_t nch = std::max(1u, ceil_div_u32(n_rows, rows_per_chunk((uint32_t)n_cols)));
     CK(ctx->chunk_sum.ensure((size_t)nch * 4));
     CK(cudaMemcpyAsync(ctx->dsym.p, d, L * 4, cudaMemcpyHostToDevice, s));
     scz_info in;
@@ -1131,10 +1224,18 @@ int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t*
     hs.nnz = n;  // PlainSrc ignores the split
     CK(cudaMemcpyAsync(ctx->state.p, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
     EncParams ep{ctx->state.as<TensorState>(), ctx->enctab.as<EncTab>(), (uint32_t)alphabet, precision,
-                 block_syms, ctx->slots.as<uint8_t>(), slot_cap, nblk, ctx->block_len.as<uint32_t>()};
+                 block_syms, ctx->slots.as<uint8_t>(), slot_cap, nblk, ctx->block_len.as<uint32_t>(),
+                 (uint32_t)alphabet};
     PlainSrc src{ctx->dsym.as<uint32_t>(), 0};
-    if (v2) k_rans_enc_v2<PlainSrc><<<dim3(ceil_div_u32(nblk, ENC_WPB), 1), ENC_WPB * 32, 0, s>>>(ep, src);
-    else k_rans_enc_v1<PlainSrc><<<1, 32, 0, s>>>(ep, src);
+    if (v2 && alphabet <= ENC_TAB_SMEM_MAX) {
+        const size_t sm = (size_t)alphabet * sizeof(EncTab);
+        CK(cudaFuncSetAttribute(k_rans_enc_v2<PlainSrc, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sm));
+        k_rans_enc_v2<PlainSrc, true, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, sm, s>>>(ep, src);
+    } else if (v2) {
+        k_rans_enc_v2<PlainSrc, false, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, 0, s>>>(ep, src);
+    }
+    if (!v2) k_rans_enc_v1<PlainSrc><<<1, 32, 0, s>>>(ep, src);
     LAUNCHED("k_rans_enc");
     std::vector<uint32_t> bl(nblk);
     CK(cudaMemcpyAsync(bl.data(), ctx->block_len.p, nblk * 4, cudaMemcpyDeviceToHost, s));
@@ -1192,7 +1293,7 @@ int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint3
         return SCZ_OK;
     }
     cudaStream_t s = ctx->stream;
-    CK(ctx->dpayload.ensure(len + 512));
+    CK(ctx->dpayload.ensure(len + 4096));
     CK(ctx->dfreqs.ensure(alphabet * 4));
     CK(ctx->dblocks.ensure(std::max<uint64_t>(n_blocks, 1) * 4));
     CK(cudaMemcpyAsync(ctx->dpayload.p, data, len, cudaMemcpyHostToDevice, s));
@@ -1219,9 +1320,9 @@ int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint3
         using S = decltype(tag);
         const size_t lut = sizeof(S) < 4 ? ((size_t)1 << precision) * sizeof(S) : 0;
         if (lanes) {
-            size_t smem = DEC_WPB * RING + tab + lut;
+            size_t smem = dec_v2_smem(sizeof(S), precision, (uint32_t)alphabet);
             CK(cudaFuncSetAttribute(k_rans_dec_v2<S, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_rans_dec_v2<S, S><<<dim3(ceil_div_u32(n_blocks, DEC_WPB), 1), DEC_WPB * 32, smem, s>>>(dp);
+            k_rans_dec_v2<S, S><<<dim3(ceil_div_u32(n_blocks, DEC2_WPB), 1), DEC2_WPB * 32, smem, s>>>(dp);
         } else {
             size_t smem = RING + tab + lut;
             CK(cudaFuncSetAttribute(k_rans_dec_v1<S, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1360,7 +1461,7 @@ int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, c
         out_total += h_info[b].total;
     }
     cudaStream_t s = ctx->stream;
-    CK(ctx->dpayload.ensure(payload_bytes + 512));
+    CK(ctx->dpayload.ensure(payload_bytes + 4096));
     CK(ctx->dfreqs.ensure(freqs_count * 4 + 4));
     CK(ctx->dblocks.ensure(blocks_count * 4 + 4));
     CK(ctx->dout.ensure(out_total * 4));

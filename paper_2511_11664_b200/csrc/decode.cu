@@ -1,18 +1,28 @@
 // decode.cu -- CSR decode + dequantisation (K8) and the small
 // stage kernels used by the parity entry points.
 //
-//   k_row_sums   per 4096-row chunk: sum of row counts, r <= K check
-//   k_row_scan   per tensor: chunk offsets, sum(r) == nnz check
-//   k_rows_out   per chunk: row offsets (block scan), col checks
-//                (col < K, strictly increasing: sparse.py:74-89), and the
-//                dense row written once: LUT[v] at listed columns, +0.0
-//                elsewhere (tensor.py:154-155), or (q, mask) for the stage API.
+// Rows are processed in chunks of R(K) = min(1024, 4096 / K) rows so a chunk's
+// dense output (R*K fp32) fits 16 KB of shared memory; its column and value
+// segments are staged there too with coalesced loads before the scatter.
+//   k_row_sums   per chunk: sum of row counts, r <= K check (sparse.py:88-89)
+//   k_row_scan   per tensor: chunk offsets, sum(r) == nnz check (sparse.py:84-87)
+//   k_rows_out   per chunk: row offsets (block scan), column checks (col < K,
+//                strictly increasing: sparse.py:90-97); the dense rows are
+//                assembled in shared memory -- +0.0 everywhere, LUT[v] at the
+//                listed columns (tensor.py:154-155) -- and written back with
+//                coalesced 16-byte stores; or (q, mask) for the stage API.
 #include "common.cuh"
 
 namespace scz {
 
-constexpr int ROW_CHUNK = 4096;
+constexpr int ROW_CHUNK = 1024;     // max rows per chunk
+constexpr int OUT_ELEMS = 4096;     // dense fp32 elements staged per chunk
 constexpr int ROW_THREADS = 256;
+
+__host__ __device__ inline uint32_t rows_per_chunk(uint32_t K) {
+    const uint32_t r = K ? (uint32_t)OUT_ELEMS / K : (uint32_t)ROW_CHUNK;
+    return r < 1 ? 1u : (r > (uint32_t)ROW_CHUNK ? (uint32_t)ROW_CHUNK : r);
+}
 
 struct RowParams {
     const scz_info* info;   // [B]
@@ -32,11 +42,12 @@ __global__ void __launch_bounds__(ROW_THREADS) k_row_sums(RowParams p) {
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
-    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * ROW_CHUNK;
+    const uint32_t R = rows_per_chunk(in.n_cols);
+    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
     const S* r = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride + 2 * in.nnz;
     uint32_t sum = 0, bad = 0;
-    const uint64_t r1 = min(N, r0 + ROW_CHUNK);
+    const uint64_t r1 = min(N, r0 + R);
     for (uint64_t i = r0 + threadIdx.x; i < r1; i += ROW_THREADS) {
         uint32_t v = r[i];
         bad |= v > in.n_cols;
@@ -65,7 +76,8 @@ __global__ void __launch_bounds__(256) k_row_scan(RowParams p) {
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK) return;
     __shared__ uint32_t s_scan[33];
-    const uint32_t nch = (uint32_t)((in.n_rows + ROW_CHUNK - 1) / ROW_CHUNK);
+    const uint32_t R = rows_per_chunk(in.n_cols);
+    const uint32_t nch = (uint32_t)((in.n_rows + R - 1) / R);
     uint32_t* cs = p.chunk_sum + (uint64_t)b * p.nchunk_cap;
     unsigned long long carry = 0;
     for (uint32_t base = 0; base < nch; base += 256) {
@@ -84,31 +96,35 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
-    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * ROW_CHUNK;
-    if (r0 >= N) return;
     const uint32_t K = in.n_cols;
+    const uint32_t R = rows_per_chunk(K);
+    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
+    if (r0 >= N) return;
     const uint64_t nnz = in.nnz;
     const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
     const S* vals = d;
     const S* cols = d + nnz;
     const S* rc = d + 2 * nnz;
     __shared__ uint32_t s_off[ROW_CHUNK];
+    __shared__ __align__(16) float s_out[OUT_ELEMS];
     __shared__ uint32_t s_scan[33];
     __shared__ float s_lut[256];
     __shared__ int s_bad;
-    const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)ROW_CHUNK ? (N - r0) : (uint64_t)ROW_CHUNK);
+    constexpr bool STAGE_CV = !STAGE && sizeof(S) <= 2;
+    __shared__ S s_cs[STAGE_CV ? OUT_ELEMS : 1], s_vs[STAGE_CV ? OUT_ELEMS : 1];
+    const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
     // dequantisation LUT: float32(float64(q - z) * scale) (tensor.py:154)
     const uint32_t nq = in.q_bits <= 8 ? (1u << in.q_bits) : 256u;  // header q_bits is unchecked here
     if (!STAGE)
         for (uint32_t i = threadIdx.x; i < nq; i += ROW_THREADS)
             s_lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, (double)in.zero_point), in.scale));
     if (threadIdx.x == 0) s_bad = 0;
-    // per-chunk row offsets: each thread scans 16 consecutive rows
+    // per-chunk row offsets: each thread scans ROW_CHUNK / 256 consecutive rows
     constexpr int PER = ROW_CHUNK / ROW_THREADS;
     uint32_t loc[PER], sum = 0;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        uint32_t i = threadIdx.x * PER + j;
+        const uint32_t i = threadIdx.x * PER + j;
         loc[j] = i < nrow ? (uint32_t)rc[r0 + i] : 0;
         sum += loc[j];
     }
@@ -120,54 +136,72 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
         s_off[threadIdx.x * PER + j] = cbase + ex;
         ex += loc[j];
     }
+    const uint32_t n_el = nrow * K;  // <= OUT_ELEMS unless K > OUT_ELEMS (then nrow == 1)
+    const bool staged = !STAGE && n_el <= (uint32_t)OUT_ELEMS;
+    if (staged)
+        for (uint32_t i = threadIdx.x; i < n_el; i += ROW_THREADS) s_out[i] = 0.0f;
+    // the chunk's nonzeros are [cbase, cbase + tot): stage their columns and values
+    const bool cv_staged = STAGE_CV && staged && tot <= (uint32_t)OUT_ELEMS;
+    if constexpr (STAGE_CV) {
+        if (cv_staged)
+            for (uint32_t i = threadIdx.x; i < tot; i += ROW_THREADS) {
+                s_cs[i] = cols[cbase + i];
+                s_vs[i] = vals[cbase + i];
+            }
+    }
     __syncthreads();
     bool bad = false;
-    float* orow_base = STAGE ? nullptr : p.out + p.out_off[b];
+    float* ochunk = STAGE ? nullptr : p.out + p.out_off[b] + r0 * K;
     for (uint32_t li = threadIdx.x; li < nrow; li += ROW_THREADS) {
         const uint64_t i = r0 + li;
         const uint32_t off = s_off[li];
         const uint32_t r = (uint32_t)rc[i];
-        uint32_t prev = 0xffffffffu;
-        uint32_t j = 0;
-        uint32_t nc = r ? (uint32_t)cols[off] : 0xffffffffu;
         if (STAGE) {
             uint32_t* qo = p.q_out + i * K;
             uint8_t* mo = p.mask_out + i * K;
             for (uint32_t col = 0; col < K; ++col) {
-                if (j < r && nc == col) {
-                    qo[col] = (uint32_t)vals[off + j];
-                    mo[col] = 0;
-                    prev = nc;
-                    ++j;
-                    nc = j < r ? (uint32_t)cols[off + j] : 0xffffffffu;
-                    if (j < r && (nc <= prev || nc >= K)) bad = true;
-                } else {
-                    qo[col] = 0;
-                    mo[col] = 1;
-                }
+                qo[col] = 0;
+                mo[col] = 1;
             }
-        } else {
-            float* orow = orow_base + i * K;
-            for (uint32_t col = 0; col < K; ++col) {
-                float o = 0.0f;
-                if (j < r && nc == col) {
-                    const uint32_t v = (uint32_t)vals[off + j];
-                    o = v < nq ? s_lut[v]
-                               : __double2float_rn(__dmul_rn(
-                                     __dsub_rn((double)v, (double)in.zero_point), in.scale));
-                    prev = nc;
-                    ++j;
-                    nc = j < r ? (uint32_t)cols[off + j] : 0xffffffffu;
-                    if (j < r && (nc <= prev || nc >= K)) bad = true;
-                }
-                orow[col] = o;
+        } else if (!staged) {
+            for (uint32_t col = 0; col < K; ++col) ochunk[(uint64_t)li * K + col] = 0.0f;
+        }
+        uint32_t prev = 0;
+        for (uint32_t j = 0; j < r; ++j) {
+            const uint32_t c = cv_staged ? (uint32_t)s_cs[off - cbase + j] : (uint32_t)cols[off + j];
+            if (c >= K || (j > 0 && c <= prev)) {  // sparse.py:90-97
+                bad = true;
+                break;
+            }
+            prev = c;
+            const uint32_t v = cv_staged ? (uint32_t)s_vs[off - cbase + j] : (uint32_t)vals[off + j];
+            if (STAGE) {
+                p.q_out[i * K + c] = v;
+                p.mask_out[i * K + c] = 0;
+            } else {
+                const float o = v < nq ? s_lut[v]
+                                       : __double2float_rn(__dmul_rn(
+                                             __dsub_rn((double)v, (double)in.zero_point), in.scale));
+                if (staged) s_out[li * K + c] = o;
+                else ochunk[(uint64_t)li * K + c] = o;
             }
         }
-        if (j != r) bad = true;  // a column >= K or out of order was never matched
     }
     if (bad) s_bad = 1;
     __syncthreads();
     if (threadIdx.x == 0 && s_bad) p.status[b] = SCZ_CORRUPT_STREAM;
+    if (staged && !s_bad) {
+        // coalesced write-back of the chunk's dense rows
+        const uintptr_t addr = reinterpret_cast<uintptr_t>(ochunk);
+        if ((addr & 15) == 0) {
+            const uint32_t n4 = n_el / 4;
+            for (uint32_t i = threadIdx.x; i < n4; i += ROW_THREADS)
+                reinterpret_cast<float4*>(ochunk)[i] = reinterpret_cast<const float4*>(s_out)[i];
+            for (uint32_t i = 4 * n4 + threadIdx.x; i < n_el; i += ROW_THREADS) ochunk[i] = s_out[i];
+        } else {
+            for (uint32_t i = threadIdx.x; i < n_el; i += ROW_THREADS) ochunk[i] = s_out[i];
+        }
+    }
 }
 
 #define SCZ_INST_ROWS(S)                                        \
@@ -179,7 +213,7 @@ SCZ_INST_ROWS(uint16_t)
 SCZ_INST_ROWS(uint32_t)
 
 // ------------------------------------------------------ stage-API helpers
-// zero mask (u8) -> bitmap + per-tile nnz (tile_stats.z), for csr_encode.
+// zero mask (u8) -> bitmap + per-tile nnz, for csr_encode.
 __global__ void __launch_bounds__(TILE_THREADS) k_mask_bitmap(const uint8_t* mask, uint64_t n,
                                                               uint32_t* bitmap, uint32_t* tile_nnz) {
     const uint32_t tile = blockIdx.x;

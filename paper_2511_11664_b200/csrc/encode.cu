@@ -83,11 +83,16 @@ __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
 
     float mn = INFINITY, mx = -INFINITY;
     uint32_t nnz = 0, bad = 0;
-#pragma unroll 4
+    // all eight 16-byte loads in flight before any use (memory-level parallelism)
+    float4 vv[8];
+    uint32_t vvalid[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it)
+        vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &vvalid[it]);
+#pragma unroll
     for (int it = 0; it < 8; ++it) {
-        uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4;
-        uint32_t valid;
-        float4 v = load4(xb, idx, p.total, aligned, &valid);
+        const uint32_t valid = vvalid[it];
+        const float4 v = vv[it];
         float e[4] = {v.x, v.y, v.z, v.w};
         uint32_t nib = 0;
 #pragma unroll
@@ -215,9 +220,10 @@ struct QuantParams {
     const uint32_t* bitmap;
     const uint32_t* tile_off;
     const TensorState* state;
-    uint8_t* v8;          // [B][total] compacted value symbols
+    uint8_t* v8;          // [B][v8_stride] compacted value symbols (head of D)
     uint32_t* vhist;      // [B][256]
     uint32_t* sym_out;    // optional [B][total] full symbol array (stage API)
+    uint64_t v8_stride;
 };
 
 // tensor.py:130-140 for one element: exact fp64 sequence of the reference.
@@ -256,9 +262,15 @@ __global__ void __launch_bounds__(TILE_THREADS) k_quantize(QuantParams p) {
 
     __shared__ uint32_t s_wpre[TILE_WORDS];
     __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_hist[256];
+    __shared__ uint32_t s_hist[4][256];  // one copy per warp pair: less atomic contention
     const int nbins = 1 << p.q_bits;
-    for (int i = threadIdx.x; i < nbins; i += TILE_THREADS) s_hist[i] = 0;
+    for (int i = threadIdx.x; i < 4 * 256; i += TILE_THREADS) (&s_hist[0][0])[i] = 0;
+    // all eight 16-byte loads in flight first
+    float4 vv[8];
+    uint32_t vvalid[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it)
+        vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &vvalid[it]);
     uint32_t myword = bm[threadIdx.x];
     uint32_t tot;
     s_wpre[threadIdx.x] = block_exclusive_scan<TILE_THREADS>(__popc(myword), s_scan, &tot);
@@ -269,13 +281,13 @@ __global__ void __launch_bounds__(TILE_THREADS) k_quantize(QuantParams p) {
     const float r32 = st.rcp32, zf32 = (float)st.zero_point;
     const bool fast = st.fast != 0;
     const int qmax = nbins - 1;
-    uint8_t* v8 = p.v8 + (uint64_t)b * p.total;
+    uint8_t* v8 = p.v8 + (uint64_t)b * p.v8_stride;
 
-#pragma unroll 2
+#pragma unroll
     for (int it = 0; it < 8; ++it) {
-        uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4;
-        uint32_t valid;
-        float4 v = load4(xb, idx, p.total, aligned, &valid);
+        const uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4;
+        const uint32_t valid = vvalid[it];
+        const float4 v = vv[it];
         float e[4] = {v.x, v.y, v.z, v.w};
         const int word = warp * 32 + it * 4 + (lane >> 3);
         const uint32_t wbits = bm[word];
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_quantize(QuantParams p) {
             if ((valid >> j & 1) && e[j] != 0.0f) {
                 uint32_t q = quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
                 v8[rank++] = (uint8_t)q;
-                atomicAdd(&s_hist[q], 1u);
+                atomicAdd(&s_hist[warp & 3][q], 1u);
                 if (p.sym_out) p.sym_out[(uint64_t)b * p.total + idx + j] = q;
             } else if (p.sym_out && (valid >> j & 1)) {
                 p.sym_out[(uint64_t)b * p.total + idx + j] =
@@ -296,8 +308,10 @@ __global__ void __launch_bounds__(TILE_THREADS) k_quantize(QuantParams p) {
     }
     __syncthreads();
     uint32_t* gh = p.vhist + (uint64_t)b * 256;
-    for (int i = threadIdx.x; i < nbins; i += TILE_THREADS)
-        if (s_hist[i]) atomicAdd(gh + i, s_hist[i]);
+    for (int i = threadIdx.x; i < nbins; i += TILE_THREADS) {
+        const uint32_t t = s_hist[0][i] + s_hist[1][i] + s_hist[2][i] + s_hist[3][i];
+        if (t) atomicAdd(gh + i, t);
+    }
 }
 
 // ------------------------------------------------------- search histograms
@@ -409,7 +423,8 @@ struct MatParams {
     const TensorState* state;
     void* cr;             // [B][cr_stride] symbols of width sym_bytes
     uint64_t cr_stride;   // elements
-    int sym_bytes;
+    int sym_bytes;        // 1: skip tensors whose chosen width is not sizeof(S)
+    int after_v;          // 1: c ++ r start at element nnz (u8: D = v ++ c ++ r contiguous)
 };
 
 template <typename S>
@@ -422,33 +437,54 @@ __global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
+    if (p.sym_bytes && st.sym_bytes != sizeof(S)) return;  // another width variant owns this tensor
     const uint32_t K = st.n_cols;
     const uint64_t nnz = st.nnz;
     const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad;
-    S* cr = reinterpret_cast<S*>(p.cr) + (uint64_t)b * p.cr_stride;
+    S* cr = reinterpret_cast<S*>(p.cr) + (uint64_t)b * p.cr_stride + (p.after_v ? nnz : 0);
     __shared__ uint32_t s_scan[33];
+    __shared__ uint32_t s_w[TILE_WORDS + 2];  // this tile's bitmap + the next two words
+    __shared__ uint8_t s_mod[64];             // i mod K for i < 64 (K <= 32)
+    __shared__ S s_c[TILE];                   // column indices staged in rank order
     const uint64_t word = (uint64_t)tile * TILE_WORDS + threadIdx.x;
     uint32_t w = bm[word];
+    s_w[threadIdx.x] = w;
+    if (threadIdx.x < 2) {
+        const uint64_t nw = (uint64_t)(tile + 1) * TILE_WORDS + threadIdx.x;
+        s_w[TILE_WORDS + threadIdx.x] = nw < p.words_pad ? bm[nw] : 0u;
+    }
+    if (threadIdx.x < 64 && K <= 32) s_mod[threadIdx.x] = (uint8_t)(threadIdx.x % K);
     uint32_t tot;
-    uint32_t rank = p.tile_off[(uint64_t)b * p.n_tiles + tile] +
-                    block_exclusive_scan<TILE_THREADS>(__popc(w), s_scan, &tot);
+    uint32_t lrank = block_exclusive_scan<TILE_THREADS>(__popc(w), s_scan, &tot);  // syncs
+    const uint32_t base_rank = p.tile_off[(uint64_t)b * p.n_tiles + tile];
     // column index of every nonzero: p mod K (sparse.py:66-68)
     if (w) {
-        uint64_t p0 = word * 32;
-        uint32_t m = (uint32_t)(p0 % K);
+        const uint32_t m = (uint32_t)((word * 32) % K);
         while (w) {
-            int bit = __ffs(w) - 1;
+            const int bit = __ffs(w) - 1;
             w &= w - 1;
             uint32_t c = m + bit;
-            if (c >= K) c = (K <= 32) ? c % K : c - K;
-            cr[rank++] = (S)c;
+            c = (K <= 32) ? s_mod[c] : (c >= K ? c - K : c);
+            s_c[lrank++] = (S)c;
         }
     }
+    __syncthreads();
+    S* dst = cr + base_rank;
+    for (uint32_t i = threadIdx.x; i < tot; i += TILE_THREADS) dst[i] = s_c[i];  // coalesced
     // row counts for the rows starting in this tile (sparse.py:68)
-    uint64_t ts = (uint64_t)tile * TILE, te = min(ts + TILE, p.total);
-    uint64_t i0 = (ts + K - 1) / K, i1 = (te + K - 1) / K;
-    for (uint64_t i = i0 + threadIdx.x; i < i1; i += TILE_THREADS)
-        cr[nnz + i] = (S)range_popc(bm, i * K, K);
+    const uint64_t ts = (uint64_t)tile * TILE, te = min(ts + TILE, p.total);
+    const uint64_t i0 = (ts + K - 1) / K, i1 = (te + K - 1) / K;
+    if (K <= 32) {
+        const uint32_t kmask = K == 32 ? 0xffffffffu : ((1u << K) - 1u);
+        for (uint64_t i = i0 + threadIdx.x; i < i1; i += TILE_THREADS) {
+            const uint32_t start = (uint32_t)(i * K - ts);  // < TILE
+            const uint32_t wi = start >> 5, sh = start & 31;
+            cr[nnz + i] = (S)__popc(__funnelshift_r(s_w[wi], s_w[wi + 1], sh) & kmask);
+        }
+    } else {
+        for (uint64_t i = i0 + threadIdx.x; i < i1; i += TILE_THREADS)
+            cr[nnz + i] = (S)range_popc(bm, i * K, K);
+    }
 }
 
 template __global__ void k_materialize<uint8_t>(MatParams);

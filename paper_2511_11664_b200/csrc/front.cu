@@ -1,0 +1,243 @@
+// front.cu -- fused front end: K1 + K2 + K3 with ONE read of the features.
+//
+// A persistent, cooperatively launched grid walks (tensor, tile) items; all
+// CTAs are co-resident, and a tensor's tiles occupy at most two consecutive
+// waves of the grid (host guarantees n_tiles <= grid), so the per-tensor
+// barrier below cannot deadlock.  Per item:
+//   phase 1  load the 8192-element tile into registers (8 x float4 per
+//            thread), min/max/non-finite (tensor.py:48, 127), the zero bitmap
+//            (tensor.py:139) and the tile's nonzero count;
+//   barrier  the last CTA of the tensor to arrive reduces the tile stats,
+//            scans the tile counts into rank offsets and runs compute_params
+//            in fp64 (tensor.py:101-122), then releases the others;
+//   phase 2  quantise the register-resident values (tensor.py:130-140, fp32
+//            guard band + exact fp64 fix-up), compact the original-nonzero
+//            symbols into v8 in rank order (sparse.py:65-67), and histogram
+//            them (per-warp-pair shared-memory copies).
+#include "common.cuh"
+
+namespace scz {
+
+struct FrontParams {
+    const float* x;
+    uint64_t total;
+    uint32_t n_tiles;
+    uint32_t words_pad;
+    uint32_t batch;
+    int q_bits;
+    uint32_t* bitmap;
+    float4* tile_stats;   // [B][n_tiles]
+    uint32_t* tile_off;   // [B][n_tiles]
+    TensorState* state;   // [B] (tiles_done is the arrival counter)
+    uint32_t* ready;      // [B] release flags (zeroed per launch)
+    uint8_t* v8;          // [B][total]
+    uint32_t* vhist;      // [B][256]
+    uint64_t v8_stride;
+};
+
+__global__ void __launch_bounds__(TILE_THREADS) k_front(FrontParams p) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t s_words[TILE_WORDS];
+    __shared__ uint32_t s_scan[33];
+    __shared__ uint32_t s_whist[4][256];  // value histogram, one copy per warp pair
+    __shared__ float s_mn[8], s_mx[8];
+    __shared__ uint32_t s_nnz[8], s_bad[8];
+    __shared__ uint32_t s_last;
+    const uint64_t n_items = (uint64_t)p.batch * p.n_tiles;
+    const int nbins = 1 << p.q_bits;
+    const int qmax = nbins - 1;
+    for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const uint32_t b = (uint32_t)(item / p.n_tiles), tile = (uint32_t)(item % p.n_tiles);
+        const float* xb = p.x + (uint64_t)b * p.total;
+        const bool aligned = ((reinterpret_cast<uintptr_t>(xb) & 15) == 0);
+        const uint64_t tile_base = (uint64_t)tile * TILE;
+        uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad + (uint64_t)tile * TILE_WORDS;
+        // ---- phase 1 ------------------------------------------------------
+        float4 v[8];
+        uint32_t nib[8], valid[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            const uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4;
+            if (aligned && idx + 3 < p.total) {
+                v[it] = __ldcs(reinterpret_cast<const float4*>(xb + idx));
+                valid[it] = 0xF;
+            } else {
+                float e[4];
+                uint32_t m = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool ok = idx + j < p.total;
+                    e[j] = ok ? xb[idx + j] : 0.0f;
+                    m |= (uint32_t)ok << j;
+                }
+                v[it] = make_float4(e[0], e[1], e[2], e[3]);
+                valid[it] = m;
+            }
+        }
+        float mn = INFINITY, mx = -INFINITY;
+        uint32_t nnz = 0, bad = 0;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            const float e[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+            uint32_t nb = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (valid[it] >> j & 1) {
+                    bad |= !isfinite(e[j]);
+                    mn = fminf(mn, e[j]);
+                    mx = fmaxf(mx, e[j]);
+                    nb |= (uint32_t)(e[j] != 0.0f) << j;
+                }
+            }
+            nib[it] = nb;
+            nnz += __popc(nb);
+            uint32_t w = nb << (4 * (lane & 7));
+            w |= __shfl_xor_sync(0xffffffffu, w, 1);
+            w |= __shfl_xor_sync(0xffffffffu, w, 2);
+            w |= __shfl_xor_sync(0xffffffffu, w, 4);
+            if ((lane & 7) == 0) {
+                const int wi = warp * 32 + it * 4 + (lane >> 3);
+                s_words[wi] = w;
+                bm[wi] = w;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        if (lane == 0) {
+            s_mn[warp] = mn;
+            s_mx[warp] = mx;
+            s_nnz[warp] = nnz;
+            s_bad[warp] = bad;
+        }
+        for (int i = threadIdx.x; i < 4 * 256; i += TILE_THREADS) (&s_whist[0][0])[i] = 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < 8; ++w) {
+                mn = fminf(mn, s_mn[w]);
+                mx = fmaxf(mx, s_mx[w]);
+                nnz += s_nnz[w];
+                bad |= s_bad[w];
+            }
+            p.tile_stats[item] = make_float4(mn, mx, __uint_as_float(nnz), __uint_as_float(bad));
+            __threadfence();
+            const uint32_t t = atomicAdd(&p.state[b].tiles_done, 1u);
+            s_last = (t == p.n_tiles - 1);
+        }
+        __syncthreads();
+        // ---- per-tensor barrier ------------------------------------------
+        if (s_last) {
+            __threadfence();
+            const float4* ts = p.tile_stats + (uint64_t)b * p.n_tiles;
+            uint32_t* toff = p.tile_off + (uint64_t)b * p.n_tiles;
+            float gmn = INFINITY, gmx = -INFINITY;
+            uint32_t gbad = 0, carry = 0;
+            for (uint32_t base = 0; base < p.n_tiles; base += TILE_THREADS) {
+                const uint32_t i = base + threadIdx.x;
+                uint32_t c = 0;
+                if (i < p.n_tiles) {
+                    const float4 s = __ldcg(ts + i);
+                    gmn = fminf(gmn, s.x);
+                    gmx = fmaxf(gmx, s.y);
+                    c = __float_as_uint(s.z);
+                    gbad |= __float_as_uint(s.w);
+                }
+                uint32_t tot;
+                const uint32_t ex = block_exclusive_scan<TILE_THREADS>(c, s_scan, &tot);
+                if (i < p.n_tiles) toff[i] = carry + ex;
+                carry += tot;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                gmn = fminf(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+                gmx = fmaxf(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+                gbad |= __shfl_xor_sync(0xffffffffu, gbad, o);
+            }
+            if (lane == 0) {
+                s_mn[warp] = gmn;
+                s_mx[warp] = gmx;
+                s_bad[warp] = gbad;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int w = 1; w < 8; ++w) {
+                    gmn = fminf(gmn, s_mn[w]);
+                    gmx = fmaxf(gmx, s_mx[w]);
+                    gbad |= s_bad[w];
+                }
+                TensorState& st = p.state[b];
+                st.xmin = gmn;
+                st.xmax = gmx;
+                st.nonfinite = gbad;
+                st.nnz = carry;
+                if (gbad) {
+                    st.status = SCZ_INVALID_INPUT;
+                    st.scale = 1.0;
+                    st.zero_point = 0;
+                    st.fast = 0;
+                    st.rcp32 = 1.0f;
+                } else {
+                    double s;
+                    int64_t z;
+                    device_compute_params(gmn, gmx, p.q_bits, &s, &z);
+                    st.scale = s;
+                    st.zero_point = z;
+                    st.fast = (s >= 0x1p-120 && s <= 0x1p120) ? 1u : 0u;
+                    st.rcp32 = (float)(1.0 / s);
+                }
+                __threadfence();
+                atomicExch(&p.ready[b], 1u);
+            }
+        } else if (threadIdx.x == 0) {
+            while (atomicAdd(&p.ready[b], 0u) == 0u) __nanosleep(64);
+        }
+        __syncthreads();
+        __threadfence();
+        // ---- phase 2 ------------------------------------------------------
+        const TensorState& st = p.state[b];
+        const int32_t status = *(volatile const int32_t*)&st.status;
+        if (status == SCZ_OK) {
+            const double scale = *(volatile const double*)&st.scale;
+            const int64_t z = *(volatile const int64_t*)&st.zero_point;
+            const double zf = (double)z;
+            const float r32 = *(volatile const float*)&st.rcp32, zf32 = (float)z;
+            const bool fast = *(volatile const uint32_t*)&st.fast != 0;
+            const uint32_t base_rank = __ldcg(p.tile_off + item);
+            uint32_t tot;
+            const uint32_t wpre = block_exclusive_scan<TILE_THREADS>(__popc(s_words[threadIdx.x]), s_scan, &tot);
+            // block_exclusive_scan synchronised; publish each word's prefix
+            __shared__ uint32_t s_wpre[TILE_WORDS];
+            s_wpre[threadIdx.x] = wpre;
+            __syncthreads();
+            uint8_t* v8 = p.v8 + (uint64_t)b * p.v8_stride;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const int word = warp * 32 + it * 4 + (lane >> 3);
+                const int bit0 = 4 * (lane & 7);
+                uint32_t rank = base_rank + s_wpre[word] + __popc(s_words[word] & ((1u << bit0) - 1u));
+                const float e[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if ((nib[it] >> j) & 1) {
+                        const uint32_t q = quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
+                        v8[rank++] = (uint8_t)q;
+                        atomicAdd(&s_whist[warp & 3][q], 1u);
+                    }
+                }
+            }
+            __syncthreads();
+            uint32_t* gh = p.vhist + (uint64_t)b * 256;
+            for (int i = threadIdx.x; i < nbins; i += TILE_THREADS) {
+                const uint32_t t = s_whist[0][i] + s_whist[1][i] + s_whist[2][i] + s_whist[3][i];
+                if (t) atomicAdd(gh + i, t);
+            }
+        }
+        __syncthreads();  // shared buffers are reused by the next item
+    }
+}
+
+}  // namespace scz

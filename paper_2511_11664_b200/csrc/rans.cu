@@ -29,6 +29,14 @@ struct SplitSrc {  // D = v8[0..nnz) ++ cr[0..nnz+N)
     }
     static constexpr int width = sizeof(S);
 };
+struct Contig8Src {  // D = v ++ c ++ r contiguous u8 (the common width)
+    const uint8_t* d;
+    uint64_t stride;
+    __device__ __forceinline__ uint32_t at(uint32_t b, uint64_t i, uint64_t) const {
+        return d[b * stride + i];
+    }
+    static constexpr int width = 1;
+};
 struct PlainSrc {  // D given as u32 (stage API)
     const uint32_t* d;
     uint64_t stride;
@@ -48,88 +56,13 @@ struct EncParams {
     uint64_t slot_cap;        // bytes per slot
     uint32_t slots_per_tensor;
     uint32_t* block_len;      // [B][slots_per_tensor]
+    uint32_t tab_smem;        // table entries staged in dynamic smem (v2)
 };
 
 __device__ __forceinline__ void flag_err(TensorState& st, uint32_t bit) {
     atomicOr(&st.errbits, bit);
 }
 constexpr uint32_t ERR_OVERFLOW = 1, ERR_UNCODABLE = 2;
-
-template <class Src>
-__global__ void __launch_bounds__(ENC_WPB * 32) k_rans_enc_v2(EncParams p, Src src) {
-    const uint32_t b = blockIdx.y;
-    TensorState& st = p.state[b];
-    if (st.status != SCZ_OK) return;
-    if (Src::width && st.sym_bytes != (uint32_t)Src::width) return;  // other width variant
-    __shared__ EncTab s_tab[TAB_SMEM_MAX];
-    const uint32_t A = st.alphabet;
-    const EncTab* gt = p.enctab + (uint64_t)b * p.acap;
-    const bool smem_tab = A <= TAB_SMEM_MAX;
-    if (smem_tab)
-        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) s_tab[i] = gt[i];
-    __syncthreads();
-    const EncTab* tab = smem_tab ? s_tab : gt;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t L = st.stream_len;
-    const uint32_t nblk = L ? ceil_div_u32(L, p.block_syms) : 1;
-    const uint32_t blk = blockIdx.x * ENC_WPB + warp;
-    if (blk >= nblk) return;
-    const uint64_t nnz = st.nnz;
-    const uint64_t base = (uint64_t)blk * p.block_syms;
-    const uint32_t len = (uint32_t)min((uint64_t)p.block_syms, L - base);
-    const uint32_t steps = (len + 31) / 32;
-    const int n = p.precision;
-    const uint32_t gtm = lanemask_gt();
-    uint8_t* slot = p.slots + ((uint64_t)b * p.slots_per_tensor + blk) * p.slot_cap;
-    uint8_t* tail = slot + p.slot_cap - 1;  // emitted byte k lands at tail[-k]
-    uint32_t x = STATE_LOW, emitted = 0, err = 0;
-
-    // software pipeline: symbol of the next step is fetched one step ahead
-    uint32_t i_next = (steps - 1) * 32 + lane;
-    uint32_t sym_next = (steps && i_next < len) ? src.at(b, base + i_next, nnz) : 0;
-    for (int s = (int)steps - 1; s >= 0; --s) {
-        const uint32_t i = (uint32_t)s * 32 + lane;
-        const bool active = i < len;
-        uint32_t sym = sym_next;
-        if (s > 0) sym_next = src.at(b, base + i - 32, nnz);  // i - 32 < len always
-        EncTab t = {1, 0, 0, 0xFFFFFFFFu};
-        if (active) {
-            if (sym >= A) {
-                err |= ERR_OVERFLOW;
-            } else {
-                t = tab[sym];
-                if (t.freq == 0) err |= ERR_UNCODABLE;
-            }
-        }
-        const bool live = active && t.freq != 0 && sym < A;
-        const uint32_t bound = t.freq << (31 - n);  // ((L >> n) << 8) * f
-        uint32_t e = 0;
-        if (live && x >= bound) e = ((x >> 8) >= bound) ? 2u : 1u;
-        const uint32_t b1 = __ballot_sync(0xffffffffu, e >= 1);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, e == 2);
-        const uint32_t k = emitted + __popc(b1 & gtm) + __popc(b2 & gtm);
-        if (e >= 1) tail[-(int64_t)k] = (uint8_t)(x & 0xFF);
-        if (e == 2) tail[-(int64_t)k - 1] = (uint8_t)((x >> 8) & 0xFF);
-        emitted += __popc(b1) + __popc(b2);
-        x >>= 8 * e;
-        if (live) {
-            uint32_t q = enc_div(x, t);
-            x = (q << n) + t.cum + (x - q * t.freq);
-        }
-    }
-    // block bytes: W little-endian states, then the emitted bytes (decoder order)
-    const uint32_t blen = 4 * 32 + emitted;
-    uint8_t* start = slot + p.slot_cap - blen;
-    start[4 * lane + 0] = (uint8_t)x;
-    start[4 * lane + 1] = (uint8_t)(x >> 8);
-    start[4 * lane + 2] = (uint8_t)(x >> 16);
-    start[4 * lane + 3] = (uint8_t)(x >> 24);
-    err = __reduce_or_sync(0xffffffffu, err);
-    if (lane == 0) {
-        p.block_len[(uint64_t)b * p.slots_per_tensor + blk] = blen;
-        if (err) flag_err(st, err);
-    }
-}
 
 // v1: the reference's single stream.  One warp per tensor; all lanes carry
 // the same state, lane j prefetches the table entry of the j-th next symbol.
@@ -322,75 +255,6 @@ struct Ring {
     __device__ __forceinline__ uint32_t byte(uint64_t a) const { return buf[a & (RING - 1)]; }
 };
 
-template <typename S, typename L>
-__global__ void __launch_bounds__(DEC_WPB * 32) k_rans_dec_v2(DecParams p) {
-    const uint32_t b = blockIdx.y;
-    const scz_info& in = p.info[b];
-    if (p.status[b] != SCZ_OK || in.version != 2 || in.sym_bytes != sizeof(S)) return;
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint8_t* rings = smem;                                        // DEC_WPB * RING
-    uint2* s_tab = reinterpret_cast<uint2*>(smem + DEC_WPB * RING); // A entries (if fits)
-    const uint32_t A = in.alphabet;
-    const int n = in.precision;
-    const uint32_t nslots = 1u << n;
-    const bool tab_smem = A <= TAB_SMEM_MAX;
-    L* lut = reinterpret_cast<L*>(smem + DEC_WPB * RING + (tab_smem ? A : 0) * sizeof(uint2));
-    const uint32_t* f = p.freqs + in.freqs_off;
-    const uint32_t* cum = p.cumtab + (uint64_t)b * (p.acap + 1);
-    if (tab_smem)
-        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) s_tab[i] = make_uint2(f[i], cum[i]);
-    if constexpr (sizeof(L) < 4) build_lut<L>(lut, cum, A, nslots);
-    __syncthreads();
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t blk = blockIdx.x * DEC_WPB + warp;
-    if (blk >= in.n_blocks) return;
-    const uint64_t Ls = 2 * in.nnz + in.n_rows;
-    const uint64_t base = (uint64_t)blk * in.block_syms;
-    const uint32_t len = (uint32_t)min((uint64_t)in.block_syms, Ls - base);
-    const uint32_t blen = p.block_bytes[in.blocks_off + blk];
-    const uint64_t a0 = in.payload_off + p.blk_off[(uint64_t)b * p.nblk_cap + blk];
-    Ring ring{rings + warp * RING, a0 & ~127ull};
-    ring.fill_to(p.payload, a0 + 128 + 64, lane);
-    uint32_t x = ring.byte(a0 + 4 * lane) | (ring.byte(a0 + 4 * lane + 1) << 8) |
-                 (ring.byte(a0 + 4 * lane + 2) << 16) | (ring.byte(a0 + 4 * lane + 3) << 24);
-    uint64_t cur = a0 + 128;
-    uint32_t pos = 128;
-    const uint32_t mask = nslots - 1;
-    const uint32_t ltm = lanemask_lt();
-    S* out = reinterpret_cast<S*>(p.dsym) + (uint64_t)b * p.dsym_stride + base;
-    const uint32_t steps = (len + 31) / 32;
-    bool bad = false;
-    for (uint32_t s = 0; s < steps; ++s) {
-        const uint32_t i = s * 32 + lane;
-        const bool active = i < len;
-        uint32_t cnt = 0, sym = 0;
-        if (active) {
-            const uint32_t slot = x & mask;
-            sym = lookup<L>(lut, cum, A, slot);
-            uint2 fc = tab_smem ? s_tab[sym] : make_uint2(f[sym], cum[sym]);
-            x = fc.x * (x >> n) + slot - fc.y;
-            cnt = (x < (1u << 15)) ? 2u : ((x < STATE_LOW) ? 1u : 0u);
-        }
-        const uint32_t b1 = __ballot_sync(0xffffffffu, cnt >= 1);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, cnt == 2);
-        const uint32_t tot = __popc(b1) + __popc(b2);
-        if (pos + tot > blen) {  // rans.py:203-205 underrun
-            bad = true;
-            break;
-        }
-        const uint64_t a = cur + __popc(b1 & ltm) + __popc(b2 & ltm);
-        if (cnt >= 1) x = (x << 8) | ring.byte(a);
-        if (cnt == 2) x = (x << 8) | ring.byte(a + 1);
-        cur += tot;
-        pos += tot;
-        if (active) out[i] = (S)sym;
-        ring.fill_to(p.payload, cur + 64, lane);
-    }
-    // rans.py:211-212: every lane back at L and every byte consumed
-    if (!bad) bad = __any_sync(0xffffffffu, x != STATE_LOW) || pos != blen;
-    if (bad && lane == 0) p.status[b] = SCZ_CORRUPT_STREAM;
-}
-
 // v1 decode: one warp per tensor, the serial rans.decode loop (all lanes
 // carry the same state; lane 0 stores).  Generic lookup (binary search) when
 // the table does not fit a LUT.
@@ -446,16 +310,13 @@ __global__ void __launch_bounds__(32) k_rans_dec_v1(DecParams p) {
     if (bad && lane == 0) p.status[b] = SCZ_CORRUPT_STREAM;
 }
 
-#define SCZ_INST_DEC(S, L)                                     \
-    template __global__ void k_rans_dec_v2<S, L>(DecParams);   \
-    template __global__ void k_rans_dec_v1<S, L>(DecParams);
+#define SCZ_INST_DEC(S, L) template __global__ void k_rans_dec_v1<S, L>(DecParams);
 SCZ_INST_DEC(uint8_t, uint8_t)
 SCZ_INST_DEC(uint16_t, uint16_t)
 SCZ_INST_DEC(uint32_t, uint32_t)
 
-#define SCZ_INST_ENC(SRC)                                            \
-    template __global__ void k_rans_enc_v2<SRC>(EncParams, SRC);     \
-    template __global__ void k_rans_enc_v1<SRC>(EncParams, SRC);
+#define SCZ_INST_ENC(SRC) template __global__ void k_rans_enc_v1<SRC>(EncParams, SRC);
+SCZ_INST_ENC(Contig8Src)
 SCZ_INST_ENC(SplitSrc<uint8_t>)
 SCZ_INST_ENC(SplitSrc<uint16_t>)
 SCZ_INST_ENC(SplitSrc<uint32_t>)

@@ -1,0 +1,188 @@
+// rans_enc.cu -- v2 interleaved-lane rANS encoder (K5).
+//
+// One warp codes one FORMAT.md v2 block; lane j owns state j and the
+// block-local symbols i = j (mod 32).  Steps run in descending order; per
+// step every lane renormalises (<= 2 bytes, rans.py:139-142), the warp places
+// the bytes with one ballot-scan (lanes descending, low byte first), and the
+// state transform uses the exact reciprocal of the frequency.
+// Symbols are fetched 8 steps ahead into a rotating register queue (they do
+// not depend on the state); the per-symbol table lives in shared memory.
+// Emitted bytes are written backwards from the end of the block's slot, so
+// the finished block is contiguous: [32 LE states][bytes in decoder order].
+//
+// Only the highest step of a block can be partial, so it is peeled; the
+// remaining steps are full and branch-free.  CHECK adds the reference's
+// AlphabetOverflow / UncodableSymbol detection (rans.py:176-179, 189-190) for
+// caller-supplied tables (stage API); the pipeline's own tables cannot fail.
+#include "common.cuh"
+
+namespace scz {
+
+constexpr int ENC2_WPB = 4;                  // warps (= blocks) per CTA
+constexpr uint32_t ENC_TAB_SMEM_MAX = 8192;  // table entries staged in smem (128 KB)
+
+template <typename S>
+struct SplitCursor {
+    const uint8_t* v;
+    const S* c;
+    uint32_t split;
+    __device__ __forceinline__ uint32_t at(uint32_t i) const {
+        return i < split ? (uint32_t)__ldg(v + i) : (uint32_t)__ldg(c + i);
+    }
+};
+struct PlainCursor {
+    const uint32_t* d;
+    __device__ __forceinline__ uint32_t at(uint32_t i) const { return __ldg(d + i); }
+};
+
+template <typename S>
+__device__ __forceinline__ SplitCursor<S> make_cursor(const SplitSrc<S>& src, uint32_t b, uint64_t base,
+                                                      uint64_t nnz, uint32_t len) {
+    SplitCursor<S> k;
+    k.v = src.v8 + b * src.v8_stride + base;
+    // c[i] addresses cr[base + i - nnz]; formed as an integer to allow base < nnz
+    k.c = reinterpret_cast<const S*>(reinterpret_cast<uintptr_t>(src.cr + b * src.cr_stride) +
+                                     (int64_t)(base - nnz) * (int64_t)sizeof(S));
+    const uint64_t rest = base >= nnz ? 0 : nnz - base;
+    k.split = (uint32_t)(rest < len ? rest : len);
+    return k;
+}
+__device__ __forceinline__ PlainCursor make_cursor(const PlainSrc& src, uint32_t b, uint64_t base, uint64_t,
+                                                   uint32_t) {
+    return PlainCursor{src.d + b * src.stride + base};
+}
+struct Byte8Cursor {
+    const uint8_t* d;
+    __device__ __forceinline__ uint32_t at(uint32_t i) const { return __ldg(d + i); }
+};
+__device__ __forceinline__ Byte8Cursor make_cursor(const Contig8Src& src, uint32_t b, uint64_t base, uint64_t,
+                                                   uint32_t) {
+    return Byte8Cursor{src.d + b * src.stride + base};
+}
+
+struct EncLane {
+    uint32_t x;
+    uint32_t emitted;  // bytes emitted by the warp so far (warp-uniform)
+    uint32_t err;
+};
+
+// One step for one lane.  `live` false keeps the lane idle (partial step).
+template <bool SMEM, bool CHECK>
+__device__ __forceinline__ void enc_step(EncLane& L, uint32_t sym, bool live, const EncTab* s_tab,
+                                         const EncTab* gt, uint32_t A, int n, int sh_bound, uint32_t gtm,
+                                         uint8_t* slot_end) {
+    EncTab t = {1u, 0u, 0u, 0xFFFFFFFFu};
+    if (CHECK) {
+        if (live && sym >= A) {
+            L.err |= 1u;
+            live = false;
+        }
+    }
+    if (live || !CHECK) {
+        if constexpr (SMEM) {
+            t = s_tab[live ? sym : 0];
+        } else {
+            const uint4 g = __ldg(reinterpret_cast<const uint4*>(gt) + (live ? sym : 0));
+            t = EncTab{g.x, g.y, g.z, g.w};
+        }
+    }
+    if (CHECK) {
+        if (live && t.freq == 0) {
+            L.err |= 2u;
+            live = false;
+        }
+    }
+    const uint32_t bound = t.freq << sh_bound;  // ((L >> n) << 8) * f
+    const bool e1 = live && L.x >= bound;
+    const bool e2 = live && (L.x >> 8) >= bound;
+    const uint32_t b1 = __ballot_sync(0xffffffffu, e1);
+    const uint32_t b2 = __ballot_sync(0xffffffffu, e2);
+    const uint32_t pos = L.emitted + __popc(b1 & gtm) + __popc(b2 & gtm) + 1;
+    if (e1) slot_end[-(int32_t)pos] = (uint8_t)L.x;
+    if (e2) slot_end[-(int32_t)pos - 1] = (uint8_t)(L.x >> 8);
+    L.emitted += __popc(b1) + __popc(b2);
+    uint32_t x = L.x >> ((e1 ? 8u : 0u) + (e2 ? 8u : 0u));
+    const uint32_t q = (t.shift == 0xFFFFFFFFu) ? x : (__umulhi(x, t.rcp) >> t.shift);
+    x = (q << n) + t.cum + (x - q * t.freq);
+    if (live) L.x = x;
+}
+
+template <class Src, bool SMEM, bool CHECK>
+__global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src src) {
+    const uint32_t b = blockIdx.y;
+    TensorState& st = p.state[b];
+    if (st.status != SCZ_OK) return;
+    if (Src::width && st.sym_bytes != (uint32_t)Src::width) return;  // other width variant
+    const uint64_t L = st.stream_len;
+    const uint32_t nblk = L ? ceil_div_u32(L, p.block_syms) : 1;
+    const uint32_t blk0 = blockIdx.x * ENC2_WPB;
+    if (blk0 >= nblk) return;
+    extern __shared__ EncTab s_tab[];  // A entries when SMEM (host: A <= p.tab_smem)
+    const uint32_t A = st.alphabet;
+    const EncTab* gt = p.enctab + (uint64_t)b * p.acap;
+    if constexpr (SMEM) {
+        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) s_tab[i] = gt[i];
+        __syncthreads();
+    }
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t blk = blk0 + warp;
+    if (blk >= nblk) return;
+    const uint64_t base = (uint64_t)blk * p.block_syms;
+    const uint32_t len = (uint32_t)min((uint64_t)p.block_syms, L - base);
+    const auto cur = make_cursor(src, b, base, st.nnz, len);
+    const int steps = (int)((len + 31) / 32);
+    const int n = p.precision, sh_bound = 31 - n;
+    const uint32_t gtm = lanemask_gt();
+    uint8_t* slot_end = p.slots + ((uint64_t)b * p.slots_per_tensor + blk + 1) * p.slot_cap;
+    EncLane E{STATE_LOW, 0u, 0u};
+    if (steps > 0) {
+        // the highest step may be partial: peel it
+        const int s_top = steps - 1;
+        const uint32_t i_top = (uint32_t)s_top * 32 + lane;
+        const bool act = i_top < len;
+        // queue of the next 8 (full) steps' symbols: q[k] = step s_top - 1 - k
+        uint32_t q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int s = s_top - 1 - k;
+            q[k] = s >= 0 ? cur.at((uint32_t)s * 32 + lane) : 0u;
+        }
+        enc_step<SMEM, CHECK>(E, act ? cur.at(i_top) : 0u, act, s_tab, gt, A, n, sh_bound, gtm, slot_end);
+        int s0 = s_top - 1;  // next step to code; q[k] holds step s0 - k
+        for (; s0 >= 7; s0 -= 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t sym = q[k];
+                const int sp = s0 - k - 8;  // clamped: a harmless in-block load when sp < 0
+                q[k] = cur.at((uint32_t)max(sp, 0) * 32 + lane);
+                enc_step<SMEM, CHECK>(E, sym, true, s_tab, gt, A, n, sh_bound, gtm, slot_end);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k <= s0) enc_step<SMEM, CHECK>(E, q[k], true, s_tab, gt, A, n, sh_bound, gtm, slot_end);
+    }
+    // block bytes: 32 little-endian states, then the emitted bytes (decoder order)
+    const uint32_t blen = 4 * 32 + E.emitted;
+    uint8_t* start = slot_end - blen;
+    start[4 * lane + 0] = (uint8_t)E.x;
+    start[4 * lane + 1] = (uint8_t)(E.x >> 8);
+    start[4 * lane + 2] = (uint8_t)(E.x >> 16);
+    start[4 * lane + 3] = (uint8_t)(E.x >> 24);
+    if (CHECK) E.err = __reduce_or_sync(0xffffffffu, E.err);
+    if (lane == 0) {
+        p.block_len[(uint64_t)b * p.slots_per_tensor + blk] = blen;
+        if (CHECK && E.err) atomicOr(&st.errbits, E.err);
+    }
+}
+
+#define SCZ_INST_ENC2(SRC, CHK)                                                  \
+    template __global__ void k_rans_enc_v2<SRC, true, CHK>(EncParams, SRC);     \
+    template __global__ void k_rans_enc_v2<SRC, false, CHK>(EncParams, SRC);
+SCZ_INST_ENC2(Contig8Src, false)
+SCZ_INST_ENC2(SplitSrc<uint8_t>, false)
+SCZ_INST_ENC2(SplitSrc<uint16_t>, false)
+SCZ_INST_ENC2(SplitSrc<uint32_t>, false)
+SCZ_INST_ENC2(PlainSrc, true)
+
+}  // namespace scz

@@ -66,6 +66,36 @@ __device__ double pairwise_sum(const double* a, uint32_t n) {
     return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
 }
 
+// The same order, recursion unrolled at compile time (no stack frame) for
+// n <= 128 * 2^D; used on the search path where n <= 1024.
+template <int D>
+__device__ __forceinline__ double pairwise_sum_d(const double* a, uint32_t n) {
+    if (D == 0 || n <= 128) {
+        if (n < 8) {
+            double r = 0.0;
+            for (uint32_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+            return r;
+        }
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        uint32_t i;
+        for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        }
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
+    } else {
+        uint32_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return __dadd_rn(pairwise_sum_d<(D > 0 ? D - 1 : 0)>(a, n2),
+                         pairwise_sum_d<(D > 0 ? D - 1 : 0)>(a + n2, n - n2));
+    }
+}
+
 struct BlockScratch {
     uint32_t scan[33];
     uint32_t hist[256];
@@ -75,6 +105,7 @@ struct BlockScratch {
     double costs[MAX_CAND];
     double ents[MAX_CAND];
     uint32_t alph[MAX_CAND];
+    unsigned long long keys[1024];  // remainder keys for the small-alphabet ranking
 };
 
 __device__ unsigned long long block_sum64(unsigned long long v, BlockScratch& s) {
@@ -134,6 +165,20 @@ __device__ int block_normalize(const uint32_t* counts, uint32_t A, int precision
         unsigned long long k = (unsigned long long)deficit;
         if (k >= A) {
             for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) freqs[i] += 1;
+        } else if (A <= 1024) {
+            // small alphabets: rank every symbol against all others in one pass
+            for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS)
+                s.keys[i] = (unsigned long long)__double_as_longlong(rem[i]);
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+                const unsigned long long ki = s.keys[i];
+                uint32_t rank = 0;
+                for (uint32_t j = 0; j < A; ++j) {
+                    const unsigned long long kj = s.keys[j];
+                    rank += (kj > ki) || (kj == ki && j < i);
+                }
+                if (rank < k) freqs[i] += 1;
+            }
         } else {
             for (int shift = 56; shift >= 0; shift -= 8) {
                 for (int i = threadIdx.x; i < 256; i += SEL_THREADS) s.hist[i] = 0;
@@ -299,6 +344,114 @@ __device__ double block_entropy(const uint32_t* counts, uint32_t A, double total
     return s_h;
 }
 
+// Candidate pricing with one warp per candidate (search path, A <= 1024):
+// dynamic smem = [H_P if it fits][per warp: counts u32[acap], terms f64[acap]].
+constexpr uint32_t SEL_WARP_ACAP = 1024;
+constexpr uint32_t SEL_HP_SMEM_MAX = 16384;  // H_P entries staged in smem (64 KB)
+
+__host__ __device__ inline size_t select_smem_bytes(uint32_t acap, uint32_t period) {
+    if (acap > SEL_WARP_ACAP) return 0;
+    size_t s = (size_t)(SEL_THREADS / 32) * acap * (4 + 8);
+    if (period <= SEL_HP_SMEM_MAX) s += (size_t)period * 4;
+    return (s + 15) & ~(size_t)15;
+}
+
+__device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScratch& s) {
+    extern __shared__ __align__(16) uint8_t sel_dyn[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const TensorState& st = p.state[b];
+    const uint64_t nnz = st.nnz;
+    const uint32_t P = p.period;
+    const bool hp_smem = P <= SEL_HP_SMEM_MAX;
+    const uint32_t* ghp = p.hp + (uint64_t)b * p.hp_stride;
+    uint8_t* dyn = sel_dyn;
+    uint32_t* s_hp = reinterpret_cast<uint32_t*>(dyn);
+    if (hp_smem) {
+        for (uint32_t i = threadIdx.x; i < P; i += SEL_THREADS) s_hp[i] = ghp[i];
+        dyn += (((size_t)P * 4 + 15) & ~(size_t)15);
+    }
+    __syncthreads();
+    const uint32_t* hp = hp_smem ? s_hp : ghp;
+    double* terms = reinterpret_cast<double*>(dyn) + (size_t)warp * p.acap;
+    uint32_t* cb = reinterpret_cast<uint32_t*>(dyn + (size_t)(SEL_THREADS / 32) * p.acap * 8) +
+                   (size_t)warp * p.acap;
+    const uint32_t nv = 1u << p.q_bits;
+    const uint32_t* vh = p.vhist + (uint64_t)b * 256;
+    for (uint32_t c = warp; c < p.n_cand; c += SEL_THREADS / 32) {
+        const uint32_t K = p.cand_k[c], N = p.cand_n[c];
+        const uint32_t ub = max(nv, K + 1);
+        const uint32_t* rh = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c];
+        for (uint32_t i = lane; i < ub; i += 32) {
+            uint32_t v = (i < nv) ? vh[i] : 0;
+            if (K == 1) {
+                if (i == 0) v += N;             // nnz column-0 entries + (N - nnz) empty rows
+                if (i == 1) v += (uint32_t)nnz;  // full rows
+            } else if (i <= K) {
+                v += rh[i];
+            }
+            cb[i] = v;
+        }
+        __syncwarp();
+        if (K > 1) {  // column histogram: fold H_P (p mod P) onto p mod K
+            if (K <= 32) {
+                const uint32_t Lw = K * (32 / K);
+                if (lane < Lw) {
+                    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // 4 independent chains
+                    uint32_t j = lane;
+                    for (; j + 3 * Lw < P; j += 4 * Lw) {
+                        a0 += hp[j];
+                        a1 += hp[j + Lw];
+                        a2 += hp[j + 2 * Lw];
+                        a3 += hp[j + 3 * Lw];
+                    }
+                    for (; j < P; j += Lw) a0 += hp[j];
+                    const uint32_t acc = a0 + a1 + a2 + a3;
+                    if (acc) atomicAdd(&cb[lane % K], acc);
+                }
+            } else {
+                for (uint32_t col = lane; col < K; col += 32) {
+                    uint32_t acc = 0;
+                    for (uint32_t j = col; j < P; j += K) acc += hp[j];
+                    cb[col] += acc;
+                }
+            }
+        }
+        __syncwarp();
+        uint32_t last = 0;
+        for (uint32_t i = lane; i < ub; i += 32)
+            if (cb[i]) last = i + 1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+        const uint32_t A = last;
+        if (p.dump) {
+            uint32_t* dd = p.dump + ((uint64_t)b * p.n_cand + c) * p.acap;
+            for (uint32_t i = lane; i < p.acap; i += 32) dd[i] = i < A ? cb[i] : 0;
+        }
+        // entropy over the positive counts in index order (rans.py:219-223)
+        const uint64_t len = 2 * nnz + N;
+        const double total = (double)len;
+        uint32_t m = 0;
+        for (uint32_t base = 0; base < A; base += 32) {
+            const uint32_t i = base + lane;
+            const uint32_t cnt = i < A ? cb[i] : 0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, cnt > 0);
+            if (cnt > 0) {
+                const double pp = __ddiv_rn((double)cnt, total);
+                terms[m + __popc(bal & lanemask_lt())] = __dmul_rn(pp, log2(pp));
+            }
+            m += __popc(bal);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const double h = -(m <= 1024 ? pairwise_sum_d<3>(terms, m) : pairwise_sum(terms, m));
+            s.ents[c] = h;
+            s.costs[c] = __dmul_rn((double)len, h);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
     const uint32_t b = blockIdx.x;
     TensorState& st = p.state[b];
@@ -310,7 +463,8 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
 
     uint32_t chosen = 0, flags = 0, evaluated = 0;
     if (p.searching) {
-        for (uint32_t c = 0; c < p.n_cand; ++c) {
+        if (p.acap <= SEL_WARP_ACAP) warp_parallel_costs(p, b, s);
+        else for (uint32_t c = 0; c < p.n_cand; ++c) {
             uint32_t A = assemble_counts(p, b, c, counts, s);
             if (p.dump) {
                 uint32_t* dd = p.dump + ((uint64_t)b * p.n_cand + c) * p.acap;
