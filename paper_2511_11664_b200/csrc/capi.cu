@@ -140,7 +140,7 @@ struct scz_ctx {
     int32_t* h_status_async = nullptr;
     uint32_t last_batch = 0;
     HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
-    DevBuf ready;
+    DevBuf ready, candcnt;
     uint32_t front_grid = 0;  // co-resident CTAs of k_front (0 = not queried)
     bool use_front = getenv("SCZ_FUSED_FRONT") != nullptr;  // experimental (slower today)
 
@@ -509,7 +509,12 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         cp.n_words = ceil_div_u32(T, 32);
         cp.period_words = (uint32_t)(pl.period / 32);
         cp.n_rows = ceil_div_u32(cp.n_words, cp.period_words);
-        cp.rows_per_cta = 64;
+        {   // enough CTAs to fill the GPU even for a single tensor
+            const uint64_t gx = ceil_div_u32(cp.period_words, 128);
+            const uint64_t want_gy = (296 + gx * B - 1) / (gx * B);
+            uint32_t rpc = ceil_div_u32(cp.n_rows, want_gy);
+            cp.rows_per_cta = std::max(1u, std::min(64u, rpc));
+        }
         cp.hp = ctx->hp.as<uint32_t>();
         cp.hp_stride = (uint32_t)pl.period;
         dim3 g(ceil_div_u32(cp.period_words, 128), ceil_div_u32(cp.n_rows, cp.rows_per_cta), B);
@@ -545,8 +550,6 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
             size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
             k_rowhist2<<<dim3(chunks, B), RH_THREADS, smem, s>>>(rp);
             LAUNCHED("k_rowhist");
-            k_rowhist_zero<<<B, 64, 0, s>>>(rp);
-            LAUNCHED("k_rowhist_zero");
         }
     }
 
@@ -576,6 +579,10 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     sel.cum = ctx->cum.as<uint32_t>();
     sel.enctab = ctx->enctab.as<EncTab>();
     sel.cand_out = cand_out;
+    if (!dump && pl.searching) {  // per-candidate histograms stay on device for the chosen table
+        CK(ctx->candcnt.ensure((size_t)B * ncand * pl.acap * 4));
+        dump = ctx->candcnt.as<uint32_t>();
+    }
     sel.dump = dump;
     const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)pl.period) : 0;
     if (sel_smem > 48 * 1024)
@@ -678,7 +685,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     scz_info* hi = ctx->h_misc.as<scz_info>();
     uint64_t* hoff = reinterpret_cast<uint64_t*>(hi + B);
     int32_t* hst = reinterpret_cast<int32_t*>(hoff + B);
-    uint32_t acap = 1, nblk_cap = 1, nchunk_cap = 1, widths = 0;
+    uint32_t acap = 1, nblk_cap = 1, nchunk_cap = 1, widths = 0, maxK = 1;
     uint64_t Lmax = 1, off = 0, maxA = 1;
     int maxn = 1;
     for (uint32_t b = 0; b < B; ++b) {
@@ -691,6 +698,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         nblk_cap = std::max(nblk_cap, hi[b].version == 2 ? hi[b].n_blocks : 1u);
         Lmax = std::max<uint64_t>(Lmax, 2 * hi[b].nnz + hi[b].n_rows);
         nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, rows_per_chunk(hi[b].n_cols)));
+        maxK = std::max(maxK, hi[b].n_cols);
         maxn = std::max(maxn, (int)hi[b].precision);
         hoff[b] = off;
         off += hi[b].total;
@@ -747,9 +755,19 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     LAUNCHED("k_row_scan");
     auto rows_out = [&](auto tag) -> int {
         using S = decltype(tag);
-        if (stage) k_rows_out<S, true><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
-        else k_rows_out<S, false><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
-        LAUNCHED(wname<S>("k_rows_out"));
+        if (stage) {
+            k_rows_out<S, true><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+            LAUNCHED(wname<S>("k_rows_out"));
+        } else {
+            if constexpr (sizeof(S) <= 2) {
+                k_rows_fast<S><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                LAUNCHED(wname<S>("k_rows_out"));
+            }
+            if (sizeof(S) > 2 || maxK > (uint32_t)OUT_ELEMS) {
+                k_rows_out<S, false><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                LAUNCHED("k_rows_out/general");
+            }
+        }
         return SCZ_OK;
     };
     if (widths & 1) { if ((st = rows_out(uint8_t{})) != SCZ_OK) return st; }
@@ -803,7 +821,7 @@ void scz_ctx_destroy(scz_ctx* ctx) {
                       &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
                       &ctx->info, &ctx->payload, &ctx->ticket, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
                       &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
-                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready})
+                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready, &ctx->candcnt})
         b->release();
     for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
                        &ctx->h_misc})

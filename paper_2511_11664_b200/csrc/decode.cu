@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
     const uint32_t K = in.n_cols;
+    if (!STAGE && sizeof(S) <= 2 && K <= (uint32_t)OUT_ELEMS) return;  // k_rows_fast's case
     const uint32_t R = rows_per_chunk(K);
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
@@ -203,6 +204,97 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
         }
     }
 }
+
+// Fast path of k_rows_out for u8/u16 symbols and K <= OUT_ELEMS (the search
+// path and every BASELINE config): the chunk's columns and values are staged
+// with coalesced loads, rows are scattered into a zeroed shared tile, and the
+// tile is written back with 16-byte stores.  Static shared arrays only.
+template <typename S>
+__global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
+    const uint32_t b = blockIdx.y, chunk = blockIdx.x;
+    const scz_info& in = p.info[b];
+    if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
+    const uint32_t K = in.n_cols;
+    if (K > (uint32_t)OUT_ELEMS) return;  // k_rows_out handles these
+    const uint32_t R = rows_per_chunk(K);
+    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
+    if (r0 >= N) return;
+    const uint64_t nnz = in.nnz;
+    const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    __shared__ uint32_t s_off[ROW_CHUNK];
+    __shared__ __align__(16) float s_out[OUT_ELEMS];
+    __shared__ S s_c[OUT_ELEMS], s_v[OUT_ELEMS];
+    __shared__ uint32_t s_scan[33];
+    __shared__ float s_lut[256];
+    __shared__ int s_bad;
+    const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
+    const uint32_t nq = in.q_bits <= 8 ? (1u << in.q_bits) : 256u;
+    for (uint32_t i = threadIdx.x; i < nq; i += ROW_THREADS)
+        s_lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, (double)in.zero_point), in.scale));
+    if (threadIdx.x == 0) s_bad = 0;
+    constexpr int PER = ROW_CHUNK / ROW_THREADS;
+    uint32_t loc[PER], sum = 0;
+    const S* rc = d + 2 * nnz + r0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t i = threadIdx.x * PER + j;
+        loc[j] = i < nrow ? (uint32_t)rc[i] : 0u;
+        sum += loc[j];
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
+    const uint32_t cbase = p.chunk_sum[(uint64_t)b * p.nchunk_cap + chunk];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        s_off[threadIdx.x * PER + j] = ex;  // chunk-local offset
+        ex += loc[j];
+    }
+    const uint32_t n_el = nrow * K;
+    for (uint32_t i = threadIdx.x; i < OUT_ELEMS / 4; i += ROW_THREADS)
+        reinterpret_cast<float4*>(s_out)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const S* gc = d + nnz + cbase;
+    const S* gv = d + cbase;
+    for (uint32_t i = threadIdx.x; i < tot; i += ROW_THREADS) {  // tot <= nrow * K (row_sums checked r <= K)
+        s_c[i] = gc[i];
+        s_v[i] = gv[i];
+    }
+    __syncthreads();
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t li = threadIdx.x * PER + j;  // this thread's rows (their counts are in loc[])
+        if (li >= nrow) break;
+        const uint32_t off = s_off[li], r = loc[j];
+        uint32_t prev = 0;
+        for (uint32_t e = 0; e < r; ++e) {
+            const uint32_t c = s_c[off + e];
+            bad |= (c >= K) | ((e > 0) & (c <= prev));  // sparse.py:90-97
+            prev = c;
+            const uint32_t v = s_v[off + e];
+            const float o = v < nq ? s_lut[v]
+                                   : __double2float_rn(__dmul_rn(
+                                         __dsub_rn((double)v, (double)in.zero_point), in.scale));
+            if (c < K) s_out[li * K + c] = o;
+        }
+    }
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (s_bad) {
+        if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+        return;
+    }
+    float* ochunk = p.out + p.out_off[b] + r0 * K;
+    if ((reinterpret_cast<uintptr_t>(ochunk) & 15) == 0) {
+        const uint32_t n4 = n_el / 4;
+        for (uint32_t i = threadIdx.x; i < n4; i += ROW_THREADS)
+            reinterpret_cast<float4*>(ochunk)[i] = reinterpret_cast<const float4*>(s_out)[i];
+        for (uint32_t i = 4 * n4 + threadIdx.x; i < n_el; i += ROW_THREADS) ochunk[i] = s_out[i];
+    } else {
+        for (uint32_t i = threadIdx.x; i < n_el; i += ROW_THREADS) ochunk[i] = s_out[i];
+    }
+}
+template __global__ void k_rows_fast<uint8_t>(RowParams);
+template __global__ void k_rows_fast<uint16_t>(RowParams);
 
 #define SCZ_INST_ROWS(S)                                        \
     template __global__ void k_row_sums<S>(RowParams);          \

@@ -250,7 +250,7 @@ __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, i
     return quant_exact(x, scale, zf, (double)qmax);
 }
 
-__global__ void __launch_bounds__(TILE_THREADS) k_quantize(QuantParams p) {
+__global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const TensorState& st = p.state[b];

@@ -105,6 +105,7 @@ struct BlockScratch {
     double costs[MAX_CAND];
     double ents[MAX_CAND];
     uint32_t alph[MAX_CAND];
+    uint32_t acnt[MAX_CAND];        // alphabet of every priced candidate (warp path)
     unsigned long long keys[1024];  // remainder keys for the small-alphabet ranking
 };
 
@@ -285,11 +286,18 @@ __device__ uint32_t assemble_counts(const SelectParams& p, uint32_t b, uint32_t 
     const uint32_t ubound = max(nv, K + 1);
     const uint32_t* vh = p.vhist + (uint64_t)b * 256;
     const uint32_t* rh = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c];
+    // rows with r = 0: N minus the rows counted in bins 1..K (k_rowhist2 skips 0)
+    unsigned long long rsum = 0;
+    if (K > 1)
+        for (uint32_t i = 1 + threadIdx.x; i <= K; i += SEL_THREADS) rsum += rh[i];
+    rsum = block_sum64(rsum, s);
     for (uint32_t i = threadIdx.x; i < ubound; i += SEL_THREADS) {
         uint32_t v = (i < nv) ? vh[i] : 0;
         if (K == 1) {
             if (i == 0) v += (uint32_t)(N - nnz) + (uint32_t)nnz;  // c = 0 for all, r = 0 rows
             if (i == 1) v += (uint32_t)nnz;                      // r = 1 rows
+        } else if (i == 0) {
+            v += N - (uint32_t)rsum;
         } else if (i <= K) {
             v += rh[i];
         }
@@ -381,11 +389,17 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScra
         const uint32_t K = p.cand_k[c], N = p.cand_n[c];
         const uint32_t ub = max(nv, K + 1);
         const uint32_t* rh = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c];
+        uint32_t rsum = 0;  // rows with r >= 1 (bin 0 is N - rsum)
+        if (K > 1)
+            for (uint32_t i = 1 + lane; i <= K; i += 32) rsum += rh[i];
+        rsum = warp_sum(rsum);
         for (uint32_t i = lane; i < ub; i += 32) {
             uint32_t v = (i < nv) ? vh[i] : 0;
             if (K == 1) {
                 if (i == 0) v += N;             // nnz column-0 entries + (N - nnz) empty rows
                 if (i == 1) v += (uint32_t)nnz;  // full rows
+            } else if (i == 0) {
+                v += N - rsum;
             } else if (i <= K) {
                 v += rh[i];
             }
@@ -423,10 +437,11 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScra
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
         const uint32_t A = last;
-        if (p.dump) {
+        if (p.dump) {  // kept for the chosen candidate's table (and scz_search)
             uint32_t* dd = p.dump + ((uint64_t)b * p.n_cand + c) * p.acap;
             for (uint32_t i = lane; i < p.acap; i += 32) dd[i] = i < A ? cb[i] : 0;
         }
+        if (lane == 0) s.acnt[c] = A;
         // entropy over the positive counts in index order (rans.py:219-223)
         const uint64_t len = 2 * nnz + N;
         const double total = (double)len;
@@ -522,10 +537,17 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
         __syncthreads();
     }
     // chosen candidate: histogram -> normalised table -> encoder table
-    uint32_t A = assemble_counts(p, b, chosen, counts, s);
+    uint32_t A;
+    const uint32_t* ccounts = counts;
+    if (p.searching && p.acap <= SEL_WARP_ACAP && p.dump) {  // already assembled by its warp
+        A = s.acnt[chosen];
+        ccounts = p.dump + ((uint64_t)b * p.n_cand + chosen) * p.acap;
+    } else {
+        A = assemble_counts(p, b, chosen, counts, s);
+    }
     uint32_t* freqs = p.freqs + (uint64_t)b * p.acap;
     uint32_t* cum = p.cum + (uint64_t)b * (p.acap + 1);
-    int status = block_normalize(counts, A, p.precision, freqs, terms, cum, s);
+    int status = block_normalize(ccounts, A, p.precision, freqs, terms, cum, s);
     EncTab* et = p.enctab + (uint64_t)b * p.acap;
     if (status == SCZ_OK)
         for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) make_enc_tab(freqs[i], cum[i], &et[i]);
