@@ -685,7 +685,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     scz_info* hi = ctx->h_misc.as<scz_info>();
     uint64_t* hoff = reinterpret_cast<uint64_t*>(hi + B);
     int32_t* hst = reinterpret_cast<int32_t*>(hoff + B);
-    uint32_t acap = 1, nblk_cap = 1, nchunk_cap = 1, widths = 0, maxK = 1;
+    uint32_t acap = 1, nblk_cap = 1, nchunk_cap = 1, widths = 0, maxK = 1, kmask = 0;
     uint64_t Lmax = 1, off = 0, maxA = 1;
     int maxn = 1;
     for (uint32_t b = 0; b < B; ++b) {
@@ -699,6 +699,10 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         Lmax = std::max<uint64_t>(Lmax, 2 * hi[b].nnz + hi[b].n_rows);
         nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, rows_per_chunk(hi[b].n_cols)));
         maxK = std::max(maxK, hi[b].n_cols);
+        {   // which CSR-decode variants this batch needs (K 1 / 2 / 4 / other)
+            const uint32_t K = hi[b].n_cols;
+            kmask |= K == 1 ? 1u : (K == 2 ? 2u : (K == 4 ? 4u : 8u));
+        }
         maxn = std::max(maxn, (int)hi[b].precision);
         hoff[b] = off;
         off += hi[b].total;
@@ -760,8 +764,22 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
             LAUNCHED(wname<S>("k_rows_out"));
         } else {
             if constexpr (sizeof(S) <= 2) {
-                k_rows_fast<S><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
-                LAUNCHED(wname<S>("k_rows_out"));
+                if (kmask & 1u) {
+                    k_rows_small<S, 1><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    LAUNCHED(wname<S>("k_rows_out"));
+                }
+                if (kmask & 2u) {
+                    k_rows_small<S, 2><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    LAUNCHED(wname<S>("k_rows_out"));
+                }
+                if (kmask & 4u) {
+                    k_rows_small<S, 4><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    LAUNCHED(wname<S>("k_rows_out"));
+                }
+                if (kmask & 8u) {
+                    k_rows_fast<S><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    LAUNCHED(wname<S>("k_rows_out"));
+                }
             }
             if (sizeof(S) > 2 || maxK > (uint32_t)OUT_ELEMS) {
                 k_rows_out<S, false><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);

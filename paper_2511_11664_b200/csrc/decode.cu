@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
     const uint32_t K = in.n_cols;
-    if (K > (uint32_t)OUT_ELEMS) return;  // k_rows_out handles these
+    if (K > (uint32_t)OUT_ELEMS) return;       // k_rows_out handles these
+    if (K == 1 || K == 2 || K == 4) return;    // k_rows_small handles these
     const uint32_t R = rows_per_chunk(K);
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
@@ -295,6 +296,100 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
 }
 template __global__ void k_rows_fast<uint8_t>(RowParams);
 template __global__ void k_rows_fast<uint16_t>(RowParams);
+
+// K in {1, 2, 4} (every BASELINE shape picks one of these): a row is one
+// 4/8/16-byte vector assembled in registers from <= K independent,
+// predicated loads; consecutive threads own consecutive rows, so every store
+// instruction of a warp is one contiguous, coalesced span.
+template <typename S, int KK>
+__global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
+    const uint32_t b = blockIdx.y, chunk = blockIdx.x;
+    const scz_info& in = p.info[b];
+    if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S) || in.n_cols != (uint32_t)KK) return;
+    constexpr uint32_t R = (uint32_t)ROW_CHUNK;  // == rows_per_chunk(KK) for KK <= 4
+    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
+    if (r0 >= N) return;
+    const uint64_t nnz = in.nnz;
+    const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    __shared__ uint32_t s_off[ROW_CHUNK];
+    __shared__ uint8_t s_r[ROW_CHUNK];
+    __shared__ uint32_t s_scan[33];
+    __shared__ float s_lut[256];
+    __shared__ int s_bad;
+    const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
+    const uint32_t nq = in.q_bits <= 8 ? (1u << in.q_bits) : 256u;
+    for (uint32_t i = threadIdx.x; i < nq; i += ROW_THREADS)
+        s_lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, (double)in.zero_point), in.scale));
+    if (threadIdx.x == 0) s_bad = 0;
+    constexpr int PER = ROW_CHUNK / ROW_THREADS;
+    uint32_t loc[PER], sum = 0;
+    const S* rc = d + 2 * nnz + r0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t i = threadIdx.x * PER + j;
+        loc[j] = i < nrow ? (uint32_t)rc[i] : 0u;
+        sum += loc[j];
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot) +
+                  p.chunk_sum[(uint64_t)b * p.nchunk_cap + chunk];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        s_off[threadIdx.x * PER + j] = ex;
+        s_r[threadIdx.x * PER + j] = (uint8_t)loc[j];
+        ex += loc[j];
+    }
+    __syncthreads();
+    const S* cols = d + nnz;
+    float* orow0 = p.out + p.out_off[b] + r0 * KK;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t li = j * ROW_THREADS + threadIdx.x;
+        if (li >= nrow) break;
+        const uint32_t off = s_off[li], r = s_r[li];
+        uint32_t c[KK], v[KK];
+#pragma unroll
+        for (int e = 0; e < KK; ++e) {
+            c[e] = e < (int)r ? (uint32_t)cols[off + e] : 0xffffffffu;
+            v[e] = e < (int)r ? (uint32_t)d[off + e] : 0u;
+        }
+        float o[KK];
+#pragma unroll
+        for (int col = 0; col < KK; ++col) o[col] = 0.0f;
+#pragma unroll
+        for (int e = 0; e < KK; ++e) {
+            if (e < (int)r) {
+                bad |= (c[e] >= (uint32_t)KK) | (e > 0 && c[e] <= c[e > 0 ? e - 1 : 0]);  // sparse.py:90-97
+                const float val = v[e] < nq ? s_lut[v[e]]
+                                            : __double2float_rn(__dmul_rn(
+                                                  __dsub_rn((double)v[e], (double)in.zero_point), in.scale));
+#pragma unroll
+                for (int col = 0; col < KK; ++col)
+                    if (c[e] == (uint32_t)col) o[col] = val;
+            }
+        }
+        float* orow = orow0 + (uint64_t)li * KK;
+        if constexpr (KK == 4) {
+            if ((reinterpret_cast<uintptr_t>(orow) & 15) == 0) *reinterpret_cast<float4*>(orow) = make_float4(o[0], o[1], o[2], o[3]);
+            else { orow[0] = o[0]; orow[1] = o[1]; orow[2] = o[2]; orow[3] = o[3]; }
+        } else if constexpr (KK == 2) {
+            if ((reinterpret_cast<uintptr_t>(orow) & 7) == 0) *reinterpret_cast<float2*>(orow) = make_float2(o[0], o[1]);
+            else { orow[0] = o[0]; orow[1] = o[1]; }
+        } else {
+            orow[0] = o[0];
+        }
+    }
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_bad) p.status[b] = SCZ_CORRUPT_STREAM;
+}
+#define SCZ_INST_SMALL(S)                                      \
+    template __global__ void k_rows_small<S, 1>(RowParams);    \
+    template __global__ void k_rows_small<S, 2>(RowParams);    \
+    template __global__ void k_rows_small<S, 4>(RowParams);
+SCZ_INST_SMALL(uint8_t)
+SCZ_INST_SMALL(uint16_t)
 
 #define SCZ_INST_ROWS(S)                                        \
     template __global__ void k_row_sums<S>(RowParams);          \

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad + (uint64_t)tile * TILE_WORDS;
 
     __shared__ uint32_t s_wpre[TILE_WORDS];
+    __shared__ uint32_t s_wbits[TILE_WORDS];
     __shared__ uint32_t s_scan[33];
     __shared__ uint32_t s_hist[4][256];  // one copy per warp pair: less atomic contention
     const int nbins = 1 << p.q_bits;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     for (int it = 0; it < 8; ++it)
         vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &vvalid[it]);
     uint32_t myword = bm[threadIdx.x];
+    s_wbits[threadIdx.x] = myword;
     uint32_t tot;
     s_wpre[threadIdx.x] = block_exclusive_scan<TILE_THREADS>(__popc(myword), s_scan, &tot);
     // (block_exclusive_scan ends with __syncthreads)
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
         const float4 v = vv[it];
         float e[4] = {v.x, v.y, v.z, v.w};
         const int word = warp * 32 + it * 4 + (lane >> 3);
-        const uint32_t wbits = bm[word];
+        const uint32_t wbits = s_wbits[word];
         const int bit0 = 4 * (lane & 7);
         uint32_t rank = base_rank + s_wpre[word] + __popc(wbits & ((1u << bit0) - 1u));
 #pragma unroll
@@ -459,7 +461,14 @@ __global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
     const uint32_t base_rank = p.tile_off[(uint64_t)b * p.n_tiles + tile];
     // column index of every nonzero: p mod K (sparse.py:66-68)
     if (w) {
-        const uint32_t m = (uint32_t)((word * 32) % K);
+        // (32 * word) mod K without a 64-bit modulo: T < 2^31 so the fp64
+        // quotient estimate is within one of the truth
+        const uint32_t xw = (uint32_t)(word * 32);
+        uint32_t qk = __double2uint_rz(__dmul_rn((double)xw, __drcp_rn((double)K)));
+        int64_t rr = (int64_t)xw - (int64_t)qk * K;
+        if (rr < 0) rr += K;
+        if (rr >= K) rr -= K;
+        const uint32_t m = (uint32_t)rr;
         while (w) {
             const int bit = __ffs(w) - 1;
             w &= w - 1;

@@ -113,11 +113,14 @@ __global__ void __launch_bounds__(RH_THREADS) k_rowhist2(RowHist2Params p) {
             s_h[warp][v][lane] += 1;
         }
         __syncthreads();
-        for (uint32_t v = 1 + threadIdx.x; v <= K; v += RH_THREADS) {
+        // warp `warp` reduces bins warp, warp + 8, ...: lane l sums the 8 warp
+        // copies of its column, then a warp sum (no serial per-bin loops)
+        for (uint32_t v = 1 + warp; v <= K; v += RH_THREADS / 32) {
             uint32_t t = 0;
-            for (int wv = 0; wv < RH_THREADS / 32; ++wv)
-                for (int l = 0; l < 32; ++l) t += s_h[wv][v][l];
-            if (t) atomicAdd(gh + v, t);
+#pragma unroll
+            for (int wv = 0; wv < RH_THREADS / 32; ++wv) t += s_h[wv][v][lane];
+            t = warp_sum(t);
+            if (lane == 0 && t) atomicAdd(gh + v, t);
         }
         return;
     }
