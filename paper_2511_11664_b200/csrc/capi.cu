@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -26,6 +27,10 @@ using namespace scz;
 
 namespace {
 
+// Bumped by every device/pinned (re)allocation: cached CUDA graphs hold raw
+// pointers, so a graph captured under another generation is stale.
+std::atomic<uint64_t> g_alloc_gen{1};
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -37,6 +42,7 @@ struct DevBuf {
         size_t want = std::max<size_t>(n + n / 8, 4096);
         cudaError_t e = cudaMalloc(&p, want);
         if (e == cudaSuccess) cap = want;
+        g_alloc_gen.fetch_add(1);
         return e;
     }
     template <typename T>
@@ -59,6 +65,7 @@ struct HostBuf {
         size_t want = std::max<size_t>(n + n / 8, 4096);
         cudaError_t e = cudaMallocHost(&p, want);
         if (e == cudaSuccess) cap = want;
+        g_alloc_gen.fetch_add(1);
         return e;
     }
     template <typename T>
@@ -141,6 +148,17 @@ struct scz_ctx {
     uint32_t last_batch = 0;
     HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
     DevBuf ready, candcnt;
+    // CUDA-graph cache: a launch sequence seen twice with the same key and
+    // allocation generation is captured once and replayed afterwards.
+    struct Graph {
+        std::string key;
+        uint64_t gen = 0;
+        int seen = 0;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t nkern = 0;
+    };
+    std::vector<Graph> graphs;
+    bool use_graphs = getenv("SCZ_NO_GRAPHS") == nullptr;
     uint32_t front_grid = 0;  // co-resident CTAs of k_front (0 = not queried)
     bool use_front = getenv("SCZ_FUSED_FRONT") != nullptr;  // experimental (slower today)
 
@@ -424,6 +442,76 @@ __global__ void __launch_bounds__(256) k_pack(const scz_info* info, const uint8_
     for (uint32_t i = head + 4 * nwords + threadIdx.x; i < len; i += 256) dst[i] = src[i];
 }
 
+// Run `body` (stream-ordered launches only, no host syncs) through the graph
+// cache: first sighting eager, second sighting captured + instantiated, then
+// replayed.  Disabled while per-kernel timing is on.
+template <class F>
+int graph_run(scz_ctx* ctx, const std::string& key, F&& body) {
+    if (!ctx->use_graphs || ctx->timing) return body();
+    const uint64_t gen = g_alloc_gen.load();
+    scz_ctx::Graph* g = nullptr;
+    for (auto& e : ctx->graphs)
+        if (e.key == key) g = &e;
+    if (g && g->exec && g->gen == gen) {
+        CK(cudaGraphLaunch(g->exec, ctx->stream));
+        ctx->launches += g->nkern;
+        return SCZ_OK;
+    }
+    if (!g) {
+        if (ctx->graphs.size() >= 16) {  // small FIFO cache
+            if (ctx->graphs.front().exec) cudaGraphExecDestroy(ctx->graphs.front().exec);
+            ctx->graphs.erase(ctx->graphs.begin());
+        }
+        ctx->graphs.push_back(scz_ctx::Graph{key});
+        g = &ctx->graphs.back();
+    }
+    if (g->exec) {
+        cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+    }
+    if (!g->seen || g->gen != gen) {  // first sighting under this generation: eager
+        g->seen = 1;
+        int st = body();
+        g->gen = g_alloc_gen.load();
+        return st;
+    }
+    const uint64_t l0 = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    int st = body();
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+    if (st != SCZ_OK || ce != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        if (st != SCZ_OK) return st;
+        ctx->use_graphs = false;  // capture unsupported here: stay eager
+        return body();
+    }
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) {
+        cudaGetLastError();
+        ctx->use_graphs = false;
+        return body();
+    }
+    g->exec = exec;
+    g->gen = g_alloc_gen.load();
+    g->nkern = ctx->launches - l0;
+    CK(cudaGraphLaunch(exec, ctx->stream));
+    return SCZ_OK;
+}
+
+std::string key_of(const char* kind, std::initializer_list<uint64_t> vals) {
+    std::string k(kind);
+    char buf[24];
+    for (uint64_t v : vals) {
+        snprintf(buf, sizeof buf, "|%llx", (unsigned long long)v);
+        k += buf;
+    }
+    return k;
+}
+
 // The encode pipeline over a device batch.  cand_out (device) optional.
 int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_out,
                uint32_t* dump = nullptr) {
@@ -498,7 +586,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         QuantParams qp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
                        ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
                        ctx->vhist.as<uint32_t>(), nullptr, dstride};
-        k_quantize<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(qp);
+        k_quantize<false><<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(qp);
         LAUNCHED("k_quantize");
     }
 
@@ -844,6 +932,8 @@ void scz_ctx_destroy(scz_ctx* ctx) {
     for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
                        &ctx->h_misc})
         b->release();
+    for (auto& g : ctx->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -861,7 +951,10 @@ int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t ba
     EncPlan pl;
     int st = plan_encode(ctx, total, batch, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
     if (st) return st;
-    if ((st = run_encode(ctx, d_x, pl, nullptr)) != SCZ_OK) return st;
+    const std::string key = key_of("enc", {(uint64_t)(uintptr_t)d_x, total, batch, (uint64_t)q_bits,
+                                           (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format,
+                                           lanes, block_syms});
+    if ((st = graph_run(ctx, key, [&] { return run_encode(ctx, d_x, pl, nullptr); })) != SCZ_OK) return st;
     out->batch = batch;
     out->d_info = ctx->info.as<scz_info>();
     out->d_freqs = ctx->freqs.as<uint32_t>();
@@ -926,7 +1019,11 @@ int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64
     if (st) return st;
     CK(ctx->x_in.ensure(total * 4));
     CK(cudaMemcpyAsync(ctx->x_in.p, x, total * 4, cudaMemcpyHostToDevice, ctx->stream));
-    if ((st = run_encode(ctx, ctx->x_in.as<float>(), pl, nullptr)) != SCZ_OK) return st;
+    const std::string key = key_of("enc", {(uint64_t)(uintptr_t)ctx->x_in.p, total, 1, (uint64_t)q_bits,
+                                           (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format,
+                                           lanes, block_syms});
+    if ((st = graph_run(ctx, key, [&] { return run_encode(ctx, ctx->x_in.as<float>(), pl, nullptr); })) != SCZ_OK)
+        return st;
     CK(ctx->h_info.ensure(sizeof(scz_info)));
     CK(cudaMemcpyAsync(ctx->h_info.p, ctx->info.p, sizeof(scz_info), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1038,7 +1135,7 @@ int quantize_impl(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, bool giv
     QuantParams qp{ctx->x_in.as<float>(), n, ntiles, wp, q_bits, ctx->bitmap.as<uint32_t>(),
                    ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
                    ctx->vhist.as<uint32_t>(), qd, n};
-    k_quantize<<<dim3(ntiles, 1), TILE_THREADS, 0, s>>>(qp);
+    k_quantize<true><<<dim3(ntiles, 1), TILE_THREADS, 0, s>>>(qp);
     LAUNCHED("k_quantize");
     k_unpack_mask<<<ceil_div_u32(n, 256), 256, 0, s>>>(ctx->bitmap.as<uint32_t>(), n, md);
     LAUNCHED("k_unpack_mask");

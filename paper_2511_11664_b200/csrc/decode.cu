@@ -24,6 +24,22 @@ __host__ __device__ inline uint32_t rows_per_chunk(uint32_t K) {
     return r < 1 ? 1u : (r > (uint32_t)ROW_CHUNK ? (uint32_t)ROW_CHUNK : r);
 }
 
+// float32((float64(v) - z) * scale) (tensor.py:154).  The 256-entry LUT covers
+// every u8 symbol; wider symbols >= 256 (only in hand-made streams) take an
+// out-of-line fp64 path so it is never if-converted into the hot loop.
+__device__ __noinline__ float dequant_slow(uint32_t v, double z, double scale) {
+    return __double2float_rn(__dmul_rn(__dsub_rn((double)v, z), scale));
+}
+template <typename S>
+__device__ __forceinline__ float dequant(uint32_t v, const float* lut, double z, double scale) {
+    if constexpr (sizeof(S) == 1) return lut[v];
+    else return v < 256u ? lut[v] : dequant_slow(v, z, scale);
+}
+__device__ __forceinline__ void build_dequant_lut(float* lut, double z, double scale) {
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
+        lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, z), scale));
+}
+
 struct RowParams {
     const scz_info* info;   // [B]
     const void* dsym;       // [B][dsym_stride] decoded D
@@ -115,10 +131,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
     __shared__ S s_cs[STAGE_CV ? OUT_ELEMS : 1], s_vs[STAGE_CV ? OUT_ELEMS : 1];
     const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
     // dequantisation LUT: float32(float64(q - z) * scale) (tensor.py:154)
-    const uint32_t nq = in.q_bits <= 8 ? (1u << in.q_bits) : 256u;  // header q_bits is unchecked here
-    if (!STAGE)
-        for (uint32_t i = threadIdx.x; i < nq; i += ROW_THREADS)
-            s_lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, (double)in.zero_point), in.scale));
+    if (!STAGE) build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
     if (threadIdx.x == 0) s_bad = 0;
     // per-chunk row offsets: each thread scans ROW_CHUNK / 256 consecutive rows
     constexpr int PER = ROW_CHUNK / ROW_THREADS;
@@ -180,9 +193,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
                 p.q_out[i * K + c] = v;
                 p.mask_out[i * K + c] = 0;
             } else {
-                const float o = v < nq ? s_lut[v]
-                                       : __double2float_rn(__dmul_rn(
-                                             __dsub_rn((double)v, (double)in.zero_point), in.scale));
+                const float o = dequant<S>(v, s_lut, (double)in.zero_point, in.scale);
                 if (staged) s_out[li * K + c] = o;
                 else ochunk[(uint64_t)li * K + c] = o;
             }
@@ -229,9 +240,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
     __shared__ float s_lut[256];
     __shared__ int s_bad;
     const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
-    const uint32_t nq = in.q_bits <= 8 ? (1u << in.q_bits) : 256u;
-    for (uint32_t i = threadIdx.x; i < nq; i += ROW_THREADS)
-        s_lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, (double)in.zero_point), in.scale));
+    build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
     if (threadIdx.x == 0) s_bad = 0;
     constexpr int PER = ROW_CHUNK / ROW_THREADS;
     uint32_t loc[PER], sum = 0;
@@ -272,9 +281,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
             bad |= (c >= K) | ((e > 0) & (c <= prev));  // sparse.py:90-97
             prev = c;
             const uint32_t v = s_v[off + e];
-            const float o = v < nq ? s_lut[v]
-                                   : __double2float_rn(__dmul_rn(
-                                         __dsub_rn((double)v, (double)in.zero_point), in.scale));
+            const float o = dequant<S>(v, s_lut, (double)in.zero_point, in.scale);
             if (c < K) s_out[li * K + c] = o;
         }
     }
@@ -317,9 +324,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
     __shared__ float s_lut[256];
     __shared__ int s_bad;
     const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
-    const uint32_t nq = in.q_bits <= 8 ? (1u << in.q_bits) : 256u;
-    for (uint32_t i = threadIdx.x; i < nq; i += ROW_THREADS)
-        s_lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, (double)in.zero_point), in.scale));
+    build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
     if (threadIdx.x == 0) s_bad = 0;
     constexpr int PER = ROW_CHUNK / ROW_THREADS;
     uint32_t loc[PER], sum = 0;
@@ -342,42 +347,46 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
     __syncthreads();
     const S* cols = d + nnz;
     float* orow0 = p.out + p.out_off[b] + r0 * KK;
+    // rows are KK floats: one alignment test for the whole chunk (uniform)
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const uint32_t li = j * ROW_THREADS + threadIdx.x;
         if (li >= nrow) break;
         const uint32_t off = s_off[li], r = s_r[li];
-        uint32_t c[KK], v[KK];
+        // branch-free: clamped unconditional loads, then a column-presence mask
+        uint32_t c[KK];
+        float a[KK];
+        uint32_t mask = 0;
 #pragma unroll
         for (int e = 0; e < KK; ++e) {
-            c[e] = e < (int)r ? (uint32_t)cols[off + e] : 0xffffffffu;
-            v[e] = e < (int)r ? (uint32_t)d[off + e] : 0u;
+            const bool live = (uint32_t)e < r;
+            const uint32_t idx = off + (live ? (uint32_t)e : 0u);  // off <= nnz: in-bounds
+            c[e] = (uint32_t)cols[idx];
+            a[e] = dequant<S>((uint32_t)d[idx], s_lut, (double)in.zero_point, in.scale);
+            const bool order_bad = e > 0 && c[e] <= c[e > 0 ? e - 1 : 0];
+            bad |= live & ((c[e] >= (uint32_t)KK) | order_bad);  // sparse.py:90-97
+            mask |= live ? (1u << (c[e] & (KK - 1))) : 0u;
         }
         float o[KK];
 #pragma unroll
-        for (int col = 0; col < KK; ++col) o[col] = 0.0f;
+        for (int col = 0; col < KK; ++col) {
+            const uint32_t before = __popc(mask & ((1u << col) - 1u));  // entries left of col
+            float val = a[0];
 #pragma unroll
-        for (int e = 0; e < KK; ++e) {
-            if (e < (int)r) {
-                bad |= (c[e] >= (uint32_t)KK) | (e > 0 && c[e] <= c[e > 0 ? e - 1 : 0]);  // sparse.py:90-97
-                const float val = v[e] < nq ? s_lut[v[e]]
-                                            : __double2float_rn(__dmul_rn(
-                                                  __dsub_rn((double)v[e], (double)in.zero_point), in.scale));
-#pragma unroll
-                for (int col = 0; col < KK; ++col)
-                    if (c[e] == (uint32_t)col) o[col] = val;
-            }
+            for (int e = 1; e < KK; ++e) val = before == (uint32_t)e ? a[e] : val;
+            o[col] = (mask >> col) & 1u ? val : 0.0f;
         }
         float* orow = orow0 + (uint64_t)li * KK;
         if constexpr (KK == 4) {
-            if ((reinterpret_cast<uintptr_t>(orow) & 15) == 0) *reinterpret_cast<float4*>(orow) = make_float4(o[0], o[1], o[2], o[3]);
+            if (vec_ok) __stcs(reinterpret_cast<float4*>(orow), make_float4(o[0], o[1], o[2], o[3]));
             else { orow[0] = o[0]; orow[1] = o[1]; orow[2] = o[2]; orow[3] = o[3]; }
         } else if constexpr (KK == 2) {
-            if ((reinterpret_cast<uintptr_t>(orow) & 7) == 0) *reinterpret_cast<float2*>(orow) = make_float2(o[0], o[1]);
+            if (vec_ok) __stcs(reinterpret_cast<float2*>(orow), make_float2(o[0], o[1]));
             else { orow[0] = o[0]; orow[1] = o[1]; }
         } else {
-            orow[0] = o[0];
+            __stcs(orow, o[0]);
         }
     }
     if (bad) s_bad = 1;

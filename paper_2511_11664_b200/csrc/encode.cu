@@ -227,7 +227,9 @@ struct QuantParams {
 };
 
 // tensor.py:130-140 for one element: exact fp64 sequence of the reference.
-__device__ __forceinline__ uint32_t quant_exact(float x, double scale, double zf, double qmax) {
+// Out of line on purpose: it runs for ~0.03 % of elements and must not be
+// if-converted into every element of the hot loop.
+__device__ __noinline__ uint32_t quant_exact(float x, double scale, double zf, double qmax) {
     double y = __dadd_rn(__ddiv_rn((double)x, scale), zf);
     double a = floor(__dadd_rn(fabs(y), 0.5));
     double r = (y > 0.0) ? a : ((y < 0.0) ? -a : 0.0);
@@ -250,6 +252,7 @@ __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, i
     return quant_exact(x, scale, zf, (double)qmax);
 }
 
+template <bool SYM_OUT>  // SYM_OUT: also write every element's symbol (stage API)
 __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -301,8 +304,8 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
                 uint32_t q = quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
                 v8[rank++] = (uint8_t)q;
                 atomicAdd(&s_hist[warp & 3][q], 1u);
-                if (p.sym_out) p.sym_out[(uint64_t)b * p.total + idx + j] = q;
-            } else if (p.sym_out && (valid >> j & 1)) {
+                if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + idx + j] = q;
+            } else if (SYM_OUT && (valid >> j & 1)) {
                 p.sym_out[(uint64_t)b * p.total + idx + j] =
                     quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
             }
