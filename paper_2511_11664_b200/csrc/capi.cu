@@ -147,7 +147,7 @@ struct scz_ctx {
     int32_t* h_status_async = nullptr;
     uint32_t last_batch = 0;
     HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
-    DevBuf ready, candcnt;
+    DevBuf ready, candcnt, selbuf;
     // CUDA-graph cache: a launch sequence seen twice with the same key and
     // allocation generation is captured once and replayed afterwards.
     struct Graph {
@@ -533,7 +533,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     CK(ctx->state.ensure((size_t)B * sizeof(TensorState)));
     CK(ctx->vhist.ensure((size_t)B * 256 * 4));
     const uint64_t dstride = (pl.L_max + 15) & ~15ull;  // D = v ++ c ++ r (u8 width)
-    CK(ctx->v8.ensure((size_t)B * dstride + 64));
+    CK(ctx->v8.ensure((size_t)B * dstride + 1024 + 64));  // + encoder chunk over-read
     int maxw = (pl.widths & 4) ? 4 : ((pl.widths & 2) ? 2 : 1);
     CK(ctx->cr.ensure((size_t)B * 2 * T * maxw));
     CK(ctx->hp.ensure((size_t)B * pl.period * 4));
@@ -616,20 +616,27 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         rp.n_words = ceil_div_u32(T, 32);
         rp.n_cand = ncand;
         uint32_t chunks = 0, maxbins = 0;
-        for (uint32_t c = 0; c < ncand; ++c) {
-            uint32_t K = (uint32_t)(T / pl.rows[c]);
-            rp.cand_k[c] = K;
-            rp.cand_rows[c] = (uint32_t)pl.rows[c];
-            rp.rhist_off[c] = rh_off[c];
-            rp.chunk_start[c] = chunks;
-            if (K == 2 || K == 4 || K == 8) {
-                rp.units_per_chunk[c] = RH_THREADS * 16;  // bitmap words
-                chunks += ceil_div_u32(rp.n_words, rp.units_per_chunk[c]);
-            } else if (K > 1) {
-                rp.units_per_chunk[c] = RH_THREADS * 32;  // rows
-                chunks += ceil_div_u32(pl.rows[c], rp.units_per_chunk[c]);
-                if (K + 1 > RH_PRIV_BINS) maxbins = std::max(maxbins, K + 1);
+        // chunk sizes: 16 words / 32 rows per thread, shrunk for small batches
+        // until the grid covers the GPU twice
+        for (uint32_t div = 1;; div *= 2) {
+            chunks = 0;
+            maxbins = 0;
+            for (uint32_t c = 0; c < ncand; ++c) {
+                uint32_t K = (uint32_t)(T / pl.rows[c]);
+                rp.cand_k[c] = K;
+                rp.cand_rows[c] = (uint32_t)pl.rows[c];
+                rp.rhist_off[c] = rh_off[c];
+                rp.chunk_start[c] = chunks;
+                if (K == 2 || K == 4 || K == 8) {
+                    rp.units_per_chunk[c] = RH_THREADS * 16 / div;  // bitmap words
+                    chunks += ceil_div_u32(rp.n_words, rp.units_per_chunk[c]);
+                } else if (K > 1) {
+                    rp.units_per_chunk[c] = RH_THREADS * 32 / div;  // rows
+                    chunks += ceil_div_u32(pl.rows[c], rp.units_per_chunk[c]);
+                    if (K + 1 > RH_PRIV_BINS) maxbins = std::max(maxbins, K + 1);
+                }
             }
+            if ((uint64_t)chunks * B >= 2ull * ctx->num_sms || div >= 16) break;
         }
         rp.chunk_start[ncand] = chunks;
         rp.rhist = ctx->rhist.as<uint32_t>();
@@ -672,10 +679,25 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         dump = ctx->candcnt.as<uint32_t>();
     }
     sel.dump = dump;
-    const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)pl.period) : 0;
-    if (sel_smem > 48 * 1024)
+    sel.groups = 1;
+    if (pl.searching && pl.acap <= SEL_WARP_ACAP) {
+        // small batches: spread the candidates over several CTAs per tensor
+        const uint32_t per_cta = SEL_THREADS / 32;
+        const uint32_t want = ceil_div_u32(ncand, per_cta);
+        const uint32_t room = std::max<uint32_t>(1, (uint32_t)(2 * ctx->num_sms) / B);
+        sel.groups = std::max<uint32_t>(1, std::min(want, room));
+    }
+    if (sel.groups > 1) {
+        CK(ctx->selbuf.ensure((size_t)B * (MAX_CAND * 20 + 16)));
+        sel.gcost = ctx->selbuf.as<double>();
+        sel.gacnt = reinterpret_cast<uint32_t*>(sel.gcost + (size_t)B * MAX_CAND * 2);
+        sel.ticket = sel.gacnt + (size_t)B * MAX_CAND;
+        CK(cudaMemsetAsync(sel.ticket, 0, (size_t)B * 4, s));
+    }
+    const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)pl.period, (uint32_t)rh_total) : 0;
+    if (sel_smem > 0)  // static BlockScratch + dynamic may pass 48 KB: always opt in
         CK(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
-    k_select<<<B, SEL_THREADS, sel_smem, s>>>(sel);
+    k_select<<<dim3(sel.groups, B), SEL_THREADS, sel_smem, s>>>(sel);
     LAUNCHED("k_select");
 
     MatParams mp{T, pl.n_tiles, pl.words_pad, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(),
@@ -737,7 +759,9 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
 void dec_class(const scz_info& in, uint8_t* width) {
     // symbol width + lookup flavour: 1 = u8 LUT, 2 = u16 LUT, 4 = binary search
     if (in.precision <= 15 && in.alphabet <= 256) *width = 1;
-    else if (in.precision <= 15 && in.alphabet <= 4096) *width = 2;
+    // u16 LUT: the v2 decoder's step + symbol tables must fit shared memory
+    else if (in.precision <= 15 && in.alphabet <= 4096 && (in.precision <= 14 || in.alphabet <= 2048))
+        *width = 2;
     else *width = 4;
 }
 
@@ -802,6 +826,17 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     CK(ctx->dblk_off.ensure((size_t)B * nblk_cap * 4));
     CK(ctx->dsym.ensure((size_t)B * Lmax * 4));
     CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 4));
+    bool any_v1 = false, any_v2 = false;
+    for (uint32_t b = 0; b < B; ++b) (hi[b].version == 2 ? any_v2 : any_v1) = true;
+    // everything below is stream-ordered (pinned H2D of the prepared infos +
+    // launches) and replays from the graph cache for a repeated batch shape
+    const std::string key = key_of(
+        "dec", {B, acap, nblk_cap, nchunk_cap, widths, maxK, kmask, Lmax, maxA, (uint64_t)maxn,
+                (uint64_t)any_v1 | ((uint64_t)any_v2 << 1) | ((uint64_t)stage << 2),
+                (uint64_t)(uintptr_t)d_freqs, (uint64_t)(uintptr_t)d_blocks, (uint64_t)(uintptr_t)d_payload,
+                (uint64_t)(uintptr_t)d_out, (uint64_t)(uintptr_t)q_out, (uint64_t)(uintptr_t)mask_out,
+                (uint64_t)(uintptr_t)hi});
+    return graph_run(ctx, key, [&]() -> int {
     CK(cudaMemcpyAsync(ctx->dinfo.p, hi, (size_t)B * sizeof(scz_info), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->out_off.p, hoff, (size_t)B * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->dstatus.p, hst, (size_t)B * 4, cudaMemcpyHostToDevice, s));
@@ -810,8 +845,6 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
                  ctx->dstatus.as<int32_t>()};
     k_dec_prepare<<<B, 256, 0, s>>>(dp);
     LAUNCHED("k_dec_prepare");
-    bool any_v1 = false, any_v2 = false;
-    for (uint32_t b = 0; b < B; ++b) (hi[b].version == 2 ? any_v2 : any_v1) = true;
     RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<uint32_t>(), nchunk_cap,
                  ctx->dstatus.as<int32_t>(), d_out, ctx->out_off.as<uint64_t>(), q_out, mask_out};
     auto run_width = [&](auto tag) -> int {
@@ -820,10 +853,13 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         const size_t tab = maxA <= TAB_SMEM_MAX ? maxA * sizeof(uint2) : 0;
         const size_t lut = sizeof(L) < 4 ? ((size_t)1 << maxn) * sizeof(L) : 0;
         if (any_v2) {
-            size_t smem = dec_v2_smem(sizeof(L), maxn, (uint32_t)maxA);
-            CK(cudaFuncSetAttribute(k_rans_dec_v2<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-            k_rans_dec_v2<S, L><<<dim3(ceil_div_u32(nblk_cap, DEC2_WPB), B), DEC2_WPB * 32, smem, s>>>(dp);
+            // latency mode (4 warps per CTA) when 16-warp CTAs would not cover the SMs
+            const bool small = (uint64_t)ceil_div_u32(nblk_cap, DEC2_WPB) * B < (uint64_t)ctx->num_sms;
+            const int wpb = small ? DEC2_WPB_SMALL : DEC2_WPB;
+            auto kern = small ? k_rans_dec_v2<S, L, DEC2_WPB_SMALL> : k_rans_dec_v2<S, L, DEC2_WPB>;
+            size_t smem = dec_v2_smem(wpb, sizeof(L), maxn, (uint32_t)maxA);
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kern<<<dim3(ceil_div_u32(nblk_cap, wpb), B), wpb * 32, smem, s>>>(dp);
             LAUNCHED(wname<S>("k_rans_dec_v2"));
         }
         if (any_v1) {
@@ -880,6 +916,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     if (widths & 2) { if ((st = rows_out(uint16_t{})) != SCZ_OK) return st; }
     if (widths & 4) { if ((st = rows_out(uint32_t{})) != SCZ_OK) return st; }
     return SCZ_OK;
+    });
 }
 
 }  // namespace
@@ -925,7 +962,7 @@ void scz_ctx_destroy(scz_ctx* ctx) {
     for (DevBuf* b : {&ctx->x_in, &ctx->bitmap, &ctx->tile_stats, &ctx->tile_off, &ctx->state, &ctx->vhist,
                       &ctx->v8, &ctx->cr, &ctx->hp, &ctx->rhist, &ctx->counts, &ctx->terms, &ctx->freqs,
                       &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
-                      &ctx->info, &ctx->payload, &ctx->ticket, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
+                      &ctx->info, &ctx->payload, &ctx->ticket, &ctx->selbuf, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
                       &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
                       &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready, &ctx->candcnt})
         b->release();
@@ -1453,9 +1490,12 @@ int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint3
         using S = decltype(tag);
         const size_t lut = sizeof(S) < 4 ? ((size_t)1 << precision) * sizeof(S) : 0;
         if (lanes) {
-            size_t smem = dec_v2_smem(sizeof(S), precision, (uint32_t)alphabet);
-            CK(cudaFuncSetAttribute(k_rans_dec_v2<S, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_rans_dec_v2<S, S><<<dim3(ceil_div_u32(n_blocks, DEC2_WPB), 1), DEC2_WPB * 32, smem, s>>>(dp);
+            const bool small = ceil_div_u32(n_blocks, DEC2_WPB) < (uint32_t)ctx->num_sms;
+            const int wpb = small ? DEC2_WPB_SMALL : DEC2_WPB;
+            auto kern = small ? k_rans_dec_v2<S, S, DEC2_WPB_SMALL> : k_rans_dec_v2<S, S, DEC2_WPB>;
+            size_t smem = dec_v2_smem(wpb, sizeof(S), precision, (uint32_t)alphabet);
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kern<<<dim3(ceil_div_u32(n_blocks, wpb), 1), wpb * 32, smem, s>>>(dp);
         } else {
             size_t smem = RING + tab + lut;
             CK(cudaFuncSetAttribute(k_rans_dec_v1<S, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1549,7 +1589,11 @@ int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t 
     cudaStream_t s = ctx->stream;
     CK(ctx->x_in.ensure((size_t)batch * total * 4));
     CK(cudaMemcpyAsync(ctx->x_in.p, h_x, (size_t)batch * total * 4, cudaMemcpyHostToDevice, s));
-    if ((st = run_encode(ctx, ctx->x_in.as<float>(), pl, nullptr)) != SCZ_OK) return st;
+    const std::string key = key_of("enc", {(uint64_t)(uintptr_t)ctx->x_in.p, total, batch, (uint64_t)q_bits,
+                                           (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format,
+                                           lanes, block_syms});
+    if ((st = graph_run(ctx, key, [&] { return run_encode(ctx, ctx->x_in.as<float>(), pl, nullptr); })) != SCZ_OK)
+        return st;
     CK(ctx->hb_info.ensure((size_t)batch * sizeof(scz_info)));
     scz_info* hi = ctx->hb_info.as<scz_info>();
     CK(cudaMemcpyAsync(hi, ctx->info.p, (size_t)batch * sizeof(scz_info), cudaMemcpyDeviceToHost, s));

@@ -12,22 +12,19 @@
 
 namespace scz {
 
-constexpr int DEC2_WPB = 16;         // warps (= blocks) per CTA
+constexpr int DEC2_WPB = 16;         // warps (= blocks) per CTA, throughput mode
+constexpr int DEC2_WPB_SMALL = 4;    // latency mode (grid would not fill the GPU)
 constexpr int DCHUNK = 256;          // bytes per cp.async chunk (8 per lane)
 constexpr int DRING = 4 * DCHUNK;    // per-warp ring
+constexpr uint32_t DEC_BIG_F = 256;  // symbols with more slots are filled CTA-wide
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-template <typename S, typename L>
-__global__ void __launch_bounds__(DEC2_WPB * 32) k_rans_dec_v2(DecParams p) {
+// Shared-memory layout (LUT classes, L = u8 / u16):
+//   rings  [WPB][DRING] bytes
+//   tab    [A] uint2 (f, cum)           -- only while the LUTs are built
+//   step   [2^n] u32 (f << 16) | (slot - cum): the state update in one load
+//   sym    [2^n] L   slot -> symbol (off the state recurrence)
+template <typename S, typename L, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint32_t b = blockIdx.y;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.version != 2 || in.sym_bytes != sizeof(S)) return;
@@ -37,21 +34,41 @@ __global__ void __launch_bounds__(DEC2_WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint32_t nslots = 1u << n;
     const uint32_t* gf = p.freqs + in.freqs_off;
     const uint32_t* gcum = p.cumtab + (uint64_t)b * (p.acap + 1);
-    const uint32_t blk0 = blockIdx.x * DEC2_WPB;
+    const uint32_t blk0 = blockIdx.x * WPB;
     if (blk0 >= in.n_blocks) return;  // whole CTA idle
     uint8_t* rings = smem;
-    // classes (dec_class): u8/u16 LUT with the (f, cum) table in smem, or
-    // binary search over the cdf in global memory for huge alphabets / n = 16
-    uint2* tab = reinterpret_cast<uint2*>(smem + DEC2_WPB * DRING);   // A entries
-    L* lut = reinterpret_cast<L*>(tab + A);                            // 2^n entries
+    uint2* tab = reinterpret_cast<uint2*>(smem + WPB * DRING);
+    uint32_t* lstep = reinterpret_cast<uint32_t*>(tab + A);
+    L* lsym = reinterpret_cast<L*>(lstep + nslots);
     if constexpr (sizeof(L) < 4) {
+        __shared__ uint32_t s_nbig, s_bigs[128];  // sum f = 2^n: < 2^15 / 256 big ones
+        if (threadIdx.x == 0) s_nbig = 0;
         for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) tab[i] = make_uint2(gf[i], gcum[i]);
         __syncthreads();
-        // warp w writes the slot ranges of symbols w, w + nw, ... (coalesced)
+        // warp w fills the slot ranges of symbols w, w + nw, ... (coalesced);
+        // the few symbols with more than DEC_BIG_F slots go CTA-wide below
         const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        for (uint32_t s = warp; s < A; s += nw) {
-            const uint32_t c0 = tab[s].y, c1 = c0 + tab[s].x;
-            for (uint32_t sl = c0 + lane; sl < c1; sl += 32) lut[sl] = (L)s;
+        for (uint32_t s0 = warp; s0 < A; s0 += nw) {
+            const uint32_t f = tab[s0].x, c0 = tab[s0].y;
+            if (f > DEC_BIG_F) {
+                if (lane == 0) s_bigs[atomicAdd(&s_nbig, 1u)] = s0;
+                continue;
+            }
+            const uint32_t e = (f << 16) - c0;
+            for (uint32_t sl = c0 + lane; sl < c0 + f; sl += 32) {
+                lstep[sl] = e + sl;
+                lsym[sl] = (L)s0;
+            }
+        }
+        __syncthreads();
+        for (uint32_t j = 0; j < s_nbig; ++j) {
+            const uint32_t s0 = s_bigs[j];
+            const uint32_t f = tab[s0].x, c0 = tab[s0].y;
+            const uint32_t e = (f << 16) - c0;
+            for (uint32_t sl = c0 + threadIdx.x; sl < c0 + f; sl += blockDim.x) {
+                lstep[sl] = e + sl;
+                lsym[sl] = (L)s0;
+            }
         }
         __syncthreads();
     }
@@ -67,15 +84,21 @@ __global__ void __launch_bounds__(DEC2_WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint8_t* gsrc = p.payload + cbase + 8 * lane;
     uint8_t* ring = rings + warp * DRING;
     uint8_t* rdst = ring + 8 * lane;
-    // chunk c (absolute offset 256c from cbase) lives in ring slot c & 3
-    cp_async8(rdst + 0 * DCHUNK, gsrc + 0 * DCHUNK); cp_async_commit();
-    cp_async8(rdst + 1 * DCHUNK, gsrc + 1 * DCHUNK); cp_async_commit();
-    cp_async8(rdst + 2 * DCHUNK, gsrc + 2 * DCHUNK); cp_async_commit();
-    cp_async8(rdst + 3 * DCHUNK, gsrc + 3 * DCHUNK); cp_async_commit();
-    cp_async_wait<2>();  // chunks 0 and 1 landed
-    __syncwarp();
     uint32_t cur = (uint32_t)(a0 - cbase);  // byte offset from cbase
     const uint32_t end = cur + blen;
+    // chunk c (bytes [256c, 256c + 256) from cbase) lives in ring slot c & 3;
+    // chunks starting at or beyond `end` are never fetched (a 256-aligned
+    // chunk holding a valid byte never leaves that byte's allocation)
+    auto fetch = [&](uint32_t c) {
+        if (c * DCHUNK < end) cp_async8(rdst + (c & 3) * DCHUNK, gsrc + (size_t)c * DCHUNK);
+        cp_async_commit();
+    };
+    fetch(0);
+    fetch(1);
+    fetch(2);
+    fetch(3);
+    cp_async_wait<2>();  // chunks 0 and 1 landed
+    __syncwarp();
     auto rb = [&](uint32_t a) -> uint32_t { return ring[a & (DRING - 1)]; };
     uint32_t x = rb(cur + 4 * lane) | (rb(cur + 4 * lane + 1) << 8) | (rb(cur + 4 * lane + 2) << 16) |
                  (rb(cur + 4 * lane + 3) << 24);
@@ -86,8 +109,7 @@ __global__ void __launch_bounds__(DEC2_WPB * 32) k_rans_dec_v2(DecParams p) {
         if ((cur >> 8) != k) {  // warp-uniform, taken about once per 7 steps
             __syncwarp();
             ++k;
-            cp_async8(rdst + ((k + 3) & 3) * DCHUNK, gsrc + (k + 3) * DCHUNK);
-            cp_async_commit();
+            fetch(k + 3);
             cp_async_wait<2>();
             __syncwarp();
         }
@@ -95,19 +117,20 @@ __global__ void __launch_bounds__(DEC2_WPB * 32) k_rans_dec_v2(DecParams p) {
     advance();
     const uint32_t mask = nslots - 1;
     const uint32_t ltm = lanemask_lt();
-    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    const uint32_t* ring32 = reinterpret_cast<const uint32_t*>(ring);
     S* out = reinterpret_cast<S*>(p.dsym) + (uint64_t)b * p.dsym_stride + base + lane;
     const uint32_t steps = (len + 31) / 32;
-    bool bad = false;
-    // One step: pop the lane's symbol (rans.py:147-152) and refill.
-    auto step = [&](bool active) -> bool {
+    // One step: pop the lane's symbol (rans.py:147-152) and refill.  A
+    // stream that runs past its block end keeps decoding ring garbage and is
+    // rejected by the final cur == end check (rans.py:203-205 underrun).
+    auto step = [&](bool active) {
         uint32_t cnt = 0, sym = 0;
         if (active) {
             const uint32_t slot = x & mask;
             if constexpr (sizeof(L) < 4) {
-                sym = lut[slot];
-                const uint2 fc = tab[sym];
-                x = fc.x * (x >> n) + slot - fc.y;
+                const uint32_t e = lstep[slot];
+                sym = lsym[slot];
+                x = (e >> 16) * (x >> n) + (e & 0xffffu);
             } else {
                 uint32_t lo = 0, hi = A + 1;  // np.searchsorted(cdf, slot, 'right') - 1
                 while (hi - lo > 1) {
@@ -122,43 +145,41 @@ __global__ void __launch_bounds__(DEC2_WPB * 32) k_rans_dec_v2(DecParams p) {
         }
         const uint32_t b1 = __ballot_sync(0xffffffffu, cnt >= 1);
         const uint32_t b2 = __ballot_sync(0xffffffffu, cnt == 2);
-        const uint32_t tot = __popc(b1) + __popc(b2);
-        if (cur + tot > end) return false;  // rans.py:203-205 underrun
         const uint32_t a = cur + __popc(b1 & ltm) + __popc(b2 & ltm);
-        uint32_t r0, r1;  // both bytes read unconditionally (cheap), selected below
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r0) : "r"(ring_s + (a & (DRING - 1))));
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r1) : "r"(ring_s + ((a + 1) & (DRING - 1))));
-        x = cnt == 2 ? ((x << 16) | (r0 << 8) | r1) : (cnt == 1 ? ((x << 8) | r0) : x);
-        cur += tot;
+        // bytes a, a + 1 from two aligned words; PRMT shifts them into x
+        const uint32_t w0 = ring32[(a >> 2) & (DRING / 4 - 1)];
+        const uint32_t w1 = ring32[((a >> 2) + 1) & (DRING / 4 - 1)];
+        const uint32_t v = __funnelshift_r(w0, w1, (a & 3) * 8);
+        const uint32_t sel = cnt == 2 ? 0x1045u : (cnt == 1 ? 0x2104u : 0x3210u);
+        x = __byte_perm(x, v, sel);
+        cur += __popc(b1) + __popc(b2);
         if (active) *out = (S)sym;
         out += 32;
         advance();
-        return true;
     };
     if (steps > 0) {
         const uint32_t full = len / 32;
-        uint32_t s = 0;
-        for (; s < full; ++s)
-            if (!step(true)) {
-                bad = true;
-                break;
-            }
-        if (!bad && s < steps && !step(s * 32 + lane < len)) bad = true;  // partial last step
+        for (uint32_t s = 0; s < full; ++s) step(true);
+        if (full < steps) step(full * 32 + lane < len);  // partial last step
     }
     cp_async_wait<0>();
     // rans.py:211-212: every lane back at L and every byte consumed
-    if (!bad) bad = __any_sync(0xffffffffu, x != STATE_LOW) || cur != end;
+    const bool bad = __any_sync(0xffffffffu, x != STATE_LOW) || cur != end;
     if (bad && lane == 0) p.status[b] = SCZ_CORRUPT_STREAM;
 }
 
-template __global__ void k_rans_dec_v2<uint8_t, uint8_t>(DecParams);
-template __global__ void k_rans_dec_v2<uint16_t, uint16_t>(DecParams);
-template __global__ void k_rans_dec_v2<uint32_t, uint32_t>(DecParams);
+#define SCZ_DEC2(S, L)                                                      \
+    template __global__ void k_rans_dec_v2<S, L, DEC2_WPB>(DecParams);       \
+    template __global__ void k_rans_dec_v2<S, L, DEC2_WPB_SMALL>(DecParams);
+SCZ_DEC2(uint8_t, uint8_t)
+SCZ_DEC2(uint16_t, uint16_t)
+SCZ_DEC2(uint32_t, uint32_t)
+#undef SCZ_DEC2
 
 // dynamic shared memory of k_rans_dec_v2 for a batch (max over tensors)
-inline size_t dec_v2_smem(size_t lwidth, int n, uint32_t maxA) {
-    size_t s = (size_t)DEC2_WPB * DRING;
-    if (lwidth < 4) s += (size_t)maxA * sizeof(uint2) + ((size_t)1 << n) * lwidth;
+inline size_t dec_v2_smem(int wpb, size_t lwidth, int n, uint32_t maxA) {
+    size_t s = (size_t)wpb * DRING;
+    if (lwidth < 4) s += (size_t)maxA * sizeof(uint2) + ((size_t)1 << n) * (4 + lwidth);
     return (s + 15) & ~(size_t)15;
 }
 

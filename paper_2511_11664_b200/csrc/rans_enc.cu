@@ -66,6 +66,9 @@ struct EncLane {
     uint32_t err;
 };
 
+__device__ __forceinline__ void enc_apply(EncLane& L, const EncTab& t, bool live, int n, int sh_bound,
+                                          uint32_t gtm, uint8_t* slot_end);
+
 // One step for one lane.  `live` false keeps the lane idle (partial step).
 template <bool SMEM, bool CHECK>
 __device__ __forceinline__ void enc_step(EncLane& L, uint32_t sym, bool live, const EncTab* s_tab,
@@ -92,6 +95,12 @@ __device__ __forceinline__ void enc_step(EncLane& L, uint32_t sym, bool live, co
             live = false;
         }
     }
+    enc_apply(L, t, live, n, sh_bound, gtm, slot_end);
+}
+
+// The state transform and byte placement with the symbol's table entry given.
+__device__ __forceinline__ void enc_apply(EncLane& L, const EncTab& t, bool live, int n, int sh_bound,
+                                          uint32_t gtm, uint8_t* slot_end) {
     const uint32_t bound = t.freq << sh_bound;  // ((L >> n) << 8) * f
     const bool e1 = live && L.x >= bound;
     const bool e2 = live && (L.x >> 8) >= bound;
@@ -135,7 +144,55 @@ __global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src 
     const uint32_t gtm = lanemask_gt();
     uint8_t* slot_end = p.slots + ((uint64_t)b * p.slots_per_tensor + blk + 1) * p.slot_cap;
     EncLane E{STATE_LOW, 0u, 0u};
-    if (steps > 0) {
+    if constexpr (std::is_same<Src, Contig8Src>::value && SMEM && !CHECK) {
+        // u8 symbols staged through a per-warp 2 x 1 KB shared ring (chunk g =
+        // steps [32g, 32g + 32) = block bytes [1024g, 1024g + 1024)), fetched
+        // one chunk ahead with cp.async; the table entry of the next step is
+        // loaded while the current one is coded.
+        __shared__ __align__(16) uint8_t s_ring[ENC2_WPB][2][1024];
+        const uint8_t* gsym = cur.d;
+        auto fetch = [&](int g) {
+            if (g >= 0) {
+                uint8_t* dst = s_ring[warp][g & 1] + 16 * lane;
+                const uint8_t* src = gsym + (size_t)g * 1024 + 16 * lane;
+                cp_async16(dst, src);
+                cp_async16(dst + 512, src + 512);
+            }
+            cp_async_commit();
+        };
+        if (steps > 0) {
+            const int s_top = steps - 1, g_top = s_top >> 5;
+            fetch(g_top);
+            fetch(g_top - 1);
+            for (int g = g_top; g >= 0; --g) {
+                cp_async_wait<1>();
+                __syncwarp();
+                const uint8_t* rs = s_ring[warp][g & 1] + lane;
+                const int s_lo = g * 32;
+                int s = g == g_top ? s_top : s_lo + 31;
+                EncTab t;
+                if (g == g_top) {  // the highest step may be partial
+                    const bool act = (uint32_t)s * 32 + lane < len;
+                    t = s_tab[act ? rs[(s & 31) * 32] : 0];
+                    enc_apply(E, t, act, n, sh_bound, gtm, slot_end);
+                    --s;
+                }
+                if (s >= s_lo) {
+                    t = s_tab[rs[(s & 31) * 32]];
+#pragma unroll 4
+                    for (; s > s_lo; --s) {
+                        const EncTab tn = s_tab[rs[((s - 1) & 31) * 32]];
+                        enc_apply(E, t, true, n, sh_bound, gtm, slot_end);
+                        t = tn;
+                    }
+                    enc_apply(E, t, true, n, sh_bound, gtm, slot_end);
+                }
+                __syncwarp();
+                fetch(g - 2);
+            }
+        }
+        cp_async_wait<0>();
+    } else if (steps > 0) {
         // the highest step may be partial: peel it
         const int s_top = steps - 1;
         const uint32_t i_top = (uint32_t)s_top * 32 + lane;

@@ -1,6 +1,6 @@
 // select.cu -- reshape search decision (Algorithm 1) and frequency tables.
 //
-//   k_select  one CTA per tensor.  For every feasible candidate N (descending,
+//   k_select  grid (groups, B).  For every feasible candidate N (descending,
 //             optimizer.py:72-75) it assembles the histogram of D = v ++ c ++ r
 //             from the value histogram, the folded column histogram and the
 //             row-count histogram, prices it as l_D * H (optimizer.py:87-96,
@@ -39,6 +39,12 @@ struct SelectParams {
     EncTab* enctab;             // out [B][acap]
     double* cand_out;           // optional out [B][MAX_CAND][2] (entropy, cost)
     uint32_t* dump;             // optional out [B][n_cand][acap] histogram of D per candidate
+    // candidate pricing split over `groups` CTAs per tensor (small batches):
+    // each publishes its costs, the last to arrive decides and normalises
+    uint32_t groups;
+    uint32_t* ticket;           // [B], zeroed before the launch
+    double* gcost;              // [B][MAX_CAND][2] (entropy, cost)
+    uint32_t* gacnt;            // [B][MAX_CAND] alphabet per candidate
 };
 
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src
@@ -353,18 +359,22 @@ __device__ double block_entropy(const uint32_t* counts, uint32_t A, double total
 }
 
 // Candidate pricing with one warp per candidate (search path, A <= 1024):
-// dynamic smem = [H_P if it fits][per warp: counts u32[acap], terms f64[acap]].
+// dynamic smem = [H_P if it fits][vhist][row histograms if they fit]
+//                [per warp: terms f64[acap], counts u32[acap]],
+// the histograms staged with one batch of cp.async copies.
 constexpr uint32_t SEL_WARP_ACAP = 1024;
 constexpr uint32_t SEL_HP_SMEM_MAX = 16384;  // H_P entries staged in smem (64 KB)
+constexpr uint32_t SEL_RH_SMEM_MAX = 8192;   // row-histogram words staged in smem
 
-__host__ __device__ inline size_t select_smem_bytes(uint32_t acap, uint32_t period) {
+__host__ __device__ inline size_t select_smem_bytes(uint32_t acap, uint32_t period, uint32_t rh_stride) {
     if (acap > SEL_WARP_ACAP) return 0;
-    size_t s = (size_t)(SEL_THREADS / 32) * acap * (4 + 8);
+    size_t s = (size_t)(SEL_THREADS / 32) * acap * (4 + 8) + 256 * 4;
     if (period <= SEL_HP_SMEM_MAX) s += (size_t)period * 4;
+    if (rh_stride <= SEL_RH_SMEM_MAX) s += ((size_t)rh_stride * 4 + 15) & ~(size_t)15;
     return (s + 15) & ~(size_t)15;
 }
 
-__device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScratch& s) {
+__device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, uint32_t g, BlockScratch& s) {
     extern __shared__ __align__(16) uint8_t sel_dyn[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const TensorState& st = p.state[b];
@@ -372,23 +382,38 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScra
     const uint32_t P = p.period;
     const bool hp_smem = P <= SEL_HP_SMEM_MAX;
     const uint32_t* ghp = p.hp + (uint64_t)b * p.hp_stride;
+    const uint32_t* grh = p.rhist + (uint64_t)b * p.rhist_stride;
+    const uint32_t* gvh = p.vhist + (uint64_t)b * 256;
+    const bool rh_smem = p.rhist_stride <= SEL_RH_SMEM_MAX;
     uint8_t* dyn = sel_dyn;
     uint32_t* s_hp = reinterpret_cast<uint32_t*>(dyn);
-    if (hp_smem) {
-        for (uint32_t i = threadIdx.x; i < P; i += SEL_THREADS) s_hp[i] = ghp[i];
-        dyn += (((size_t)P * 4 + 15) & ~(size_t)15);
+    if (hp_smem) {  // P is a multiple of 32 and the rows 128-byte aligned: 16-byte copies
+        for (uint32_t i = threadIdx.x; i < P / 4; i += SEL_THREADS) cp_async16(s_hp + 4 * i, ghp + 4 * i);
+        dyn += (size_t)P * 4;
     }
+    uint32_t* s_vh = reinterpret_cast<uint32_t*>(dyn);
+    if (threadIdx.x < 64) cp_async16(s_vh + 4 * threadIdx.x, gvh + 4 * threadIdx.x);
+    dyn += 256 * 4;
+    uint32_t* s_rh = reinterpret_cast<uint32_t*>(dyn);
+    if (rh_smem) {
+        for (uint32_t i = threadIdx.x; i < p.rhist_stride; i += SEL_THREADS) cp_async4(s_rh + i, grh + i);
+        dyn += ((size_t)p.rhist_stride * 4 + 15) & ~(size_t)15;
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     const uint32_t* hp = hp_smem ? s_hp : ghp;
+    const uint32_t* rhb = rh_smem ? s_rh : grh;
     double* terms = reinterpret_cast<double*>(dyn) + (size_t)warp * p.acap;
     uint32_t* cb = reinterpret_cast<uint32_t*>(dyn + (size_t)(SEL_THREADS / 32) * p.acap * 8) +
                    (size_t)warp * p.acap;
     const uint32_t nv = 1u << p.q_bits;
-    const uint32_t* vh = p.vhist + (uint64_t)b * 256;
-    for (uint32_t c = warp; c < p.n_cand; c += SEL_THREADS / 32) {
+    const uint32_t* vh = s_vh;
+    constexpr uint32_t NW = SEL_THREADS / 32;
+    for (uint32_t c = g * NW + warp; c < p.n_cand; c += NW * p.groups) {
         const uint32_t K = p.cand_k[c], N = p.cand_n[c];
         const uint32_t ub = max(nv, K + 1);
-        const uint32_t* rh = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c];
+        const uint32_t* rh = rhb + p.rhist_off[c];
         uint32_t rsum = 0;  // rows with r >= 1 (bin 0 is N - rsum)
         if (K > 1)
             for (uint32_t i = 1 + lane; i <= K; i += 32) rsum += rh[i];
@@ -424,9 +449,16 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScra
                 }
             } else {
                 for (uint32_t col = lane; col < K; col += 32) {
-                    uint32_t acc = 0;
-                    for (uint32_t j = col; j < P; j += K) acc += hp[j];
-                    cb[col] += acc;
+                    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // independent chains
+                    uint32_t j = col;
+                    for (; j + 3 * K < P; j += 4 * K) {
+                        a0 += hp[j];
+                        a1 += hp[j + K];
+                        a2 += hp[j + 2 * K];
+                        a3 += hp[j + 3 * K];
+                    }
+                    for (; j < P; j += K) a0 += hp[j];
+                    cb[col] += a0 + a1 + a2 + a3;
                 }
             }
         }
@@ -441,7 +473,10 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScra
             uint32_t* dd = p.dump + ((uint64_t)b * p.n_cand + c) * p.acap;
             for (uint32_t i = lane; i < p.acap; i += 32) dd[i] = i < A ? cb[i] : 0;
         }
-        if (lane == 0) s.acnt[c] = A;
+        if (lane == 0) {
+            s.acnt[c] = A;
+            if (p.groups > 1) p.gacnt[(uint64_t)b * MAX_CAND + c] = A;
+        }
         // entropy over the positive counts in index order (rans.py:219-223)
         const uint64_t len = 2 * nnz + N;
         const double total = (double)len;
@@ -461,14 +496,39 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, BlockScra
             const double h = -(m <= 1024 ? pairwise_sum_d<3>(terms, m) : pairwise_sum(terms, m));
             s.ents[c] = h;
             s.costs[c] = __dmul_rn((double)len, h);
+            if (p.groups > 1) {
+                double* gc = p.gcost + ((uint64_t)b * MAX_CAND + c) * 2;
+                gc[0] = h;
+                gc[1] = s.costs[c];
+            }
         }
         __syncwarp();
     }
     __syncthreads();
 }
 
+// Multi-CTA pricing: true in the CTA that arrives last for tensor b, which
+// then holds every candidate's (entropy, cost, alphabet) in `s`.
+__device__ bool gather_costs(const SelectParams& p, uint32_t b, BlockScratch& s) {
+    if (p.groups <= 1) return true;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s.alph[3] = atomicAdd(p.ticket + b, 1u) == p.groups - 1;
+    __syncthreads();
+    if (!s.alph[3]) return false;
+    __threadfence();
+    for (uint32_t c = threadIdx.x; c < p.n_cand; c += SEL_THREADS) {
+        const volatile double* gc = p.gcost + ((uint64_t)b * MAX_CAND + c) * 2;
+        s.ents[c] = gc[0];
+        s.costs[c] = gc[1];
+        s.acnt[c] = *(const volatile uint32_t*)(p.gacnt + (uint64_t)b * MAX_CAND + c);
+    }
+    __syncthreads();
+    return true;
+}
+
 __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
-    const uint32_t b = blockIdx.x;
+    const uint32_t b = blockIdx.y, g = blockIdx.x;
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
     __shared__ BlockScratch s;
@@ -478,8 +538,10 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
 
     uint32_t chosen = 0, flags = 0, evaluated = 0;
     if (p.searching) {
-        if (p.acap <= SEL_WARP_ACAP) warp_parallel_costs(p, b, s);
-        else for (uint32_t c = 0; c < p.n_cand; ++c) {
+        if (p.acap <= SEL_WARP_ACAP) {
+            warp_parallel_costs(p, b, g, s);
+            if (!gather_costs(p, b, s)) return;
+        } else for (uint32_t c = 0; c < p.n_cand; ++c) {
             uint32_t A = assemble_counts(p, b, c, counts, s);
             if (p.dump) {
                 uint32_t* dd = p.dump + ((uint64_t)b * p.n_cand + c) * p.acap;

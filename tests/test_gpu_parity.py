@@ -448,3 +448,19 @@ def test_fused_front_end_matches_default(tmp_path):
         subprocess.check_call([sys.executable, "-c", code % (root, str(path))], env=env, timeout=300)
         outs.append(path.read_bytes())
     assert outs[0] == outs[1]
+
+
+def test_graph_replay_tracks_new_inputs_and_reallocation():
+    """Repeated shapes replay a captured CUDA graph: every replay must see the
+    new input values (device) and new headers (decode), and a buffer
+    reallocation in between (a larger tensor) must invalidate the graphs."""
+    rng = np.random.default_rng(11)
+    shapes = [(1, 32, 20, 20)] * 4 + [(1, 64, 56, 56)] + [(1, 32, 20, 20)] * 4
+    for i, dims in enumerate(shapes):
+        t = sz.gen_synthetic("relu-laplace", list(dims), float(rng.uniform(0.3, 0.9)), 1000 + i)
+        for fmt in (1, 2):
+            ref = orc.compress(t.data, dims, 6, None, 14, fmt=fmt, lanes=32, block_syms=2048)
+            c = sz.compress(t, 6, format=fmt, block_syms=2048)
+            assert container.to_bytes(c) == orc.to_bytes(ref), (i, fmt)
+            out = sz.decompress(c)
+            assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32)), (i, fmt)
