@@ -147,7 +147,7 @@ struct scz_ctx {
     int32_t* h_status_async = nullptr;
     uint32_t last_batch = 0;
     HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
-    DevBuf ready, candcnt, selbuf;
+    DevBuf ready, candcnt, selbuf, dlut, probe;
     // CUDA-graph cache: a launch sequence seen twice with the same key and
     // allocation generation is captured once and replayed afterwards.
     struct Graph {
@@ -524,7 +524,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     uint64_t rh_total = 0;
     for (uint32_t c = 0; c < ncand; ++c) {
         rh_off[c] = (uint32_t)rh_total;
-        rh_total += T / pl.rows[c] + 1;
+        rh_total += 2 * (T / pl.rows[c]) + 1;  // K + 1 row bins, K column bins
     }
     if (rh_total >= (1ull << 32)) return ctx->fail(SCZ_UNSUPPORTED, "row histogram too large");
     CK(ctx->bitmap.ensure((size_t)B * pl.words_pad * 4 + 64));
@@ -641,9 +641,13 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         rp.chunk_start[ncand] = chunks;
         rp.rhist = ctx->rhist.as<uint32_t>();
         rp.rhist_stride = (uint32_t)rh_total;
-        if (chunks) {
+        rp.hp = ctx->hp.as<uint32_t>();
+        rp.hp_stride = (uint32_t)pl.period;
+        rp.period = (uint32_t)pl.period;
+        rp.fold_start = chunks;  // + one column-fold CTA per candidate
+        {
             size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
-            k_rowhist2<<<dim3(chunks, B), RH_THREADS, smem, s>>>(rp);
+            k_rowhist2<<<dim3(chunks + ncand, B), RH_THREADS, smem, s>>>(rp);
             LAUNCHED("k_rowhist");
         }
     }
@@ -656,9 +660,6 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         sel.cand_n[c] = (uint32_t)pl.rows[c];
         sel.rhist_off[c] = rh_off[c];
     }
-    sel.period = (uint32_t)pl.period;
-    sel.hp = ctx->hp.as<uint32_t>();
-    sel.hp_stride = (uint32_t)pl.period;
     sel.rhist = ctx->rhist.as<uint32_t>();
     sel.rhist_stride = (uint32_t)rh_total;
     sel.vhist = ctx->vhist.as<uint32_t>();
@@ -694,11 +695,29 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         sel.ticket = sel.gacnt + (size_t)B * MAX_CAND;
         CK(cudaMemsetAsync(sel.ticket, 0, (size_t)B * 4, s));
     }
-    const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)pl.period, (uint32_t)rh_total) : 0;
+    const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)rh_total) : 0;
     if (sel_smem > 0)  // static BlockScratch + dynamic may pass 48 KB: always opt in
         CK(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
+    const bool probe = getenv("SCZ_SELECT_PROBE") && !ctx->timing && B <= 64;
+    if (probe) {  // debug timeline of k_select phases (synchronous; graphs off)
+        CK(ctx->probe.ensure((size_t)B * sel.groups * 16 * 8));
+        CK(cudaMemsetAsync(ctx->probe.p, 0, (size_t)B * sel.groups * 16 * 8, s));
+        sel.probe = ctx->probe.as<unsigned long long>();
+    }
     k_select<<<dim3(sel.groups, B), SEL_THREADS, sel_smem, s>>>(sel);
     LAUNCHED("k_select");
+    if (probe) {
+        std::vector<unsigned long long> h((size_t)B * sel.groups * 16);
+        CK(cudaMemcpyAsync(h.data(), sel.probe, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (uint32_t i = 0; i < B * sel.groups; ++i) {
+            const unsigned long long t0 = h[(size_t)(i - i % sel.groups) * 16];
+            fprintf(stderr, "k_select b=%u g=%u ns:", i / sel.groups, i % sel.groups);
+            for (int k = 1; k < 7; ++k)
+                fprintf(stderr, " %lld", h[(size_t)i * 16 + k] ? (long long)(h[(size_t)i * 16 + k] - t0) : -1ll);
+            fprintf(stderr, "\n");
+        }
+    }
 
     MatParams mp{T, pl.n_tiles, pl.words_pad, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(),
                  ctx->state.as<TensorState>(), ctx->cr.p, 2 * T, 1, 0};
@@ -826,12 +845,19 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     CK(ctx->dblk_off.ensure((size_t)B * nblk_cap * 4));
     CK(ctx->dsym.ensure((size_t)B * Lmax * 4));
     CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 4));
+    // v2 decode tables: (4 + 2) bytes per slot covers both LUT classes
+    int lut_n = 0;  // largest precision among v2 tensors of the LUT classes
+    for (uint32_t b = 0; b < B; ++b)
+        if (hi[b].version == 2 && hi[b].sym_bytes < 4) lut_n = std::max(lut_n, (int)hi[b].precision);
+    const uint64_t lut_stride = ((6ull << lut_n) + 15) & ~15ull;
+    CK(ctx->dlut.ensure((size_t)B * lut_stride + 64));
+    const uint32_t lut_slices = lut_n ? std::max<uint32_t>(1, (1u << lut_n) / LUT_SLICE) : 0;
     bool any_v1 = false, any_v2 = false;
     for (uint32_t b = 0; b < B; ++b) (hi[b].version == 2 ? any_v2 : any_v1) = true;
     // everything below is stream-ordered (pinned H2D of the prepared infos +
     // launches) and replays from the graph cache for a repeated batch shape
     const std::string key = key_of(
-        "dec", {B, acap, nblk_cap, nchunk_cap, widths, maxK, kmask, Lmax, maxA, (uint64_t)maxn,
+        "dec", {B, acap, nblk_cap, nchunk_cap, widths, maxK, kmask, Lmax, maxA, (uint64_t)maxn, (uint64_t)lut_n,
                 (uint64_t)any_v1 | ((uint64_t)any_v2 << 1) | ((uint64_t)stage << 2),
                 (uint64_t)(uintptr_t)d_freqs, (uint64_t)(uintptr_t)d_blocks, (uint64_t)(uintptr_t)d_payload,
                 (uint64_t)(uintptr_t)d_out, (uint64_t)(uintptr_t)q_out, (uint64_t)(uintptr_t)mask_out,
@@ -842,8 +868,8 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     CK(cudaMemcpyAsync(ctx->dstatus.p, hst, (size_t)B * 4, cudaMemcpyHostToDevice, s));
     DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
                  ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
-                 ctx->dstatus.as<int32_t>()};
-    k_dec_prepare<<<B, 256, 0, s>>>(dp);
+                 ctx->dstatus.as<int32_t>(), ctx->dlut.as<uint8_t>(), lut_stride};
+    k_dec_prepare<<<dim3(1 + lut_slices, B), 256, 0, s>>>(dp);
     LAUNCHED("k_dec_prepare");
     RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<uint32_t>(), nchunk_cap,
                  ctx->dstatus.as<int32_t>(), d_out, ctx->out_off.as<uint64_t>(), q_out, mask_out};
@@ -962,7 +988,7 @@ void scz_ctx_destroy(scz_ctx* ctx) {
     for (DevBuf* b : {&ctx->x_in, &ctx->bitmap, &ctx->tile_stats, &ctx->tile_off, &ctx->state, &ctx->vhist,
                       &ctx->v8, &ctx->cr, &ctx->hp, &ctx->rhist, &ctx->counts, &ctx->terms, &ctx->freqs,
                       &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
-                      &ctx->info, &ctx->payload, &ctx->ticket, &ctx->selbuf, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
+                      &ctx->info, &ctx->payload, &ctx->ticket, &ctx->selbuf, &ctx->dlut, &ctx->probe, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
                       &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
                       &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready, &ctx->candcnt})
         b->release();
@@ -1479,11 +1505,15 @@ int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint3
     CK(ctx->dsym.ensure(count * 4));
     CK(cudaMemcpyAsync(ctx->dinfo.p, &hi, sizeof hi, cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(ctx->dstatus.p, 0, 4, s));
+    const bool use_lut = lanes && hi.sym_bytes < 4;
+    const uint64_t lut_stride = use_lut ? ((6ull << precision) + 15) & ~15ull : 16;
+    CK(ctx->dlut.ensure(lut_stride + 64));
     DecParams dp{ctx->dinfo.as<scz_info>(), ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
                  ctx->dpayload.as<uint8_t>(), ctx->cumtab.as<uint32_t>(), ctx->dblk_off.as<uint32_t>(),
                  (uint32_t)alphabet, (uint32_t)std::max<uint64_t>(n_blocks, 1), ctx->dsym.p, count,
-                 ctx->dstatus.as<int32_t>()};
-    k_dec_prepare<<<1, 256, 0, s>>>(dp);
+                 ctx->dstatus.as<int32_t>(), ctx->dlut.as<uint8_t>(), lut_stride};
+    const uint32_t lut_slices = use_lut ? std::max<uint32_t>(1, (1u << precision) / LUT_SLICE) : 0;
+    k_dec_prepare<<<dim3(1 + lut_slices, 1), 256, 0, s>>>(dp);
     LAUNCHED("k_dec_prepare");
     const size_t tab = alphabet <= TAB_SMEM_MAX ? alphabet * sizeof(uint2) : 0;
     auto go = [&](auto tag) -> int {

@@ -152,13 +152,79 @@ struct DecParams {
     void* dsym;                  // out [B][dsym_stride] symbols, width sym_w
     uint64_t dsym_stride;
     int32_t* status;             // [B]
+    // v2 LUT classes: per-tensor decode tables built once in global memory
+    // (k_dec_prepare slices) and bulk-copied into each decoder CTA:
+    //   [2^n] u32 (f << 16) | (slot - cum)   then   [2^n] symbol (u8 / u16)
+    uint8_t* lut;
+    uint64_t lut_stride;         // bytes per tensor
 };
+
+constexpr uint32_t LUT_SLICE = 2048;  // slots per k_dec_prepare slice CTA
+
+__host__ __device__ inline uint32_t lut_sym_off(int n) { return 4u << n; }
 
 // Per tensor: validate the table (rans.py:49-56, Σ f == 2^n), build the cdf,
 // scan block lengths into offsets and check them against the header.
+// Slice CTA (blockIdx.x >= 1): slots [LUT_SLICE * (x - 1), LUT_SLICE * x) of
+// the v2 decode tables of tensor blockIdx.y; thread t owns 8 consecutive
+// slots: one binary search of the cdf, then a forward walk.
+template <typename L>
+__device__ void build_lut_slice(const DecParams& p, const scz_info& in, uint32_t b, uint32_t slice) {
+    const int n = in.precision;
+    const uint32_t A = in.alphabet;
+    const uint32_t s0 = slice * LUT_SLICE;
+    if (s0 >= (1u << n)) return;
+    __shared__ uint32_t s_cum[4097];
+    __shared__ uint32_t s_scan[33];
+    const uint32_t* f = p.freqs + in.freqs_off;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < A; base += 256) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < A ? f[i] : 0;
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan<256>(v, s_scan, &tot);
+        if (i < A) s_cum[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) s_cum[A] = carry;
+    __syncthreads();
+    if (carry != (1u << n)) return;  // corrupt table: the prepare CTA flags it
+    uint8_t* base = p.lut + (uint64_t)b * p.lut_stride;
+    uint32_t* step = reinterpret_cast<uint32_t*>(base);
+    L* sym = reinterpret_cast<L*>(base + lut_sym_off(n));
+    const uint32_t slot0 = s0 + 8 * threadIdx.x;
+    if (slot0 >= (1u << n)) return;
+    uint32_t lo = 0, hi = A;  // last symbol with cum <= slot0
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_cum[mid] <= slot0) lo = mid;
+        else hi = mid;
+    }
+    uint32_t e[8];
+    L sy[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t sl = slot0 + k;
+        while (s_cum[lo + 1] <= sl) ++lo;  // f = 0 symbols are skipped here
+        e[k] = ((s_cum[lo + 1] - s_cum[lo]) << 16) | (sl - s_cum[lo]);
+        sy[k] = (L)lo;
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(step + slot0);
+    d4[0] = make_uint4(e[0], e[1], e[2], e[3]);
+    d4[1] = make_uint4(e[4], e[5], e[6], e[7]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sym[slot0 + k] = sy[k];
+}
+
 __global__ void __launch_bounds__(256) k_dec_prepare(DecParams p) {
-    const uint32_t b = blockIdx.x;
+    const uint32_t b = blockIdx.y;
     const scz_info& in = p.info[b];
+    if (blockIdx.x > 0) {
+        if (p.status[b] != SCZ_OK || in.version != 2) return;
+        if (in.sym_bytes == 1) build_lut_slice<uint8_t>(p, in, b, blockIdx.x - 1);
+        else if (in.sym_bytes == 2) build_lut_slice<uint16_t>(p, in, b, blockIdx.x - 1);
+        return;
+    }
     __shared__ uint32_t s_scan[33];
     __shared__ int s_bad;
     if (threadIdx.x == 0) s_bad = 0;

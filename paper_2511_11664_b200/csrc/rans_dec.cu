@@ -20,15 +20,17 @@ constexpr uint32_t DEC_BIG_F = 256;  // symbols with more slots are filled CTA-w
 
 // Shared-memory layout (LUT classes, L = u8 / u16):
 //   rings  [WPB][DRING] bytes
-//   tab    [A] uint2 (f, cum)           -- only while the LUTs are built
 //   step   [2^n] u32 (f << 16) | (slot - cum): the state update in one load
 //   sym    [2^n] L   slot -> symbol (off the state recurrence)
+// The two tables are built once per tensor by k_dec_prepare and arrive with
+// one bulk copy (TMA) while the payload ring is being primed.
 template <typename S, typename L, int WPB>
 __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint32_t b = blockIdx.y;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.version != 2 || in.sym_bytes != sizeof(S)) return;
     extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(8) uint64_t s_bar;
     const uint32_t A = in.alphabet;
     const int n = in.precision;
     const uint32_t nslots = 1u << n;
@@ -37,40 +39,16 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint32_t blk0 = blockIdx.x * WPB;
     if (blk0 >= in.n_blocks) return;  // whole CTA idle
     uint8_t* rings = smem;
-    uint2* tab = reinterpret_cast<uint2*>(smem + WPB * DRING);
-    uint32_t* lstep = reinterpret_cast<uint32_t*>(tab + A);
-    L* lsym = reinterpret_cast<L*>(lstep + nslots);
+    uint32_t* lstep = reinterpret_cast<uint32_t*>(smem + WPB * DRING);
+    const L* lsym = reinterpret_cast<const L*>(reinterpret_cast<const uint8_t*>(lstep) + lut_sym_off(n));
     if constexpr (sizeof(L) < 4) {
-        __shared__ uint32_t s_nbig, s_bigs[128];  // sum f = 2^n: < 2^15 / 256 big ones
-        if (threadIdx.x == 0) s_nbig = 0;
-        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) tab[i] = make_uint2(gf[i], gcum[i]);
-        __syncthreads();
-        // warp w fills the slot ranges of symbols w, w + nw, ... (coalesced);
-        // the few symbols with more than DEC_BIG_F slots go CTA-wide below
-        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        for (uint32_t s0 = warp; s0 < A; s0 += nw) {
-            const uint32_t f = tab[s0].x, c0 = tab[s0].y;
-            if (f > DEC_BIG_F) {
-                if (lane == 0) s_bigs[atomicAdd(&s_nbig, 1u)] = s0;
-                continue;
-            }
-            const uint32_t e = (f << 16) - c0;
-            for (uint32_t sl = c0 + lane; sl < c0 + f; sl += 32) {
-                lstep[sl] = e + sl;
-                lsym[sl] = (L)s0;
-            }
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar, 1);
+            const uint32_t bytes = (lut_sym_off(n) + nslots * (uint32_t)sizeof(L) + 15u) & ~15u;
+            mbar_expect_tx(&s_bar, bytes);
+            bulk_g2s(lstep, p.lut + (uint64_t)b * p.lut_stride, bytes, &s_bar);
         }
-        __syncthreads();
-        for (uint32_t j = 0; j < s_nbig; ++j) {
-            const uint32_t s0 = s_bigs[j];
-            const uint32_t f = tab[s0].x, c0 = tab[s0].y;
-            const uint32_t e = (f << 16) - c0;
-            for (uint32_t sl = c0 + threadIdx.x; sl < c0 + f; sl += blockDim.x) {
-                lstep[sl] = e + sl;
-                lsym[sl] = (L)s0;
-            }
-        }
-        __syncthreads();
+        __syncthreads();  // s_bar initialised before any warp polls it
     }
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t blk = blk0 + warp;
@@ -104,7 +82,9 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
                  (rb(cur + 4 * lane + 3) << 24);
     cur += 128;
     uint32_t k = 0;  // chunk holding `cur`; chunks <= k + 1 have landed
-    // a step consumes <= 64 bytes < one chunk, so at most one chunk boundary
+    // A step consumes <= 64 bytes, so four steps stay inside chunks k, k + 1
+    // (landed) and cross at most one chunk boundary: the ring is advanced
+    // once per four steps, keeping the branch off three of four recurrences.
     auto advance = [&]() {
         if ((cur >> 8) != k) {  // warp-uniform, taken about once per 7 steps
             __syncwarp();
@@ -115,6 +95,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
         }
     };
     advance();
+    if constexpr (sizeof(L) < 4) mbar_wait(&s_bar, 0);
     const uint32_t mask = nslots - 1;
     const uint32_t ltm = lanemask_lt();
     const uint32_t* ring32 = reinterpret_cast<const uint32_t*>(ring);
@@ -155,11 +136,21 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
         cur += __popc(b1) + __popc(b2);
         if (active) *out = (S)sym;
         out += 32;
-        advance();
     };
     if (steps > 0) {
         const uint32_t full = len / 32;
-        for (uint32_t s = 0; s < full; ++s) step(true);
+        uint32_t s = 0;
+        for (; s + 4 <= full; s += 4) {
+            step(true);
+            step(true);
+            step(true);
+            step(true);
+            advance();
+        }
+        for (; s < full; ++s) {
+            step(true);
+            advance();
+        }
         if (full < steps) step(full * 32 + lane < len);  // partial last step
     }
     cp_async_wait<0>();
@@ -177,9 +168,9 @@ SCZ_DEC2(uint32_t, uint32_t)
 #undef SCZ_DEC2
 
 // dynamic shared memory of k_rans_dec_v2 for a batch (max over tensors)
-inline size_t dec_v2_smem(int wpb, size_t lwidth, int n, uint32_t maxA) {
+inline size_t dec_v2_smem(int wpb, size_t lwidth, int n, uint32_t) {
     size_t s = (size_t)wpb * DRING;
-    if (lwidth < 4) s += (size_t)maxA * sizeof(uint2) + ((size_t)1 << n) * (4 + lwidth);
+    if (lwidth < 4) s += ((((size_t)1 << n) * (4 + lwidth)) + 15) & ~(size_t)15;
     return (s + 15) & ~(size_t)15;
 }
 

@@ -11,6 +11,10 @@
 //   K >= 64         few rows: shared-memory atomics aggregated by match_any.
 // Value 0 is never counted per row: it is N - sum(others), so bitmap padding
 // beyond T never matters.
+//
+// The grid also carries one fold CTA per candidate: the column histogram of
+// candidate K (nonzeros per p mod K) is H_P folded onto K columns (K | P),
+// stored after the candidate's K + 1 row bins, so k_select never touches H_P.
 #include "common.cuh"
 
 namespace scz {
@@ -29,9 +33,42 @@ struct RowHist2Params {
     uint32_t chunk_start[MAX_CAND + 1];
     uint32_t units_per_chunk[MAX_CAND];  // words (SWAR) or rows (other regimes)
     uint32_t rhist_off[MAX_CAND];
-    uint32_t* rhist;                   // [B][rhist_stride]; bin 0 filled later
+    uint32_t* rhist;                   // [B][rhist_stride]: per candidate K + 1 row bins, K column bins
     uint32_t rhist_stride;
+    const uint32_t* hp;                // [B][hp_stride] nonzeros per (p mod P)
+    uint32_t hp_stride, period;
+    uint32_t fold_start;               // chunks >= fold_start: fold CTA of candidate chunk - fold_start
 };
+
+__device__ void fold_columns(const RowHist2Params& p, uint32_t b, uint32_t c) {
+    const uint32_t K = p.cand_k[c], P = p.period;
+    if (K <= 1) return;
+    const uint32_t* hp = p.hp + (uint64_t)b * p.hp_stride;
+    uint32_t* ch = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c] + K + 1;
+    auto fold = [&](uint32_t j, uint32_t stride) -> uint32_t {
+        uint32_t a[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // independent load chains
+        for (; j + 7 * stride < P; j += 8 * stride) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] += __ldg(hp + j + u * stride);
+        }
+        for (; j < P; j += stride) a[0] += __ldg(hp + j);
+        return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    };
+    if (K <= RH_THREADS) {
+        extern __shared__ uint32_t s_dyn[];
+        for (uint32_t i = threadIdx.x; i < K; i += RH_THREADS) s_dyn[i] = 0;
+        __syncthreads();
+        const uint32_t L = K * (RH_THREADS / K);
+        if (threadIdx.x < L) {
+            const uint32_t acc = fold(threadIdx.x, L);
+            if (acc) atomicAdd(&s_dyn[threadIdx.x % K], acc);
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < K; i += RH_THREADS) ch[i] = s_dyn[i];
+    } else {
+        for (uint32_t col = threadIdx.x; col < K; col += RH_THREADS) ch[col] = fold(col, K);
+    }
+}
 
 template <int K>
 __device__ __forceinline__ void swar_counts(uint32_t w, uint32_t* c) {
@@ -74,8 +111,12 @@ __device__ void rowhist_swar(const uint32_t* bm, uint32_t w0, uint32_t w1, uint3
     if (threadIdx.x >= 1 && threadIdx.x <= K && s_c[threadIdx.x]) atomicAdd(gh + threadIdx.x, s_c[threadIdx.x]);
 }
 
-__global__ void __launch_bounds__(RH_THREADS) k_rowhist2(RowHist2Params p) {
+__global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__ RowHist2Params p) {
     const uint32_t chunk = blockIdx.x, b = blockIdx.y;
+    if (chunk >= p.fold_start) {
+        fold_columns(p, b, chunk - p.fold_start);
+        return;
+    }
     uint32_t c = 0;
     while (c + 1 < p.n_cand && p.chunk_start[c + 1] <= chunk) ++c;
     const uint32_t K = p.cand_k[c], N = p.cand_rows[c];
@@ -153,19 +194,6 @@ __global__ void __launch_bounds__(RH_THREADS) k_rowhist2(RowHist2Params p) {
     if (use_smem)
         for (uint32_t i = 1 + threadIdx.x; i <= K; i += RH_THREADS)
             if (s_big[i]) atomicAdd(gh + i, s_big[i]);
-}
-
-// r = 0 bin of every candidate: N - (rows with r >= 1)
-__global__ void k_rowhist_zero(RowHist2Params p) {
-    const uint32_t b = blockIdx.x;
-    for (uint32_t c = threadIdx.x; c < p.n_cand; c += blockDim.x) {
-        const uint32_t K = p.cand_k[c];
-        if (K <= 1) continue;
-        uint32_t* gh = p.rhist + (uint64_t)b * p.rhist_stride + p.rhist_off[c];
-        uint32_t s = 0;
-        for (uint32_t v = 1; v <= K; ++v) s += gh[v];
-        gh[0] = p.cand_rows[c] - s;
-    }
 }
 
 }  // namespace scz

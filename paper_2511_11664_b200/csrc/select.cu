@@ -2,8 +2,8 @@
 //
 //   k_select  grid (groups, B).  For every feasible candidate N (descending,
 //             optimizer.py:72-75) it assembles the histogram of D = v ++ c ++ r
-//             from the value histogram, the folded column histogram and the
-//             row-count histogram, prices it as l_D * H (optimizer.py:87-96,
+//             from the value histogram, the column histogram and the
+//             row-count histogram (k_rowhist2), prices it as l_D * H (optimizer.py:87-96,
 //             rans.py:216-223 with numpy's pairwise summation order), replays
 //             the early-stopped scan (optimizer.py:129-138), then normalises
 //             the chosen histogram (rans.py:88-131) and builds the encoder
@@ -20,10 +20,7 @@ struct SelectParams {
     uint32_t cand_k[MAX_CAND];
     uint32_t cand_n[MAX_CAND];
     uint32_t rhist_off[MAX_CAND];
-    uint32_t period;            // P (column histogram period)
-    const uint32_t* hp;
-    uint32_t hp_stride;
-    const uint32_t* rhist;
+    const uint32_t* rhist;      // per candidate: K + 1 row bins, then K column bins
     uint32_t rhist_stride;
     const uint32_t* vhist;      // [B][256]
     int q_bits;
@@ -45,60 +42,74 @@ struct SelectParams {
     uint32_t* ticket;           // [B], zeroed before the launch
     double* gcost;              // [B][MAX_CAND][2] (entropy, cost)
     uint32_t* gacnt;            // [B][MAX_CAND] alphabet per candidate
+    // SCZ_SELECT_PROBE=1: %globaltimer stamps per CTA (debug timeline)
+    unsigned long long* probe;
 };
+__device__ __forceinline__ unsigned long long sel_timer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SEL_PROBE(i)                                                                           \
+    do {                                                                                       \
+        if (p.probe && threadIdx.x == 0) p.probe[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (i)] = sel_timer(); \
+    } while (0)
 
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src
 // pairwise_sum) of a[0..n): blocks of <= 128 with 8 accumulators, halves
-// rounded down to a multiple of 8 above that.  Serial, one thread.
-__device__ double pairwise_sum(const double* a, uint32_t n) {
+// rounded down to a multiple of 8 above that.  One thread; the recursion is
+// replayed with an explicit stack (depth <= 25 for n < 2^31), so no device
+// call stack is needed.
+__device__ __forceinline__ double pairwise_leaf(const double* a, uint32_t n) {
     if (n < 8) {
         double r = 0.0;
         for (uint32_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
         return r;
     }
-    if (n <= 128) {
-        double r[8];
-        for (int j = 0; j < 8; ++j) r[j] = a[j];
-        uint32_t i;
-        for (i = 8; i < n - (n % 8); i += 8)
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-        return res;
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    uint32_t i;
+    for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
     }
-    uint32_t n2 = n / 2;
-    n2 -= n2 % 8;
-    return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
 }
 
-// The same order, recursion unrolled at compile time (no stack frame) for
-// n <= 128 * 2^D; used on the search path where n <= 1024.
-template <int D>
-__device__ __forceinline__ double pairwise_sum_d(const double* a, uint32_t n) {
-    if (D == 0 || n <= 128) {
-        if (n < 8) {
-            double r = 0.0;
-            for (uint32_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
-            return r;
+__device__ __noinline__ double pairwise_sum(const double* a, uint32_t n) {
+    uint32_t offs[26], lens[26];
+    double lefts[26];
+    uint32_t right = 0;  // bit d: the node at depth d is a right child
+    int d = 0;
+    offs[0] = 0;
+    lens[0] = n;
+    for (;;) {
+        while (lens[d] > 128) {  // descend to the leftmost leaf
+            uint32_t n2 = lens[d] / 2;
+            n2 -= n2 % 8;
+            offs[d + 1] = offs[d];
+            lens[d + 1] = n2;
+            right &= ~(1u << (d + 1));
+            ++d;
         }
-        double r[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = a[j];
-        uint32_t i;
-        for (i = 8; i < n - (n % 8); i += 8) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        double ret = pairwise_leaf(a + offs[d], lens[d]);
+        for (;;) {  // ascend past finished right children
+            if (d == 0) return ret;
+            if ((right >> d) & 1u) {
+                ret = __dadd_rn(lefts[d - 1], ret);
+                --d;
+            } else {  // left child done: visit its right sibling
+                lefts[d - 1] = ret;
+                offs[d] = offs[d - 1] + lens[d];
+                lens[d] = lens[d - 1] - lens[d];
+                right |= 1u << d;
+                break;
+            }
         }
-        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-        return res;
-    } else {
-        uint32_t n2 = n / 2;
-        n2 -= n2 % 8;
-        return __dadd_rn(pairwise_sum_d<(D > 0 ? D - 1 : 0)>(a, n2),
-                         pairwise_sum_d<(D > 0 ? D - 1 : 0)>(a + n2, n - n2));
     }
 }
 
@@ -140,7 +151,12 @@ __device__ uint32_t block_max32(uint32_t v, BlockScratch& s) {
 
 // rans.py:88-131 normalize_frequencies over counts[0..A) by one CTA.
 // Returns an SCZ_* status (same for all threads).
-__device__ int block_normalize(const uint32_t* counts, uint32_t A, int precision,
+// Code size matters here: k_select runs most of its code once per tensor, so
+// instruction-cache misses, not arithmetic, set its latency.  The bulky
+// helpers are out of line.
+__device__ __noinline__ double plog2p(double pp) { return __dmul_rn(pp, log2(pp)); }
+
+__device__ __noinline__ int block_normalize(const uint32_t* counts, uint32_t A, int precision,
                                uint32_t* freqs, double* rem, uint32_t* cum, BlockScratch& s) {
     unsigned long long total = 0, npresent = 0;
     for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
@@ -174,16 +190,23 @@ __device__ int block_normalize(const uint32_t* counts, uint32_t A, int precision
             for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) freqs[i] += 1;
         } else if (A <= 1024) {
             // small alphabets: rank every symbol against all others in one pass
-            for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS)
-                s.keys[i] = (unsigned long long)__double_as_longlong(rem[i]);
+            // (keys padded with zeros to a multiple of 8: a zero pad never
+            // outranks a real key, since pads sit at indices >= A)
+            const uint32_t A8 = (A + 7) & ~7u;
+            for (uint32_t i = threadIdx.x; i < A8; i += SEL_THREADS)
+                s.keys[i] = i < A ? (unsigned long long)__double_as_longlong(rem[i]) : 0ull;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
                 const unsigned long long ki = s.keys[i];
-                uint32_t rank = 0;
-                for (uint32_t j = 0; j < A; ++j) {
-                    const unsigned long long kj = s.keys[j];
-                    rank += (kj > ki) || (kj == ki && j < i);
+                uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (uint32_t j = 0; j < A8; j += 8) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const unsigned long long kj = s.keys[j + u];
+                        r[u] += (kj > ki) | ((kj == ki) & (j + u < i));
+                    }
                 }
+                const uint32_t rank = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
                 if (rank < k) freqs[i] += 1;
             }
         } else {
@@ -283,7 +306,7 @@ __device__ int block_normalize(const uint32_t* counts, uint32_t A, int precision
 }
 
 // Histogram of D for candidate c into counts[0..acap); returns alphabet.
-__device__ uint32_t assemble_counts(const SelectParams& p, uint32_t b, uint32_t c,
+__device__ __noinline__ uint32_t assemble_counts(const SelectParams& p, uint32_t b, uint32_t c,
                                     uint32_t* counts, BlockScratch& s) {
     const TensorState& st = p.state[b];
     const uint32_t K = p.cand_k[c], N = p.cand_n[c];
@@ -310,24 +333,8 @@ __device__ uint32_t assemble_counts(const SelectParams& p, uint32_t b, uint32_t 
         counts[i] = v;
     }
     __syncthreads();
-    if (K > 1) {
-        // column histogram: fold H_P (p mod P) onto p mod K
-        const uint32_t* hp = p.hp + (uint64_t)b * p.hp_stride;
-        const uint32_t P = p.period;
-        if (K <= SEL_THREADS) {
-            const uint32_t L = K * (SEL_THREADS / K);
-            if (threadIdx.x < L) {
-                uint32_t acc = 0;
-                for (uint32_t j = threadIdx.x; j < P; j += L) acc += hp[j];
-                if (acc) atomicAdd(&counts[threadIdx.x % K], acc);
-            }
-        } else {
-            for (uint32_t col = threadIdx.x; col < K; col += SEL_THREADS) {
-                uint32_t acc = 0;
-                for (uint32_t j = col; j < P; j += K) acc += hp[j];
-                counts[col] += acc;
-            }
-        }
+    if (K > 1) {  // column histogram (folded by k_rowhist2 after the row bins)
+        for (uint32_t col = threadIdx.x; col < K; col += SEL_THREADS) counts[col] += rh[K + 1 + col];
     }
     __syncthreads();
     uint32_t last = 0;
@@ -337,7 +344,7 @@ __device__ uint32_t assemble_counts(const SelectParams& p, uint32_t b, uint32_t 
 }
 
 // -(p log2 p).sum() over the positive counts, in numpy's order (rans.py:219-223).
-__device__ double block_entropy(const uint32_t* counts, uint32_t A, double total, double* terms,
+__device__ __noinline__ double block_entropy(const uint32_t* counts, uint32_t A, double total, double* terms,
                                 BlockScratch& s) {
     uint32_t carry = 0;
     for (uint32_t base = 0; base < A; base += SEL_THREADS) {
@@ -347,7 +354,7 @@ __device__ double block_entropy(const uint32_t* counts, uint32_t A, double total
         uint32_t ex = block_exclusive_scan<SEL_THREADS>(c > 0 ? 1u : 0u, s.scan, &tot);
         if (c > 0) {
             double pp = __ddiv_rn((double)c, total);
-            terms[carry + ex] = __dmul_rn(pp, log2(pp));
+            terms[carry + ex] = plog2p(pp);
         }
         carry += tot;
     }
@@ -359,38 +366,29 @@ __device__ double block_entropy(const uint32_t* counts, uint32_t A, double total
 }
 
 // Candidate pricing with one warp per candidate (search path, A <= 1024):
-// dynamic smem = [H_P if it fits][vhist][row histograms if they fit]
+// dynamic smem = [vhist][row + column histograms if they fit]
 //                [per warp: terms f64[acap], counts u32[acap]],
 // the histograms staged with one batch of cp.async copies.
 constexpr uint32_t SEL_WARP_ACAP = 1024;
-constexpr uint32_t SEL_HP_SMEM_MAX = 16384;  // H_P entries staged in smem (64 KB)
-constexpr uint32_t SEL_RH_SMEM_MAX = 8192;   // row-histogram words staged in smem
+constexpr uint32_t SEL_RH_SMEM_MAX = 16384;  // histogram words staged in smem (64 KB)
 
-__host__ __device__ inline size_t select_smem_bytes(uint32_t acap, uint32_t period, uint32_t rh_stride) {
+__host__ __device__ inline size_t select_smem_bytes(uint32_t acap, uint32_t rh_stride) {
     if (acap > SEL_WARP_ACAP) return 0;
     size_t s = (size_t)(SEL_THREADS / 32) * acap * (4 + 8) + 256 * 4;
-    if (period <= SEL_HP_SMEM_MAX) s += (size_t)period * 4;
     if (rh_stride <= SEL_RH_SMEM_MAX) s += ((size_t)rh_stride * 4 + 15) & ~(size_t)15;
     return (s + 15) & ~(size_t)15;
 }
 
-__device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, uint32_t g, BlockScratch& s) {
+// Returns the start of the per-warp scratch (reused by the final normalise).
+__device__ uint8_t* warp_parallel_costs(const SelectParams& p, uint32_t b, uint32_t g, BlockScratch& s) {
     extern __shared__ __align__(16) uint8_t sel_dyn[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const TensorState& st = p.state[b];
     const uint64_t nnz = st.nnz;
-    const uint32_t P = p.period;
-    const bool hp_smem = P <= SEL_HP_SMEM_MAX;
-    const uint32_t* ghp = p.hp + (uint64_t)b * p.hp_stride;
     const uint32_t* grh = p.rhist + (uint64_t)b * p.rhist_stride;
     const uint32_t* gvh = p.vhist + (uint64_t)b * 256;
     const bool rh_smem = p.rhist_stride <= SEL_RH_SMEM_MAX;
     uint8_t* dyn = sel_dyn;
-    uint32_t* s_hp = reinterpret_cast<uint32_t*>(dyn);
-    if (hp_smem) {  // P is a multiple of 32 and the rows 128-byte aligned: 16-byte copies
-        for (uint32_t i = threadIdx.x; i < P / 4; i += SEL_THREADS) cp_async16(s_hp + 4 * i, ghp + 4 * i);
-        dyn += (size_t)P * 4;
-    }
     uint32_t* s_vh = reinterpret_cast<uint32_t*>(dyn);
     if (threadIdx.x < 64) cp_async16(s_vh + 4 * threadIdx.x, gvh + 4 * threadIdx.x);
     dyn += 256 * 4;
@@ -402,7 +400,7 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, uint32_t 
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    const uint32_t* hp = hp_smem ? s_hp : ghp;
+    SEL_PROBE(1);
     const uint32_t* rhb = rh_smem ? s_rh : grh;
     double* terms = reinterpret_cast<double*>(dyn) + (size_t)warp * p.acap;
     uint32_t* cb = reinterpret_cast<uint32_t*>(dyn + (size_t)(SEL_THREADS / 32) * p.acap * 8) +
@@ -431,37 +429,8 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, uint32_t 
             cb[i] = v;
         }
         __syncwarp();
-        if (K > 1) {  // column histogram: fold H_P (p mod P) onto p mod K
-            if (K <= 32) {
-                const uint32_t Lw = K * (32 / K);
-                if (lane < Lw) {
-                    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // 4 independent chains
-                    uint32_t j = lane;
-                    for (; j + 3 * Lw < P; j += 4 * Lw) {
-                        a0 += hp[j];
-                        a1 += hp[j + Lw];
-                        a2 += hp[j + 2 * Lw];
-                        a3 += hp[j + 3 * Lw];
-                    }
-                    for (; j < P; j += Lw) a0 += hp[j];
-                    const uint32_t acc = a0 + a1 + a2 + a3;
-                    if (acc) atomicAdd(&cb[lane % K], acc);
-                }
-            } else {
-                for (uint32_t col = lane; col < K; col += 32) {
-                    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // independent chains
-                    uint32_t j = col;
-                    for (; j + 3 * K < P; j += 4 * K) {
-                        a0 += hp[j];
-                        a1 += hp[j + K];
-                        a2 += hp[j + 2 * K];
-                        a3 += hp[j + 3 * K];
-                    }
-                    for (; j < P; j += K) a0 += hp[j];
-                    cb[col] += a0 + a1 + a2 + a3;
-                }
-            }
-        }
+        if (K > 1)  // column histogram (folded by k_rowhist2 after the row bins)
+            for (uint32_t col = lane; col < K; col += 32) cb[col] += rh[K + 1 + col];
         __syncwarp();
         uint32_t last = 0;
         for (uint32_t i = lane; i < ub; i += 32)
@@ -480,20 +449,29 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, uint32_t 
         // entropy over the positive counts in index order (rans.py:219-223)
         const uint64_t len = 2 * nnz + N;
         const double total = (double)len;
+        // two rounds of 4 independent divisions / logarithms per lane (ILP)
         uint32_t m = 0;
-        for (uint32_t base = 0; base < A; base += 32) {
-            const uint32_t i = base + lane;
-            const uint32_t cnt = i < A ? cb[i] : 0;
-            const uint32_t bal = __ballot_sync(0xffffffffu, cnt > 0);
-            if (cnt > 0) {
-                const double pp = __ddiv_rn((double)cnt, total);
-                terms[m + __popc(bal & lanemask_lt())] = __dmul_rn(pp, log2(pp));
+        for (uint32_t base = 0; base < A; base += 128) {
+            double pp[4];
+            uint32_t pos[4];
+            bool has[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = base + 32 * u + lane;
+                const uint32_t cnt = i < A ? cb[i] : 0;
+                const uint32_t bal = __ballot_sync(0xffffffffu, cnt > 0);
+                has[u] = cnt > 0;
+                pos[u] = m + __popc(bal & lanemask_lt());
+                m += __popc(bal);
+                pp[u] = __ddiv_rn((double)(cnt | !has[u]), total);
             }
-            m += __popc(bal);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (has[u]) terms[pos[u]] = __dmul_rn(pp[u], log2(pp[u]));
         }
         __syncwarp();
         if (lane == 0) {
-            const double h = -(m <= 1024 ? pairwise_sum_d<3>(terms, m) : pairwise_sum(terms, m));
+            const double h = -pairwise_sum(terms, m);
             s.ents[c] = h;
             s.costs[c] = __dmul_rn((double)len, h);
             if (p.groups > 1) {
@@ -505,6 +483,8 @@ __device__ void warp_parallel_costs(const SelectParams& p, uint32_t b, uint32_t 
         __syncwarp();
     }
     __syncthreads();
+    SEL_PROBE(2);
+    return dyn;
 }
 
 // Multi-CTA pricing: true in the CTA that arrives last for tensor b, which
@@ -527,8 +507,9 @@ __device__ bool gather_costs(const SelectParams& p, uint32_t b, BlockScratch& s)
     return true;
 }
 
-__global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
+__global__ void __launch_bounds__(SEL_THREADS) k_select(const __grid_constant__ SelectParams p) {
     const uint32_t b = blockIdx.y, g = blockIdx.x;
+    SEL_PROBE(0);
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
     __shared__ BlockScratch s;
@@ -537,10 +518,12 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
     const uint64_t nnz = st.nnz;
 
     uint32_t chosen = 0, flags = 0, evaluated = 0;
+    uint8_t* work = nullptr;  // shared scratch for the final normalise (warp path)
     if (p.searching) {
         if (p.acap <= SEL_WARP_ACAP) {
-            warp_parallel_costs(p, b, g, s);
+            work = warp_parallel_costs(p, b, g, s);
             if (!gather_costs(p, b, s)) return;
+            SEL_PROBE(3);
         } else for (uint32_t c = 0; c < p.n_cand; ++c) {
             uint32_t A = assemble_counts(p, b, c, counts, s);
             if (p.dump) {
@@ -607,12 +590,33 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
     } else {
         A = assemble_counts(p, b, chosen, counts, s);
     }
-    uint32_t* freqs = p.freqs + (uint64_t)b * p.acap;
-    uint32_t* cum = p.cum + (uint64_t)b * (p.acap + 1);
-    int status = block_normalize(ccounts, A, p.precision, freqs, terms, cum, s);
+    uint32_t* gfreqs = p.freqs + (uint64_t)b * p.acap;
+    uint32_t* gcum = p.cum + (uint64_t)b * (p.acap + 1);
+    uint32_t* freqs = gfreqs;
+    uint32_t* cum = gcum;
+    double* rem = terms;
+    if (work) {  // normalise in shared memory (per-warp scratch >= 20 bytes per symbol)
+        rem = reinterpret_cast<double*>(work);
+        uint32_t* scnt = reinterpret_cast<uint32_t*>(rem + p.acap);
+        freqs = scnt + p.acap;
+        cum = freqs + p.acap;
+        for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) scnt[i] = ccounts[i];
+        __syncthreads();
+        ccounts = scnt;
+    }
+    SEL_PROBE(4);
+    int status = block_normalize(ccounts, A, p.precision, freqs, rem, cum, s);
+    SEL_PROBE(5);
     EncTab* et = p.enctab + (uint64_t)b * p.acap;
     if (status == SCZ_OK)
-        for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) make_enc_tab(freqs[i], cum[i], &et[i]);
+        for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+            make_enc_tab(freqs[i], cum[i], &et[i]);
+            if (work) {
+                gfreqs[i] = freqs[i];
+                gcum[i] = cum[i];
+            }
+        }
+    if (work && status == SCZ_OK && threadIdx.x == 0) gcum[A] = cum[A];
     if (threadIdx.x == 0) {
         st.status = status;
         st.cand_index = chosen;
@@ -624,6 +628,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelectParams p) {
         st.sym_bytes = K <= 255 ? 1u : (K <= 65535 ? 2u : 4u);
         st.search_flags = flags;
         st.n_evaluated = evaluated;
+        SEL_PROBE(6);
     }
 }
 
