@@ -68,6 +68,20 @@ struct HostBuf {
         g_alloc_gen.fetch_add(1);
         return e;
     }
+    // grow to n bytes keeping the first `used` bytes (callers sync first)
+    cudaError_t grow_keep(size_t n, size_t used) {
+        if (n <= cap) return cudaSuccess;
+        void* np = nullptr;
+        size_t want = std::max<size_t>(n + n / 4, 4096);
+        cudaError_t e = cudaMallocHost(&np, want);
+        if (e != cudaSuccess) return e;
+        if (used && p) memcpy(np, p, used);
+        if (p) cudaFreeHost(p);
+        p = np;
+        cap = want;
+        g_alloc_gen.fetch_add(1);
+        return cudaSuccess;
+    }
     template <typename T>
     T* as() const { return reinterpret_cast<T*>(p); }
     void release() {
@@ -147,6 +161,24 @@ struct scz_ctx {
     int32_t* h_status_async = nullptr;
     uint32_t last_batch = 0;
     HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
+    // host-buffer batch calls: a copy stream and per-chunk events so PCIe
+    // transfers of chunk i + 1 overlap the kernels of chunk i
+    cudaStream_t xfer = nullptr, xfer_out = nullptr;
+    std::vector<cudaEvent_t> xev;
+    int xfer_init() {
+        if (!xfer) {
+            if (cudaStreamCreateWithFlags(&xfer, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&xfer_out, cudaStreamNonBlocking) != cudaSuccess)
+                return fail(SCZ_CUDA_ERROR, "copy stream creation failed");
+        }
+        while (xev.size() < 64) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                return fail(SCZ_CUDA_ERROR, "event creation failed");
+            xev.push_back(e);
+        }
+        return SCZ_OK;
+    }
     DevBuf ready, candcnt, selbuf, dlut, probe;
     // CUDA-graph cache: a launch sequence seen twice with the same key and
     // allocation generation is captured once and replayed afterwards.
@@ -993,8 +1025,15 @@ void scz_ctx_destroy(scz_ctx* ctx) {
                       &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready, &ctx->candcnt})
         b->release();
     for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
-                       &ctx->h_misc})
+                       &ctx->h_misc, &ctx->hb_info, &ctx->hb_payload, &ctx->hb_freqs, &ctx->hb_blocks})
         b->release();
+    if (ctx->xfer) {
+        cudaStreamSynchronize(ctx->xfer);
+        cudaStreamSynchronize(ctx->xfer_out);
+        cudaStreamDestroy(ctx->xfer);
+        cudaStreamDestroy(ctx->xfer_out);
+    }
+    for (cudaEvent_t e : ctx->xev) cudaEventDestroy(e);
     for (auto& g : ctx->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaStreamDestroy(ctx->stream);
@@ -1606,6 +1645,22 @@ int scz_search(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, const uint6
     return SCZ_OK;
 }
 
+// Batch chunks for the host-buffer entry points (SCZ_CHUNK_BYTES, at most
+// 8): the copies of one chunk then overlap the kernels of another.  Off by
+// default: measured on B200 + PCIe 5, chunking speeds a lone compress call
+// up by ~17% but loses 2x when a compress and a decompress share the link
+// (the pipelined round trip bench.py times), where one bulk copy per
+// direction per call saturates both directions.
+static uint32_t n_chunks(uint64_t bytes, uint32_t batch) {
+    static const uint64_t chunk_bytes = [] {
+        const char* e = getenv("SCZ_CHUNK_BYTES");
+        const unsigned long long v = e ? strtoull(e, nullptr, 10) : 0;
+        return v ? (uint64_t)v : ~0ull;
+    }();
+    const uint64_t want = std::max<uint64_t>(1, std::min<uint64_t>(8, bytes / chunk_bytes));
+    return (uint32_t)std::min<uint64_t>(want, batch);
+}
+
 int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t batch, int q_bits,
                        int64_t n_rows, int precision, int format, uint32_t lanes, uint32_t block_syms,
                        const scz_info** infos, const uint8_t** payload, const uint32_t** freqs,
@@ -1613,31 +1668,65 @@ int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t 
     if (!ctx || !h_x || !infos) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     ctx->mark();
-    EncPlan pl;
-    int st = plan_encode(ctx, total, batch, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
-    if (st) return st;
+    int st;
+    if ((st = ctx->xfer_init()) != SCZ_OK) return st;
+    const uint32_t nch = n_chunks((uint64_t)batch * total * 4, batch);
+    const uint32_t per = ceil_div_u32(batch, nch);
+    EncPlan pl;  // per-chunk plan (acap / nblk_cap do not depend on the batch size)
+    if ((st = plan_encode(ctx, total, std::min(per, batch), q_bits, n_rows, precision, format, lanes, block_syms,
+                          &pl)) != SCZ_OK)
+        return st;
     cudaStream_t s = ctx->stream;
     CK(ctx->x_in.ensure((size_t)batch * total * 4));
-    CK(cudaMemcpyAsync(ctx->x_in.p, h_x, (size_t)batch * total * 4, cudaMemcpyHostToDevice, s));
-    const std::string key = key_of("enc", {(uint64_t)(uintptr_t)ctx->x_in.p, total, batch, (uint64_t)q_bits,
-                                           (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format,
-                                           lanes, block_syms});
-    if ((st = graph_run(ctx, key, [&] { return run_encode(ctx, ctx->x_in.as<float>(), pl, nullptr); })) != SCZ_OK)
-        return st;
-    CK(ctx->hb_info.ensure((size_t)batch * sizeof(scz_info)));
-    scz_info* hi = ctx->hb_info.as<scz_info>();
-    CK(cudaMemcpyAsync(hi, ctx->info.p, (size_t)batch * sizeof(scz_info), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    uint64_t ptot = 0;
-    for (uint32_t i = 0; i < batch; ++i)
-        if (hi[i].status == SCZ_OK) ptot = std::max(ptot, hi[i].payload_off + hi[i].payload_len);
     const uint64_t ftot = (uint64_t)batch * pl.acap, btot = (uint64_t)batch * pl.nblk_cap;
-    CK(ctx->hb_payload.ensure(ptot + 16));
+    CK(ctx->hb_info.ensure((size_t)batch * sizeof(scz_info)));
     CK(ctx->hb_freqs.ensure(ftot * 4));
     CK(ctx->hb_blocks.ensure(btot * 4));
-    CK(cudaMemcpyAsync(ctx->hb_payload.p, ctx->payload.p, ptot, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ctx->hb_freqs.p, ctx->freqs.p, ftot * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ctx->hb_blocks.p, ctx->block_len.p, btot * 4, cudaMemcpyDeviceToHost, s));
+    scz_info* hi = ctx->hb_info.as<scz_info>();
+    // every chunk's features go up on the copy stream right away
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t b0 = c * per, nb = b0 < batch ? std::min(per, batch - b0) : 0;
+        if (!nb) break;
+        const size_t off = (size_t)b0 * total * 4;
+        CK(cudaMemcpyAsync(ctx->x_in.as<uint8_t>() + off, reinterpret_cast<const uint8_t*>(h_x) + off,
+                           (size_t)nb * total * 4, cudaMemcpyHostToDevice, ctx->xfer));
+        CK(cudaEventRecord(ctx->xev[c], ctx->xfer));
+    }
+    uint64_t ptot = 0;
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t b0 = c * per, nb = b0 < batch ? std::min(per, batch - b0) : 0;
+        if (!nb) break;
+        EncPlan cp = pl;
+        if (nb != pl.B && (st = plan_encode(ctx, total, nb, q_bits, n_rows, precision, format, lanes,
+                                            block_syms, &cp)) != SCZ_OK)
+            return st;
+        CK(cudaStreamWaitEvent(s, ctx->xev[c], 0));
+        const float* dx = ctx->x_in.as<float>() + (size_t)b0 * total;
+        const std::string key = key_of("enc", {(uint64_t)(uintptr_t)dx, total, nb, (uint64_t)q_bits,
+                                               (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format, lanes,
+                                               block_syms});
+        if ((st = graph_run(ctx, key, [&] { return run_encode(ctx, dx, cp, nullptr); })) != SCZ_OK) return st;
+        CK(cudaMemcpyAsync(hi + b0, ctx->info.p, (size_t)nb * sizeof(scz_info), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        uint64_t cpt = 0;
+        for (uint32_t i = 0; i < nb; ++i)
+            if (hi[b0 + i].status == SCZ_OK) cpt = std::max(cpt, hi[b0 + i].payload_off + hi[b0 + i].payload_len);
+        CK(ctx->hb_payload.grow_keep(ptot + cpt + 16, ptot));
+        // chunk outputs land at their batch-global places; the next chunk's
+        // kernels queue behind these copies on the same stream
+        CK(cudaMemcpyAsync(ctx->hb_payload.as<uint8_t>() + ptot, ctx->payload.p, cpt, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->hb_freqs.as<uint32_t>() + (size_t)b0 * pl.acap, ctx->freqs.p,
+                           (size_t)nb * pl.acap * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->hb_blocks.as<uint32_t>() + (size_t)b0 * pl.nblk_cap, ctx->block_len.p,
+                           (size_t)nb * pl.nblk_cap * 4, cudaMemcpyDeviceToHost, s));
+        for (uint32_t i = 0; i < nb; ++i) {
+            scz_info& in = hi[b0 + i];
+            in.payload_off += ptot;
+            in.freqs_off += (uint64_t)b0 * pl.acap;
+            in.blocks_off += (uint64_t)b0 * pl.nblk_cap;
+        }
+        ptot += cpt;
+    }
     CK(cudaStreamSynchronize(s));
     *infos = hi;
     if (payload) *payload = ctx->hb_payload.as<uint8_t>();
@@ -1667,21 +1756,55 @@ int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, c
             return ctx->fail(SCZ_INVALID_INPUT, "info offsets exceed the given buffers");
         out_total += h_info[b].total;
     }
+    int st;
+    if ((st = ctx->xfer_init()) != SCZ_OK) return st;
     cudaStream_t s = ctx->stream;
     CK(ctx->dpayload.ensure(payload_bytes + 4096));
     CK(ctx->dfreqs.ensure(freqs_count * 4 + 4));
     CK(ctx->dblocks.ensure(blocks_count * 4 + 4));
     CK(ctx->dout.ensure(out_total * 4));
-    CK(cudaMemcpyAsync(ctx->dpayload.p, h_payload, payload_bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(ctx->dfreqs.p, h_freqs, freqs_count * 4, cudaMemcpyHostToDevice, s));
+    // copy stream: tables, then each chunk's payload range; compute stream:
+    // decode chunk c; second copy stream: chunk c's features back to the
+    // host while chunk c + 1 decodes
+    CK(cudaMemcpyAsync(ctx->dfreqs.p, h_freqs, freqs_count * 4, cudaMemcpyHostToDevice, ctx->xfer));
     if (blocks_count && h_blocks)
-        CK(cudaMemcpyAsync(ctx->dblocks.p, h_blocks, blocks_count * 4, cudaMemcpyHostToDevice, s));
-    int st = run_decode(ctx, h_info, batch, ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
-                        ctx->dpayload.as<uint8_t>(), ctx->dout.as<float>(), false, nullptr, nullptr);
-    if (st) return st;
-    CK(cudaMemcpyAsync(h_out, ctx->dout.p, out_total * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_status, ctx->dstatus.p, (size_t)batch * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->dblocks.p, h_blocks, blocks_count * 4, cudaMemcpyHostToDevice, ctx->xfer));
+    const uint32_t nch = n_chunks(out_total * 4, batch);
+    const uint32_t per = ceil_div_u32(batch, nch);
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t b0 = c * per, nb = b0 < batch ? std::min(per, batch - b0) : 0;
+        if (!nb) break;
+        uint64_t lo = UINT64_MAX, hi_end = 0;
+        for (uint32_t i = b0; i < b0 + nb; ++i) {
+            lo = std::min<uint64_t>(lo, h_info[i].payload_off);
+            hi_end = std::max<uint64_t>(hi_end, h_info[i].payload_off + h_info[i].payload_len);
+        }
+        if (hi_end > lo)
+            CK(cudaMemcpyAsync(ctx->dpayload.as<uint8_t>() + lo, h_payload + lo, hi_end - lo,
+                               cudaMemcpyHostToDevice, ctx->xfer));
+        CK(cudaEventRecord(ctx->xev[1 + c], ctx->xfer));
+    }
+    uint64_t out_base = 0;
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t b0 = c * per, nb = b0 < batch ? std::min(per, batch - b0) : 0;
+        if (!nb) break;
+        uint64_t n_out = 0;
+        for (uint32_t i = b0; i < b0 + nb; ++i) n_out += h_info[i].total;
+        if (c) CK(cudaStreamSynchronize(s));  // run_decode restages its pinned header copy
+        CK(cudaStreamWaitEvent(s, ctx->xev[1 + c], 0));
+        if ((st = run_decode(ctx, h_info + b0, nb, ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
+                             ctx->dpayload.as<uint8_t>(), ctx->dout.as<float>() + out_base, false, nullptr,
+                             nullptr)) != SCZ_OK)
+            return st;
+        CK(cudaEventRecord(ctx->xev[16 + c], s));
+        CK(cudaMemcpyAsync(h_status + b0, ctx->dstatus.p, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamWaitEvent(ctx->xfer_out, ctx->xev[16 + c], 0));
+        CK(cudaMemcpyAsync(h_out + out_base, ctx->dout.as<float>() + out_base, n_out * 4,
+                           cudaMemcpyDeviceToHost, ctx->xfer_out));
+        out_base += n_out;
+    }
     CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(ctx->xfer_out));
     return SCZ_OK;
 }
 

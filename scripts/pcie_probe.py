@@ -1,0 +1,32 @@
+"""PCIe probe: H2D alone, D2H alone, and both at once (pinned, 512 MB each)."""
+import time
+
+import torch
+
+n = 512 << 20
+h1 = torch.empty(n, dtype=torch.uint8).pin_memory()
+h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+d1 = torch.empty(n, dtype=torch.uint8, device="cuda")
+d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def run(h2d, d2h, reps=5):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(reps):
+        if h2d:
+            with torch.cuda.stream(s1):
+                d1.copy_(h1, non_blocking=True)
+        if d2h:
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    return reps * n * (int(h2d) + int(d2h)) / dt / 1e9
+
+
+run(True, True, 2)
+print("h2d GB/s", run(True, False))
+print("d2h GB/s", run(False, True))
+print("both GB/s (sum)", run(True, True))

@@ -464,3 +464,30 @@ def test_graph_replay_tracks_new_inputs_and_reallocation():
             assert container.to_bytes(c) == orc.to_bytes(ref), (i, fmt)
             out = sz.decompress(c)
             assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32)), (i, fmt)
+
+
+def test_chunked_host_batch_calls(tmp_path):
+    """compress_many / decompress_many split large batches into chunks whose
+    copies overlap the kernels; with tiny chunks forced (SCZ_CHUNK_BYTES) the
+    containers and reconstructions equal the single-tensor path."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path.insert(0, %r); import numpy as np; import paper_2511_11664_b200 as sz\n"
+        "from paper_2511_11664_b200 import container\n"
+        "ts = [sz.gen_synthetic('relu-laplace', [1, 32, 28, 28], 0.3 + 0.02 * i, 50 + i) for i in range(19)]\n"
+        "for fmt in (1, 2):\n"
+        "    many = container.compress_many(ts, 8, format=fmt, block_syms=2048)\n"
+        "    for t, c in zip(ts, many):\n"
+        "        assert container.to_bytes(c) == container.to_bytes(sz.compress(t, 8, format=fmt, block_syms=2048))\n"
+        "    outs = container.decompress_many(many)\n"
+        "    for c, o in zip(many, outs):\n"
+        "        assert np.array_equal(o.data.view(np.uint32), sz.decompress(c).data.view(np.uint32))\n"
+        "print('ok')\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env["SCZ_CHUNK_BYTES"] = str(3 * 32 * 28 * 28 * 4)  # 3 tensors per chunk -> 7 chunks
+    out = subprocess.run([sys.executable, "-c", code % root], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
