@@ -272,9 +272,9 @@ struct scz_ctx {
     }
 };
 
-#define CK(expr)                                         \
+#define CK(...)                                          \
     do {                                                 \
-        int _st = ctx->cuda((expr), #expr);              \
+        int _st = ctx->cuda((__VA_ARGS__), #__VA_ARGS__); \
         if (_st != SCZ_OK) return _st;                   \
     } while (0)
 #define LAUNCHED(name)                                   \
@@ -286,6 +286,26 @@ struct scz_ctx {
 namespace {
 
 // Everything the encode kernels need for one batch geometry.
+// Pipeline kernels go out with programmatic dependent launch: the next
+// kernel's CTAs are scheduled while the previous grid drains, and wait in
+// pdl_wait() (every kernel's first statement) for its completion.  Inside a
+// captured graph these become programmatic edges.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 struct EncPlan {
     uint64_t T;
     uint32_t B;
@@ -382,6 +402,7 @@ __global__ void k_finalize(TensorState* state, uint32_t B, uint64_t total, int q
                            int format, uint32_t block_syms, const uint32_t* block_len,
                            uint32_t slots_per_tensor, uint32_t* blk_off, uint32_t acap,
                            scz_info* info, uint32_t* ticket) {
+    pdl_wait();
     const uint32_t b = blockIdx.x;
     TensorState& st = state[b];
     __shared__ uint32_t s_scan[33];
@@ -451,6 +472,7 @@ __global__ void k_finalize(TensorState* state, uint32_t B, uint64_t total, int q
 __global__ void __launch_bounds__(256) k_pack(const scz_info* info, const uint8_t* slots, uint64_t slot_cap,
                                               uint32_t slots_per_tensor, const uint32_t* block_len,
                                               const uint32_t* blk_off, uint8_t* payload) {
+    pdl_wait();
     const uint32_t b = blockIdx.y, blk = blockIdx.x;
     const scz_info& in = info[b];
     if (in.status != SCZ_OK || blk >= in.n_blocks) return;
@@ -613,12 +635,12 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     } else {
         StatsParams sp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
                        ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>()};
-        k_stats<<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(sp);
+        CK(launch_pdl(k_stats, dim3(pl.n_tiles, B), TILE_THREADS, 0, s, sp));
         LAUNCHED("k_stats");
         QuantParams qp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
                        ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(), ctx->v8.as<uint8_t>(),
                        ctx->vhist.as<uint32_t>(), nullptr, dstride};
-        k_quantize<false><<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(qp);
+        CK(launch_pdl(k_quantize<false>, dim3(pl.n_tiles, B), TILE_THREADS, 0, s, qp));
         LAUNCHED("k_quantize");
     }
 
@@ -638,7 +660,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         cp.hp = ctx->hp.as<uint32_t>();
         cp.hp_stride = (uint32_t)pl.period;
         dim3 g(ceil_div_u32(cp.period_words, 128), ceil_div_u32(cp.n_rows, cp.rows_per_cta), B);
-        k_colhist<<<g, 128, 0, s>>>(cp);
+        CK(launch_pdl(k_colhist, g, 128, 0, s, cp));
         LAUNCHED("k_colhist");
 
         RowHist2Params rp;
@@ -679,7 +701,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         rp.fold_start = chunks;  // + one column-fold CTA per candidate
         {
             size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
-            k_rowhist2<<<dim3(chunks + ncand, B), RH_THREADS, smem, s>>>(rp);
+            CK(launch_pdl(k_rowhist2, dim3(chunks + ncand, B), RH_THREADS, smem, s, rp));
             LAUNCHED("k_rowhist");
         }
     }
@@ -736,7 +758,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         CK(cudaMemsetAsync(ctx->probe.p, 0, (size_t)B * sel.groups * 16 * 8, s));
         sel.probe = ctx->probe.as<unsigned long long>();
     }
-    k_select<<<dim3(sel.groups, B), SEL_THREADS, sel_smem, s>>>(sel);
+    CK(launch_pdl(k_select, dim3(sel.groups, B), SEL_THREADS, sel_smem, s, sel));
     LAUNCHED("k_select");
     if (probe) {
         std::vector<unsigned long long> h((size_t)B * sel.groups * 16);
@@ -767,7 +789,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
             m2.cr_stride = dstride;
             m2.after_v = 1;
         }
-        k_materialize<S><<<dim3(pl.n_tiles, B), TILE_THREADS, 0, s>>>(m2);
+        CK(launch_pdl(k_materialize<S>, dim3(pl.n_tiles, B), TILE_THREADS, 0, s, m2));
         LAUNCHED(wname<S>("k_materialize"));
         auto launch = [&](auto src) -> int {
             using Src = decltype(src);
@@ -775,13 +797,13 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
                 if (enc_smem_tab) {
                     CK(cudaFuncSetAttribute(k_rans_enc_v2<Src, true, false>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)enc_smem));
-                    k_rans_enc_v2<Src, true, false><<<g_enc2, ENC2_WPB * 32, enc_smem, s>>>(ep, src);
+                    CK(launch_pdl(k_rans_enc_v2<Src, true, false>, g_enc2, ENC2_WPB * 32, enc_smem, s, ep, src));
                 } else {
-                    k_rans_enc_v2<Src, false, false><<<g_enc2, ENC2_WPB * 32, 0, s>>>(ep, src);
+                    CK(launch_pdl(k_rans_enc_v2<Src, false, false>, g_enc2, ENC2_WPB * 32, 0, s, ep, src));
                 }
                 LAUNCHED(wname<S>("k_rans_enc_v2"));
             } else {
-                k_rans_enc_v1<Src><<<B, 32, 0, s>>>(ep, src);
+                CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
                 LAUNCHED(wname<S>("k_rans_enc_v1"));
             }
             return SCZ_OK;
@@ -794,14 +816,14 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     if (pl.widths & 2) { if ((st = run_width(uint16_t{})) != SCZ_OK) return st; }
     if (pl.widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
 
-    k_finalize<<<B, 256, 0, s>>>(ctx->state.as<TensorState>(), B, T, pl.q_bits, pl.precision, pl.format,
+    CK(launch_pdl(k_finalize, B, 256, 0, s, ctx->state.as<TensorState>(), B, T, pl.q_bits, pl.precision, pl.format,
                                  pl.block_syms, ctx->block_len.as<uint32_t>(), pl.nblk_cap,
                                  ctx->blk_off.as<uint32_t>(), pl.acap, ctx->info.as<scz_info>(),
-                                 ctx->ticket.as<uint32_t>());
+                                 ctx->ticket.as<uint32_t>()));
     LAUNCHED("k_finalize");
-    k_pack<<<dim3(pl.nblk_cap, B), 256, 0, s>>>(ctx->info.as<scz_info>(), ctx->slots.as<uint8_t>(),
+    CK(launch_pdl(k_pack, dim3(pl.nblk_cap, B), 256, 0, s, ctx->info.as<scz_info>(), ctx->slots.as<uint8_t>(),
                                                  pl.slot_cap, pl.nblk_cap, ctx->block_len.as<uint32_t>(),
-                                                 ctx->blk_off.as<uint32_t>(), ctx->payload.as<uint8_t>());
+                                                 ctx->blk_off.as<uint32_t>(), ctx->payload.as<uint8_t>()));
     LAUNCHED("k_pack");
     return SCZ_OK;
 }
@@ -901,7 +923,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
                  ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
                  ctx->dstatus.as<int32_t>(), ctx->dlut.as<uint8_t>(), lut_stride};
-    k_dec_prepare<<<dim3(1 + lut_slices, B), 256, 0, s>>>(dp);
+    CK(launch_pdl(k_dec_prepare, dim3(1 + lut_slices, B), 256, 0, s, dp));
     LAUNCHED("k_dec_prepare");
     RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<uint32_t>(), nchunk_cap,
                  ctx->dstatus.as<int32_t>(), d_out, ctx->out_off.as<uint64_t>(), q_out, mask_out};
@@ -917,17 +939,17 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
             auto kern = small ? k_rans_dec_v2<S, L, DEC2_WPB_SMALL> : k_rans_dec_v2<S, L, DEC2_WPB>;
             size_t smem = dec_v2_smem(wpb, sizeof(L), maxn, (uint32_t)maxA);
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<dim3(ceil_div_u32(nblk_cap, wpb), B), wpb * 32, smem, s>>>(dp);
+            CK(launch_pdl(kern, dim3(ceil_div_u32(nblk_cap, wpb), B), wpb * 32, smem, s, dp));
             LAUNCHED(wname<S>("k_rans_dec_v2"));
         }
         if (any_v1) {
             size_t smem = RING + tab + lut;
             CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-            k_rans_dec_v1<S, L><<<B, 32, smem, s>>>(dp);
+            CK(launch_pdl(k_rans_dec_v1<S, L>, B, 32, smem, s, dp));
             LAUNCHED(wname<S>("k_rans_dec_v1"));
         }
-        k_row_sums<S><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+        CK(launch_pdl(k_row_sums<S>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
         LAUNCHED(wname<S>("k_row_sums"));
         return SCZ_OK;
     };
@@ -937,34 +959,34 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     if (widths & 1) { if ((st = run_width(uint8_t{})) != SCZ_OK) return st; }
     if (widths & 2) { if ((st = run_width(uint16_t{})) != SCZ_OK) return st; }
     if (widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
-    k_row_scan<<<B, 256, 0, s>>>(rp);
+    CK(launch_pdl(k_row_scan, B, 256, 0, s, rp));
     LAUNCHED("k_row_scan");
     auto rows_out = [&](auto tag) -> int {
         using S = decltype(tag);
         if (stage) {
-            k_rows_out<S, true><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+            CK(launch_pdl(k_rows_out<S, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
             LAUNCHED(wname<S>("k_rows_out"));
         } else {
             if constexpr (sizeof(S) <= 2) {
                 if (kmask & 1u) {
-                    k_rows_small<S, 1><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    CK(launch_pdl(k_rows_small<S, 1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 2u) {
-                    k_rows_small<S, 2><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    CK(launch_pdl(k_rows_small<S, 2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 4u) {
-                    k_rows_small<S, 4><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    CK(launch_pdl(k_rows_small<S, 4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 8u) {
-                    k_rows_fast<S><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                    CK(launch_pdl(k_rows_fast<S>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
             }
             if (sizeof(S) > 2 || maxK > (uint32_t)OUT_ELEMS) {
-                k_rows_out<S, false><<<dim3(nchunk_cap, B), ROW_THREADS, 0, s>>>(rp);
+                CK(launch_pdl(k_rows_out<S, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                 LAUNCHED("k_rows_out/general");
             }
         }
@@ -1201,6 +1223,7 @@ int scz_decompress(scz_ctx* ctx, const scz_info* info_in, const uint32_t* freqs,
 
 namespace {
 __global__ void k_set_params(TensorState* st, double scale, int64_t z) {
+    pdl_wait();
     st->scale = scale;
     st->zero_point = z;
     st->fast = (scale >= 0x1p-120 && scale <= 0x1p120) ? 1u : 0u;

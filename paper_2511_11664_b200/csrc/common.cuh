@@ -179,4 +179,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
+// Programmatic dependent launch: pipeline kernels are launched with the
+// PDL attribute so their launch overlaps the predecessor's tail; each one
+// waits here, before touching memory, until the predecessor grid has
+// completed and flushed (a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 }  // namespace scz

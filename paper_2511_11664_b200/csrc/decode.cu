@@ -55,6 +55,7 @@ struct RowParams {
 
 template <typename S>
 __global__ void __launch_bounds__(ROW_THREADS) k_row_sums(RowParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_row_sums(RowParams p) {
 }
 
 __global__ void __launch_bounds__(256) k_row_scan(RowParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK) return;
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(256) k_row_scan(RowParams p) {
 
 template <typename S, bool STAGE>
 __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
 // tile is written back with 16-byte stores.  Static shared arrays only.
 template <typename S>
 __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
@@ -310,6 +314,7 @@ template __global__ void k_rows_fast<uint16_t>(RowParams);
 // instruction of a warp is one contiguous, coalesced span.
 template <typename S, int KK>
 __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S) || in.n_cols != (uint32_t)KK) return;
@@ -412,6 +417,7 @@ SCZ_INST_ROWS(uint32_t)
 // zero mask (u8) -> bitmap + per-tile nnz, for csr_encode.
 __global__ void __launch_bounds__(TILE_THREADS) k_mask_bitmap(const uint8_t* mask, uint64_t n,
                                                               uint32_t* bitmap, uint32_t* tile_nnz) {
+    pdl_wait();
     const uint32_t tile = blockIdx.x;
     const uint64_t w = (uint64_t)tile * TILE_WORDS + threadIdx.x;
     uint32_t word = 0;
@@ -432,6 +438,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_mask_bitmap(const uint8_t* mas
 
 // exclusive scan of per-tile counts (single CTA); total -> *nnz
 __global__ void __launch_bounds__(256) k_tile_scan(uint32_t* cnt, uint32_t n, uint64_t* nnz) {
+    pdl_wait();
     __shared__ uint32_t s_scan[33];
     unsigned long long carry = 0;
     for (uint32_t base = 0; base < n; base += 256) {
@@ -448,6 +455,7 @@ __global__ void __launch_bounds__(256) k_tile_scan(uint32_t* cnt, uint32_t n, ui
 // values at original-nonzero positions, rank order (sparse.py:65-67)
 __global__ void __launch_bounds__(TILE_THREADS) k_compact_u32(const uint32_t* q, const uint32_t* bitmap,
                                                               const uint32_t* tile_off, uint32_t* d) {
+    pdl_wait();
     const uint32_t tile = blockIdx.x;
     __shared__ uint32_t s_scan[33];
     const uint64_t w = (uint64_t)tile * TILE_WORDS + threadIdx.x;
@@ -461,12 +469,14 @@ __global__ void __launch_bounds__(TILE_THREADS) k_compact_u32(const uint32_t* q,
 }
 
 __global__ void k_unpack_mask(const uint32_t* bitmap, uint64_t n, uint8_t* mask) {
+    pdl_wait();
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) mask[i] = ((bitmap[i >> 5] >> (i & 31)) & 1u) ? 0 : 1;
 }
 
 __global__ void k_dequant_flat(const uint32_t* q, const uint8_t* mask, uint64_t n, double scale,
                                int64_t z, float* out) {
+    pdl_wait();
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n)
         out[i] = mask[i] ? 0.0f
@@ -476,6 +486,7 @@ __global__ void k_dequant_flat(const uint32_t* q, const uint8_t* mask, uint64_t 
 // bincount with AlphabetOverflow flag (rans.py:76-85)
 __global__ void k_hist_u32(const uint32_t* d, uint64_t n, uint32_t A, uint32_t* counts,
                            int32_t* overflow) {
+    pdl_wait();
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
         uint32_t v = d[i];

@@ -74,6 +74,7 @@ __device__ void device_compute_params(float fmin, float fmax, int q_bits, double
 }
 
 __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
+    pdl_wait();
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float* xb = p.x + (uint64_t)b * p.total;
@@ -254,6 +255,7 @@ __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, i
 
 template <bool SYM_OUT>  // SYM_OUT: also write every element's symbol (stage API)
 __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
+    pdl_wait();
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const TensorState& st = p.state[b];
@@ -334,6 +336,7 @@ struct ColHistParams {
 // H_P[j] = #{p : p mod P == j, x[p] != 0}; thread owns one bitmap word
 // column of the (rows x P) view and counts its 32 bit positions.
 __global__ void __launch_bounds__(128) k_colhist(ColHistParams p) {
+    pdl_wait();
     const uint32_t q = blockIdx.x * 128 + threadIdx.x;
     const uint32_t b = blockIdx.z;
     if (q >= p.period_words) return;
@@ -389,6 +392,7 @@ struct RowHistParams {
 
 // Row-count histograms for every candidate K: r_i = popcount(row i).
 __global__ void __launch_bounds__(256) k_rowhist(RowHistParams p) {
+    pdl_wait();
     const uint32_t chunk = blockIdx.x, b = blockIdx.y;
     uint32_t c = 0;
     while (c + 1 < p.n_cand && p.chunk_start[c + 1] <= chunk) ++c;
@@ -439,6 +443,7 @@ __device__ __forceinline__ void store_sym(void* base, uint64_t i, uint32_t v) {
 
 template <typename S>
 __global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
+    pdl_wait();
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;

@@ -36,6 +36,7 @@ struct FrontParams {
 };
 
 __global__ void __launch_bounds__(TILE_THREADS) k_front(FrontParams p) {
+    pdl_wait();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_words[TILE_WORDS];
     __shared__ uint32_t s_scan[33];

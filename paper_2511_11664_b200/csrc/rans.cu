@@ -68,6 +68,7 @@ constexpr uint32_t ERR_OVERFLOW = 1, ERR_UNCODABLE = 2;
 // the same state, lane j prefetches the table entry of the j-th next symbol.
 template <class Src>
 __global__ void __launch_bounds__(32) k_rans_enc_v1(EncParams p, Src src) {
+    pdl_wait();
     const uint32_t b = blockIdx.x;
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
@@ -217,6 +218,7 @@ __device__ void build_lut_slice(const DecParams& p, const scz_info& in, uint32_t
 }
 
 __global__ void __launch_bounds__(256) k_dec_prepare(DecParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.y;
     const scz_info& in = p.info[b];
     if (blockIdx.x > 0) {
@@ -326,6 +328,7 @@ struct Ring {
 // the table does not fit a LUT.
 template <typename S, typename L>
 __global__ void __launch_bounds__(32) k_rans_dec_v1(DecParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.version != 1 || in.sym_bytes != sizeof(S)) return;

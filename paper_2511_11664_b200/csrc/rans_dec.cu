@@ -26,6 +26,7 @@ constexpr uint32_t DEC_BIG_F = 256;  // symbols with more slots are filled CTA-w
 // one bulk copy (TMA) while the payload ring is being primed.
 template <typename S, typename L, int WPB>
 __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.y;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.version != 2 || in.sym_bytes != sizeof(S)) return;

@@ -118,6 +118,7 @@ __device__ __forceinline__ void enc_apply(EncLane& L, const EncTab& t, bool live
 
 template <class Src, bool SMEM, bool CHECK>
 __global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src src) {
+    pdl_wait();
     const uint32_t b = blockIdx.y;
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;

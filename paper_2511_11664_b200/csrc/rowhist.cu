@@ -112,6 +112,7 @@ __device__ void rowhist_swar(const uint32_t* bm, uint32_t w0, uint32_t w1, uint3
 }
 
 __global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__ RowHist2Params p) {
+    pdl_wait();
     const uint32_t chunk = blockIdx.x, b = blockIdx.y;
     if (chunk >= p.fold_start) {
         fold_columns(p, b, chunk - p.fold_start);

@@ -508,6 +508,7 @@ __device__ bool gather_costs(const SelectParams& p, uint32_t b, BlockScratch& s)
 }
 
 __global__ void __launch_bounds__(SEL_THREADS) k_select(const __grid_constant__ SelectParams p) {
+    pdl_wait();
     const uint32_t b = blockIdx.y, g = blockIdx.x;
     SEL_PROBE(0);
     TensorState& st = p.state[b];
@@ -636,6 +637,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const __grid_constant__ 
 __global__ void __launch_bounds__(SEL_THREADS) k_normalize_only(const uint32_t* counts, uint32_t A,
                                                                int precision, uint32_t* freqs,
                                                                double* rem, int32_t* status) {
+    pdl_wait();
     __shared__ BlockScratch s;
     int st = block_normalize(counts, A, precision, freqs, rem, nullptr, s);
     if (threadIdx.x == 0) *status = st;
