@@ -121,13 +121,12 @@ const char* wname(const char* base) {
         {"k_rans_enc_v1/u8", "k_rans_enc_v1/u16", "k_rans_enc_v1/u32"},
         {"k_rans_dec_v2/u8", "k_rans_dec_v2/u16", "k_rans_dec_v2/u32"},
         {"k_rans_dec_v1/u8", "k_rans_dec_v1/u16", "k_rans_dec_v1/u32"},
-        {"k_row_sums/u8", "k_row_sums/u16", "k_row_sums/u32"},
         {"k_rows_out/u8", "k_rows_out/u16", "k_rows_out/u32"},
     };
     static const char* const bases[] = {"k_materialize", "k_rans_enc_v2", "k_rans_enc_v1", "k_rans_dec_v2",
-                                        "k_rans_dec_v1", "k_row_sums", "k_rows_out"};
+                                        "k_rans_dec_v1", "k_rows_out"};
     const int w = sizeof(S) == 1 ? 0 : (sizeof(S) == 2 ? 1 : 2);
-    for (int i = 0; i < 7; ++i)
+    for (int i = 0; i < 6; ++i)
         if (!strcmp(base, bases[i])) return tab[i][w];
     return base;
 }
@@ -898,7 +897,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     CK(ctx->cumtab.ensure((size_t)B * (acap + 1) * 4));
     CK(ctx->dblk_off.ensure((size_t)B * nblk_cap * 4));
     CK(ctx->dsym.ensure((size_t)B * Lmax * 4));
-    CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 4));
+    CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 8));  // look-back words
     // v2 decode tables: (4 + 2) bytes per slot covers both LUT classes
     int lut_n = 0;  // largest precision among v2 tensors of the LUT classes
     for (uint32_t b = 0; b < B; ++b)
@@ -922,10 +921,11 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     CK(cudaMemcpyAsync(ctx->dstatus.p, hst, (size_t)B * 4, cudaMemcpyHostToDevice, s));
     DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
                  ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
-                 ctx->dstatus.as<int32_t>(), ctx->dlut.as<uint8_t>(), lut_stride};
+                 ctx->dstatus.as<int32_t>(), ctx->dlut.as<uint8_t>(), lut_stride,
+                 ctx->chunk_sum.as<unsigned long long>(), nchunk_cap};
     CK(launch_pdl(k_dec_prepare, dim3(1 + lut_slices, B), 256, 0, s, dp));
     LAUNCHED("k_dec_prepare");
-    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<uint32_t>(), nchunk_cap,
+    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<unsigned long long>(), nchunk_cap,
                  ctx->dstatus.as<int32_t>(), d_out, ctx->out_off.as<uint64_t>(), q_out, mask_out};
     auto run_width = [&](auto tag) -> int {
         using S = decltype(tag);
@@ -949,8 +949,6 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
             CK(launch_pdl(k_rans_dec_v1<S, L>, B, 32, smem, s, dp));
             LAUNCHED(wname<S>("k_rans_dec_v1"));
         }
-        CK(launch_pdl(k_row_sums<S>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
-        LAUNCHED(wname<S>("k_row_sums"));
         return SCZ_OK;
     };
     // the width filter: kernels of width S skip tensors of another class
@@ -959,8 +957,6 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     if (widths & 1) { if ((st = run_width(uint8_t{})) != SCZ_OK) return st; }
     if (widths & 2) { if ((st = run_width(uint16_t{})) != SCZ_OK) return st; }
     if (widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
-    CK(launch_pdl(k_row_scan, B, 256, 0, s, rp));
-    LAUNCHED("k_row_scan");
     auto rows_out = [&](auto tag) -> int {
         using S = decltype(tag);
         if (stage) {
@@ -1364,7 +1360,8 @@ int scz_csr_decode(scz_ctx* ctx, const uint32_t* d, uint64_t nnz, uint64_t n_row
     CK(ctx->dinfo.ensure(sizeof(scz_info)));
     CK(ctx->dstatus.ensure(4));
     uint32_t nch = std::max(1u, ceil_div_u32(n_rows, rows_per_chunk((uint32_t)n_cols)));
-    CK(ctx->chunk_sum.ensure((size_t)nch * 4));
+    CK(ctx->chunk_sum.ensure((size_t)nch * 8));
+    CK(cudaMemsetAsync(ctx->chunk_sum.p, 0, (size_t)nch * 8, s));  // look-back words
     CK(cudaMemcpyAsync(ctx->dsym.p, d, L * 4, cudaMemcpyHostToDevice, s));
     scz_info in;
     memset(&in, 0, sizeof in);
@@ -1378,12 +1375,8 @@ int scz_csr_decode(scz_ctx* ctx, const uint32_t* d, uint64_t nnz, uint64_t n_row
     CK(cudaMemsetAsync(ctx->dstatus.p, 0, 4, s));
     uint32_t* qd = ctx->dsym_in.as<uint32_t>();
     uint8_t* md = reinterpret_cast<uint8_t*>(qd + n);
-    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, L, ctx->chunk_sum.as<uint32_t>(), nch,
+    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, L, ctx->chunk_sum.as<unsigned long long>(), nch,
                  ctx->dstatus.as<int32_t>(), nullptr, nullptr, qd, md};
-    k_row_sums<uint32_t><<<dim3(nch, 1), ROW_THREADS, 0, s>>>(rp);
-    LAUNCHED("k_row_sums");
-    k_row_scan<<<1, 256, 0, s>>>(rp);
-    LAUNCHED("k_row_scan");
     k_rows_out<uint32_t, true><<<dim3(nch, 1), ROW_THREADS, 0, s>>>(rp);
     LAUNCHED("k_rows_out");
     int32_t dst = 0;

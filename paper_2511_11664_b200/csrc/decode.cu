@@ -4,8 +4,10 @@
 // Rows are processed in chunks of R(K) = min(1024, 4096 / K) rows so a chunk's
 // dense output (R*K fp32) fits 16 KB of shared memory; its column and value
 // segments are staged there too with coalesced loads before the scatter.
-//   k_row_sums   per chunk: sum of row counts, r <= K check (sparse.py:88-89)
-//   k_row_scan   per tensor: chunk offsets, sum(r) == nnz check (sparse.py:84-87)
+// One pass: each chunk sums its row counts (r <= K check, sparse.py:88-89),
+// publishes the sum and finds its nonzero offset by decoupled look-back over
+// the previous chunks of the tensor (the last chunk checks sum(r) == nnz,
+// sparse.py:84-87); then
 //   k_rows_out   per chunk: row offsets (block scan), column checks (col < K,
 //                strictly increasing: sparse.py:90-97); the dense rows are
 //                assembled in shared memory -- +0.0 everywhere, LUT[v] at the
@@ -44,7 +46,7 @@ struct RowParams {
     const scz_info* info;   // [B]
     const void* dsym;       // [B][dsym_stride] decoded D
     uint64_t dsym_stride;
-    uint32_t* chunk_sum;    // [B][nchunk_cap]
+    unsigned long long* chunk_state;  // [B][nchunk_cap] look-back words, zeroed per launch
     uint32_t nchunk_cap;
     int32_t* status;        // [B]
     float* out;             // [B] tensors at out_off[b]
@@ -53,60 +55,62 @@ struct RowParams {
     uint8_t* mask_out;      // stage API: zero mask
 };
 
-template <typename S>
-__global__ void __launch_bounds__(ROW_THREADS) k_row_sums(RowParams p) {
-    pdl_wait();
-    const uint32_t b = blockIdx.y, chunk = blockIdx.x;
-    const scz_info& in = p.info[b];
-    if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
-    const uint32_t R = rows_per_chunk(in.n_cols);
-    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
-    if (r0 >= N) return;
-    const S* r = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride + 2 * in.nnz;
-    uint32_t sum = 0, bad = 0;
-    const uint64_t r1 = min(N, r0 + R);
-    for (uint64_t i = r0 + threadIdx.x; i < r1; i += ROW_THREADS) {
-        uint32_t v = r[i];
-        bad |= v > in.n_cols;
-        sum += v;
+// Decoupled look-back (single-pass scan) over the chunks of one tensor.
+// Word = flag << 32 | value; flag 1: the chunk's own row-count sum, flag 2:
+// inclusive prefix.  Chunks of a tensor are consecutive blockIdx.x of one
+// grid and start in order, so every predecessor makes progress.  Called by
+// one full warp; it inspects 32 predecessors per round.
+__device__ uint32_t chunk_prefix(unsigned long long* st, uint32_t chunk, uint32_t local) {
+    const uint32_t lane = threadIdx.x & 31;
+    const volatile unsigned long long* vs = st;
+    if (chunk == 0) {
+        if (lane == 0) atomicExch(st, (2ull << 32) | local);
+        return 0;
     }
-    sum = warp_sum(sum);
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    __shared__ uint32_t s_sum[ROW_THREADS / 32], s_bad[ROW_THREADS / 32];
-    if ((threadIdx.x & 31) == 0) {
-        s_sum[threadIdx.x >> 5] = sum;
-        s_bad[threadIdx.x >> 5] = bad;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < ROW_THREADS / 32; ++w) {
-            sum += s_sum[w];
-            bad |= s_bad[w];
+    if (lane == 0) atomicExch(st + chunk, (1ull << 32) | local);
+    uint32_t excl = 0;
+    for (int j = (int)chunk - 1;; j -= 32) {
+        const int idx = j - (int)lane;  // lane 0: nearest predecessor
+        unsigned long long w = idx >= 0 ? vs[idx] : (2ull << 32);
+        while (__any_sync(0xffffffffu, (w >> 32) == 0))
+            if ((w >> 32) == 0) w = vs[idx];
+        const uint32_t inc = __ballot_sync(0xffffffffu, (w >> 32) == 2);
+        if (inc) {
+            const uint32_t first = __ffs(inc) - 1;
+            excl += warp_sum(lane <= first ? (uint32_t)w : 0u);
+            break;
         }
-        p.chunk_sum[(uint64_t)b * p.nchunk_cap + chunk] = sum;
-        if (bad) p.status[b] = SCZ_CORRUPT_STREAM;  // sparse.py:88-89
+        excl += warp_sum((uint32_t)w);
     }
+    if (lane == 0) atomicExch(st + chunk, (2ull << 32) | (excl + local));
+    return excl;
 }
 
-__global__ void __launch_bounds__(256) k_row_scan(RowParams p) {
-    pdl_wait();
-    const uint32_t b = blockIdx.x;
-    const scz_info& in = p.info[b];
-    if (p.status[b] != SCZ_OK) return;
-    __shared__ uint32_t s_scan[33];
-    const uint32_t R = rows_per_chunk(in.n_cols);
-    const uint32_t nch = (uint32_t)((in.n_rows + R - 1) / R);
-    uint32_t* cs = p.chunk_sum + (uint64_t)b * p.nchunk_cap;
-    unsigned long long carry = 0;
-    for (uint32_t base = 0; base < nch; base += 256) {
-        uint32_t i = base + threadIdx.x;
-        uint32_t v = i < nch ? cs[i] : 0;
-        uint32_t tot;
-        uint32_t ex = block_exclusive_scan<256>(v, s_scan, &tot);
-        if (i < nch) cs[i] = (uint32_t)(carry + ex);
-        carry += tot;
+// A chunk of a tensor already marked bad (possibly by another chunk of this
+// very launch) still publishes, so later chunks never wait on it forever.
+__device__ bool chunk_dead(const RowParams& p, uint32_t b, uint32_t chunk) {
+    __shared__ int s_dead;  // one read for the CTA: status may change under us
+    if (threadIdx.x == 0) s_dead = *(const volatile int32_t*)(p.status + b) != SCZ_OK;
+    __syncthreads();
+    if (s_dead && threadIdx.x < 32) chunk_prefix(p.chunk_state + (uint64_t)b * p.nchunk_cap, chunk, 0);
+    return s_dead != 0;
+}
+
+// Chunk offset of the block (all threads): publishes `tot`, returns the
+// exclusive prefix; flags s_bad when the chunk's nonzeros overrun nnz or the
+// last chunk's inclusive sum differs from nnz (sparse.py:84-87).
+__device__ uint32_t block_chunk_base(const RowParams& p, uint32_t b, uint32_t chunk, uint32_t tot, uint64_t nnz,
+                                     bool last, int* s_bad) {
+    __shared__ uint32_t s_base;
+    if (threadIdx.x < 32) {
+        const uint32_t e = chunk_prefix(p.chunk_state + (uint64_t)b * p.nchunk_cap, chunk, tot);
+        if (threadIdx.x == 0) {
+            s_base = e;
+            if ((uint64_t)e + tot > nnz || (last && (uint64_t)e + tot != nnz)) *s_bad = 1;
+        }
     }
-    if (threadIdx.x == 0 && carry != in.nnz) p.status[b] = SCZ_CORRUPT_STREAM;  // sparse.py:84-87
+    __syncthreads();
+    return s_base;
 }
 
 template <typename S, bool STAGE>
@@ -114,12 +118,13 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
-    if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
+    if (in.sym_bytes != sizeof(S)) return;
     const uint32_t K = in.n_cols;
     if (!STAGE && sizeof(S) <= 2 && K <= (uint32_t)OUT_ELEMS) return;  // k_rows_fast's case
     const uint32_t R = rows_per_chunk(K);
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
+    if (chunk_dead(p, b, chunk)) return;
     const uint64_t nnz = in.nnz;
     const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
     const S* vals = d;
@@ -139,15 +144,23 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
     // per-chunk row offsets: each thread scans ROW_CHUNK / 256 consecutive rows
     constexpr int PER = ROW_CHUNK / ROW_THREADS;
     uint32_t loc[PER], sum = 0;
+    bool rbad = false;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const uint32_t i = threadIdx.x * PER + j;
-        loc[j] = i < nrow ? (uint32_t)rc[r0 + i] : 0;
+        const uint32_t v = i < nrow ? (uint32_t)rc[r0 + i] : 0;
+        rbad |= v > K;  // sparse.py:88-89
+        loc[j] = min(v, K + 1);
         sum += loc[j];
     }
     uint32_t tot;
     uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
-    const uint32_t cbase = p.chunk_sum[(uint64_t)b * p.nchunk_cap + chunk];
+    if (rbad) s_bad = 1;
+    const uint32_t cbase = block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
+    if (s_bad) {
+        if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         s_off[threadIdx.x * PER + j] = cbase + ex;
@@ -228,13 +241,14 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
-    if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S)) return;
+    if (in.sym_bytes != sizeof(S)) return;
     const uint32_t K = in.n_cols;
     if (K > (uint32_t)OUT_ELEMS) return;       // k_rows_out handles these
     if (K == 1 || K == 2 || K == 4) return;    // k_rows_small handles these
     const uint32_t R = rows_per_chunk(K);
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
+    if (chunk_dead(p, b, chunk)) return;
     const uint64_t nnz = in.nnz;
     const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
     __shared__ uint32_t s_off[ROW_CHUNK];
@@ -249,15 +263,23 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
     constexpr int PER = ROW_CHUNK / ROW_THREADS;
     uint32_t loc[PER], sum = 0;
     const S* rc = d + 2 * nnz + r0;
+    bool rbad = false;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const uint32_t i = threadIdx.x * PER + j;
-        loc[j] = i < nrow ? (uint32_t)rc[i] : 0u;
+        const uint32_t v = i < nrow ? (uint32_t)rc[i] : 0u;
+        rbad |= v > K;  // sparse.py:88-89
+        loc[j] = min(v, K + 1);
         sum += loc[j];
     }
     uint32_t tot;
     uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
-    const uint32_t cbase = p.chunk_sum[(uint64_t)b * p.nchunk_cap + chunk];
+    if (rbad) s_bad = 1;
+    const uint32_t cbase = block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
+    if (s_bad) {  // tot <= nrow * K holds from here on
+        if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         s_off[threadIdx.x * PER + j] = ex;  // chunk-local offset
@@ -268,7 +290,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
         reinterpret_cast<float4*>(s_out)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     const S* gc = d + nnz + cbase;
     const S* gv = d + cbase;
-    for (uint32_t i = threadIdx.x; i < tot; i += ROW_THREADS) {  // tot <= nrow * K (row_sums checked r <= K)
+    for (uint32_t i = threadIdx.x; i < tot; i += ROW_THREADS) {  // tot <= nrow * K (checked above)
         s_c[i] = gc[i];
         s_v[i] = gv[i];
     }
@@ -317,10 +339,11 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
-    if (p.status[b] != SCZ_OK || in.sym_bytes != sizeof(S) || in.n_cols != (uint32_t)KK) return;
+    if (in.sym_bytes != sizeof(S) || in.n_cols != (uint32_t)KK) return;
     constexpr uint32_t R = (uint32_t)ROW_CHUNK;  // == rows_per_chunk(KK) for KK <= 4
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
+    if (chunk_dead(p, b, chunk)) return;
     const uint64_t nnz = in.nnz;
     const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
     __shared__ uint32_t s_off[ROW_CHUNK];
@@ -334,15 +357,23 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
     constexpr int PER = ROW_CHUNK / ROW_THREADS;
     uint32_t loc[PER], sum = 0;
     const S* rc = d + 2 * nnz + r0;
+    bool rbad = false;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const uint32_t i = threadIdx.x * PER + j;
-        loc[j] = i < nrow ? (uint32_t)rc[i] : 0u;
+        const uint32_t v = i < nrow ? (uint32_t)rc[i] : 0u;
+        rbad |= v > (uint32_t)KK;  // sparse.py:88-89
+        loc[j] = min(v, (uint32_t)KK + 1);
         sum += loc[j];
     }
     uint32_t tot;
-    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot) +
-                  p.chunk_sum[(uint64_t)b * p.nchunk_cap + chunk];
+    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
+    if (rbad) s_bad = 1;
+    ex += block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
+    if (s_bad) {
+        if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         s_off[threadIdx.x * PER + j] = ex;
@@ -406,7 +437,6 @@ SCZ_INST_SMALL(uint8_t)
 SCZ_INST_SMALL(uint16_t)
 
 #define SCZ_INST_ROWS(S)                                        \
-    template __global__ void k_row_sums<S>(RowParams);          \
     template __global__ void k_rows_out<S, false>(RowParams);   \
     template __global__ void k_rows_out<S, true>(RowParams);
 SCZ_INST_ROWS(uint8_t)

@@ -158,6 +158,8 @@ struct DecParams {
     //   [2^n] u32 (f << 16) | (slot - cum)   then   [2^n] symbol (u8 / u16)
     uint8_t* lut;
     uint64_t lut_stride;         // bytes per tensor
+    unsigned long long* chunk_state;  // [B][nchunk_cap] CSR look-back words, zeroed here
+    uint32_t nchunk_cap;
 };
 
 constexpr uint32_t LUT_SLICE = 2048;  // slots per k_dec_prepare slice CTA
@@ -230,6 +232,9 @@ __global__ void __launch_bounds__(256) k_dec_prepare(DecParams p) {
     __shared__ uint32_t s_scan[33];
     __shared__ int s_bad;
     if (threadIdx.x == 0) s_bad = 0;
+    if (p.chunk_state)
+        for (uint32_t i = threadIdx.x; i < p.nchunk_cap; i += blockDim.x)
+            p.chunk_state[(uint64_t)b * p.nchunk_cap + i] = 0ull;
     __syncthreads();
     if (p.status[b] != SCZ_OK) return;
     const uint32_t A = in.alphabet;
