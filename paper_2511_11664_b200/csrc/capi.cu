@@ -144,6 +144,23 @@ int width_for(uint64_t maxsym) { return maxsym <= 255 ? 1 : (maxsym <= 65535 ? 2
 
 }  // namespace
 
+struct EncPlan {
+    uint64_t T;
+    uint32_t B;
+    int q_bits, precision, format;
+    uint32_t lanes, block_syms;
+    bool searching;
+    std::vector<uint64_t> rows;  // candidate N, descending
+    uint32_t n_tiles, words_pad;
+    uint32_t acap;
+    uint64_t L_max;
+    uint32_t nblk_cap;
+    uint64_t slot_cap;
+    uint64_t period;  // P
+    uint32_t widths;  // bitmask of c/r symbol widths present among candidates
+    uint64_t payload_cap;  // packed payload bytes per tensor (upper bound)
+};
+
 struct scz_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -189,6 +206,8 @@ struct scz_ctx {
         uint64_t nkern = 0;
     };
     std::vector<Graph> graphs;
+    std::vector<std::pair<std::string, EncPlan>> plans;  // plan_encode_cached
+    cudaEvent_t sync_ev = nullptr;                               // scz_batch_sync
     bool use_graphs = getenv("SCZ_NO_GRAPHS") == nullptr;
     uint32_t front_grid = 0;  // co-resident CTAs of k_front (0 = not queried)
     bool use_front = getenv("SCZ_FUSED_FRONT") != nullptr;  // experimental (slower today)
@@ -305,22 +324,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-struct EncPlan {
-    uint64_t T;
-    uint32_t B;
-    int q_bits, precision, format;
-    uint32_t lanes, block_syms;
-    bool searching;
-    std::vector<uint64_t> rows;  // candidate N, descending
-    uint32_t n_tiles, words_pad;
-    uint32_t acap;
-    uint64_t L_max;
-    uint32_t nblk_cap;
-    uint64_t slot_cap;
-    uint64_t period;  // P
-    uint32_t widths;  // bitmask of c/r symbol widths present among candidates
-    uint64_t payload_cap;  // packed payload bytes per tensor (upper bound)
-};
+
 
 int plan_encode(scz_ctx* ctx, uint64_t T, uint32_t B, int q_bits, int64_t n_rows, int precision,
                 int format, uint32_t lanes, uint32_t block_syms, EncPlan* pl,
@@ -555,14 +559,30 @@ int graph_run(scz_ctx* ctx, const std::string& key, F&& body) {
     return SCZ_OK;
 }
 
+// Cache keys: the kind tag and the raw 8-byte values (no formatting).
 std::string key_of(const char* kind, std::initializer_list<uint64_t> vals) {
     std::string k(kind);
-    char buf[24];
-    for (uint64_t v : vals) {
-        snprintf(buf, sizeof buf, "|%llx", (unsigned long long)v);
-        k += buf;
-    }
+    k.reserve(k.size() + 8 * vals.size());
+    for (uint64_t v : vals) k.append(reinterpret_cast<const char*>(&v), 8);
     return k;
+}
+
+// plan_encode memoised per argument tuple (divisor enumeration and the
+// candidate scan are host work on the latency path of repeated calls).
+int plan_encode_cached(scz_ctx* ctx, uint64_t T, uint32_t B, int q_bits, int64_t n_rows, int precision,
+                       int format, uint32_t lanes, uint32_t block_syms, EncPlan* pl) {
+    const std::string key = key_of("plan", {T, B, (uint64_t)q_bits, (uint64_t)n_rows, (uint64_t)precision,
+                                            (uint64_t)format, lanes, block_syms});
+    for (auto& e : ctx->plans)
+        if (e.first == key) {
+            *pl = e.second;
+            return SCZ_OK;
+        }
+    int st = plan_encode(ctx, T, B, q_bits, n_rows, precision, format, lanes, block_syms, pl);
+    if (st != SCZ_OK) return st;
+    if (ctx->plans.size() >= 16) ctx->plans.erase(ctx->plans.begin());
+    ctx->plans.emplace_back(key, *pl);
+    return SCZ_OK;
 }
 
 // The encode pipeline over a device batch.  cand_out (device) optional.
@@ -1052,6 +1072,7 @@ void scz_ctx_destroy(scz_ctx* ctx) {
         cudaStreamDestroy(ctx->xfer_out);
     }
     for (cudaEvent_t e : ctx->xev) cudaEventDestroy(e);
+    if (ctx->sync_ev) cudaEventDestroy(ctx->sync_ev);
     for (auto& g : ctx->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaStreamDestroy(ctx->stream);
@@ -1069,7 +1090,7 @@ int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t ba
     cudaSetDevice(ctx->device);
     ctx->mark();
     EncPlan pl;
-    int st = plan_encode(ctx, total, batch, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
+    int st = plan_encode_cached(ctx, total, batch, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
     if (st) return st;
     const std::string key = key_of("enc", {(uint64_t)(uintptr_t)d_x, total, batch, (uint64_t)q_bits,
                                            (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format,
@@ -1092,7 +1113,14 @@ int scz_batch_sync(scz_ctx* ctx, scz_batch* b, scz_info* h_info) {
     cudaSetDevice(ctx->device);
     CK(cudaMemcpyAsync(h_info, b->d_info, (size_t)b->batch * sizeof(scz_info), cudaMemcpyDeviceToHost,
                        ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    // spin on an event rather than a blocking stream sync: the header read
+    // sits on the single-tensor latency path
+    if (!ctx->sync_ev) CK(cudaEventCreateWithFlags(&ctx->sync_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->sync_ev, ctx->stream));
+    cudaError_t qe;
+    while ((qe = cudaEventQuery(ctx->sync_ev)) == cudaErrorNotReady) {
+    }
+    CK(qe);
     uint64_t tot = 0;
     for (uint32_t i = 0; i < b->batch; ++i)
         if (h_info[i].status == SCZ_OK) tot = std::max(tot, h_info[i].payload_off + h_info[i].payload_len);
@@ -1135,7 +1163,7 @@ int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64
     cudaSetDevice(ctx->device);
     ctx->mark();
     EncPlan pl;
-    int st = plan_encode(ctx, total, 1, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
+    int st = plan_encode_cached(ctx, total, 1, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
     if (st) return st;
     CK(ctx->x_in.ensure(total * 4));
     CK(cudaMemcpyAsync(ctx->x_in.p, x, total * 4, cudaMemcpyHostToDevice, ctx->stream));
