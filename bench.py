@@ -56,7 +56,7 @@ WORKLOADS = {
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
@@ -168,60 +168,72 @@ def run_reference(args):
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled through NVML while the
+    timed region runs: a background thread polls every ~2 ms (the timed region
+    is tens of ms, too short for `nvidia-smi -lms`), and `sample()` takes one
+    extra reading from the launching thread while queued work is executing."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, device_index):
-        self.dev = device_index
-        self.proc = None
-        self.lines = []
+    def __init__(self, torch_device):
+        self.nv = None
+        self.samples = []
+        self.stop = threading.Event()
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda._get_nvml_device_index(torch_device))
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # no NVML: the line says samples=0
+            self.nv = None
+
+    def sample(self):
+        if self.nv is None:
+            return
+        nv = self.nv
+        try:
+            mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+        except Exception:
+            return
+        self.samples.append((mhz, bits, util))
+
+    def _poll(self):
+        while not self.stop.is_set():
+            self.sample()
+            time.sleep(0.002)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+        if self.nv is not None:
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.nv is not None:
+            self.thread.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
+        if not self.samples:
             return dict(sm_mhz=None, sm_max_mhz=None, reasons=[], samples=0)
-        return dict(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons),
-                    samples=len(sm))
+        reasons = set()
+        for _, bits, _ in self.samples:
+            for name, attr in self.REASONS:
+                if bits & getattr(self.nv, attr, 0):
+                    reasons.add(name)
+        loaded = [m for m, _, u in self.samples if u > 0] or [m for m, _, _ in self.samples]
+        return dict(sm_mhz=statistics.median(loaded), sm_max_mhz=self.max_mhz, reasons=sorted(reasons),
+                    samples=len(self.samples), samples_under_load=sum(1 for s in self.samples if s[2] > 0),
+                    source="NVML, polled every ~2 ms during the timed region")
 
 
 # -------------------------------------------------------------- our arm
@@ -309,11 +321,13 @@ def run_ours(args):
     ctx.read_timing()
     l0 = ctx.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    clocks = ClockSampler(local)
+    with clocks:
         barrier()
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             device_step()
+            clocks.sample()  # work of this step is still queued / running
         ev1.record(stream)
         barrier()
     launches = ctx.launches - l0
