@@ -195,7 +195,7 @@ struct scz_ctx {
         }
         return SCZ_OK;
     }
-    DevBuf ready, candcnt, selbuf, dlut, probe;
+    DevBuf ready, candcnt, selbuf, dlut, probe, lbwords;
     // CUDA-graph cache: a launch sequence seen twice with the same key and
     // allocation generation is captured once and replayed afterwards.
     struct Graph {
@@ -792,6 +792,14 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         }
     }
 
+    // v2: blocks are packed into the payload inside the encoder (PackParams)
+    PackParams pk{};
+    if (pl.format == 2) {
+        CK(ctx->lbwords.ensure((size_t)B * pl.nblk_cap * 8));
+        CK(cudaMemsetAsync(ctx->lbwords.p, 0, (size_t)B * pl.nblk_cap * 8, s));
+        pk = PackParams{ctx->payload.as<uint8_t>(), pl.payload_cap, ctx->lbwords.as<unsigned long long>(),
+                        ctx->info.as<scz_info>(), T, pl.q_bits, 1};
+    }
     MatParams mp{T, pl.n_tiles, pl.words_pad, ctx->bitmap.as<uint32_t>(), ctx->tile_off.as<uint32_t>(),
                  ctx->state.as<TensorState>(), ctx->cr.p, 2 * T, 1, 0};
     EncParams ep{ctx->state.as<TensorState>(), ctx->enctab.as<EncTab>(), pl.acap, pl.precision,
@@ -816,10 +824,12 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
                 if (enc_smem_tab) {
                     CK(cudaFuncSetAttribute(k_rans_enc_v2<Src, true, false>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)enc_smem));
-                    CK(launch_pdl(k_rans_enc_v2<Src, true, false>, g_enc2, ENC2_WPB * 32, enc_smem, s, ep, src));
+                    CK(launch_pdl(k_rans_enc_v2<Src, true, false>, g_enc2, ENC2_WPB * 32, enc_smem, s, ep, src,
+                                  pk));
                 } else {
-                    CK(launch_pdl(k_rans_enc_v2<Src, false, false>, g_enc2, ENC2_WPB * 32, 0, s, ep, src));
+                    CK(launch_pdl(k_rans_enc_v2<Src, false, false>, g_enc2, ENC2_WPB * 32, 0, s, ep, src, pk));
                 }
+                pk.write_failed = 0;  // the first launch wrote the failed tensors' headers
                 LAUNCHED(wname<S>("k_rans_enc_v2"));
             } else {
                 CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
@@ -831,10 +841,33 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         else return launch(SplitSrc<S>{ctx->v8.as<uint8_t>(), dstride, ctx->cr.as<S>(), 2 * T});
     };
     int st;
-    if (pl.widths & 1) { if ((st = run_width(uint8_t{})) != SCZ_OK) return st; }
-    if (pl.widths & 2) { if ((st = run_width(uint16_t{})) != SCZ_OK) return st; }
-    if (pl.widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
+    if (pl.format == 2 && (pl.widths & 3)) {
+        // u8 and u16 classes share one materialise and one encoder launch
+        MatParams m8 = mp;
+        m8.cr = ctx->v8.p;  // u8: c ++ r land right after v in the same buffer
+        m8.cr_stride = dstride;
+        m8.after_v = 1;
+        CK(launch_pdl(k_materialize_u8u16, dim3(pl.n_tiles, B), TILE_THREADS, 0, s, m8, mp));
+        LAUNCHED("k_materialize");
+        const Contig8Src s8{ctx->v8.as<uint8_t>(), dstride};
+        const SplitSrc<uint16_t> s16{ctx->v8.as<uint8_t>(), dstride, ctx->cr.as<uint16_t>(), 2 * T};
+        if (enc_smem_tab) {
+            CK(cudaFuncSetAttribute(k_rans_enc_v2_u8u16<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)enc_smem));
+            CK(launch_pdl(k_rans_enc_v2_u8u16<true>, g_enc2, ENC2_WPB * 32, enc_smem, s, ep, s8, s16, pk));
+        } else {
+            CK(launch_pdl(k_rans_enc_v2_u8u16<false>, g_enc2, ENC2_WPB * 32, 0, s, ep, s8, s16, pk));
+        }
+        LAUNCHED("k_rans_enc_v2/u8u16");
+        pk.write_failed = 0;
+        if (pl.widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
+    } else {
+        if (pl.widths & 1) { if ((st = run_width(uint8_t{})) != SCZ_OK) return st; }
+        if (pl.widths & 2) { if ((st = run_width(uint16_t{})) != SCZ_OK) return st; }
+        if (pl.widths & 4) { if ((st = run_width(uint32_t{})) != SCZ_OK) return st; }
+    }
 
+    if (pl.format == 2) return SCZ_OK;  // headers and payload written by the encoder
     CK(launch_pdl(k_finalize, B, 256, 0, s, ctx->state.as<TensorState>(), B, T, pl.q_bits, pl.precision, pl.format,
                                  pl.block_syms, ctx->block_len.as<uint32_t>(), pl.nblk_cap,
                                  ctx->blk_off.as<uint32_t>(), pl.acap, ctx->info.as<scz_info>(),
@@ -901,7 +934,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         maxA = std::max<uint64_t>(maxA, hi[b].alphabet);
         nblk_cap = std::max(nblk_cap, hi[b].version == 2 ? hi[b].n_blocks : 1u);
         Lmax = std::max<uint64_t>(Lmax, 2 * hi[b].nnz + hi[b].n_rows);
-        nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, rows_per_chunk(hi[b].n_cols)));
+        nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, dec_chunk_rows(hi[b].n_cols, hi[b].sym_bytes, stage)));
         maxK = std::max(maxK, hi[b].n_cols);
         {   // which CSR-decode variants this batch needs (K 1 / 2 / 4 / other)
             const uint32_t K = hi[b].n_cols;
@@ -985,15 +1018,24 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         } else {
             if constexpr (sizeof(S) <= 2) {
                 if (kmask & 1u) {
-                    CK(launch_pdl(k_rows_small<S, 1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    if constexpr (sizeof(S) == 1)
+                        CK(launch_pdl(k_rows_small8<1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    else
+                        CK(launch_pdl(k_rows_small<S, 1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 2u) {
-                    CK(launch_pdl(k_rows_small<S, 2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    if constexpr (sizeof(S) == 1)
+                        CK(launch_pdl(k_rows_small8<2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    else
+                        CK(launch_pdl(k_rows_small<S, 2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 4u) {
-                    CK(launch_pdl(k_rows_small<S, 4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    if constexpr (sizeof(S) == 1)
+                        CK(launch_pdl(k_rows_small8<4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    else
+                        CK(launch_pdl(k_rows_small<S, 4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 8u) {
@@ -1060,7 +1102,7 @@ void scz_ctx_destroy(scz_ctx* ctx) {
                       &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
                       &ctx->info, &ctx->payload, &ctx->ticket, &ctx->selbuf, &ctx->dlut, &ctx->probe, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
                       &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
-                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready, &ctx->candcnt})
+                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready, &ctx->candcnt, &ctx->lbwords})
         b->release();
     for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
                        &ctx->h_misc, &ctx->hb_info, &ctx->hb_payload, &ctx->hb_freqs, &ctx->hb_blocks})
@@ -1510,9 +1552,9 @@ int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t*
         const size_t sm = (size_t)alphabet * sizeof(EncTab);
         CK(cudaFuncSetAttribute(k_rans_enc_v2<PlainSrc, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sm));
-        k_rans_enc_v2<PlainSrc, true, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, sm, s>>>(ep, src);
+        k_rans_enc_v2<PlainSrc, true, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, sm, s>>>(ep, src, PackParams{});
     } else if (v2) {
-        k_rans_enc_v2<PlainSrc, false, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, 0, s>>>(ep, src);
+        k_rans_enc_v2<PlainSrc, false, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, 0, s>>>(ep, src, PackParams{});
     }
     if (!v2) k_rans_enc_v1<PlainSrc><<<1, 32, 0, s>>>(ep, src);
     LAUNCHED("k_rans_enc");
@@ -1752,13 +1794,31 @@ int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t 
         if ((st = graph_run(ctx, key, [&] { return run_encode(ctx, dx, cp, nullptr); })) != SCZ_OK) return st;
         CK(cudaMemcpyAsync(hi + b0, ctx->info.p, (size_t)nb * sizeof(scz_info), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        uint64_t cpt = 0;
-        for (uint32_t i = 0; i < nb; ++i)
-            if (hi[b0 + i].status == SCZ_OK) cpt = std::max(cpt, hi[b0 + i].payload_off + hi[b0 + i].payload_len);
+        uint64_t cpt = 0, pitch = 0;
+        if (format == 2) {
+            // v2 payloads sit at fixed per-tensor strides on the device
+            // (b * payload_cap): one pitched copy of max-length rows
+            uint64_t maxlen = 0;
+            for (uint32_t i = 0; i < nb; ++i)
+                if (hi[b0 + i].status == SCZ_OK) maxlen = std::max(maxlen, hi[b0 + i].payload_len);
+            pitch = (maxlen + 15) & ~15ull;
+            cpt = pitch * nb;
+        } else {
+            for (uint32_t i = 0; i < nb; ++i)
+                if (hi[b0 + i].status == SCZ_OK) cpt = std::max(cpt, hi[b0 + i].payload_off + hi[b0 + i].payload_len);
+        }
         CK(ctx->hb_payload.grow_keep(ptot + cpt + 16, ptot));
         // chunk outputs land at their batch-global places; the next chunk's
         // kernels queue behind these copies on the same stream
-        CK(cudaMemcpyAsync(ctx->hb_payload.as<uint8_t>() + ptot, ctx->payload.p, cpt, cudaMemcpyDeviceToHost, s));
+        if (format == 2) {
+            if (pitch)
+                CK(cudaMemcpy2DAsync(ctx->hb_payload.as<uint8_t>() + ptot, pitch, ctx->payload.p, cp.payload_cap,
+                                     pitch, nb, cudaMemcpyDeviceToHost, s));
+            for (uint32_t i = 0; i < nb; ++i) hi[b0 + i].payload_off = (uint64_t)i * pitch;
+        } else {
+            CK(cudaMemcpyAsync(ctx->hb_payload.as<uint8_t>() + ptot, ctx->payload.p, cpt, cudaMemcpyDeviceToHost,
+                               s));
+        }
         CK(cudaMemcpyAsync(ctx->hb_freqs.as<uint32_t>() + (size_t)b0 * pl.acap, ctx->freqs.p,
                            (size_t)nb * pl.acap * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->hb_blocks.as<uint32_t>() + (size_t)b0 * pl.nblk_cap, ctx->block_len.p,

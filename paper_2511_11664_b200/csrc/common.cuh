@@ -131,6 +131,39 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// Decoupled look-back (single-pass scan) over the chunks of one tensor
+// (CSR decode: row-count sums; v2 encoder: block byte lengths).  Word =
+// flag << 32 | value; flag 1: the chunk's own value, flag 2: inclusive
+// prefix.  Chunks of a tensor are consecutive blockIdx.x of one grid (or
+// consecutive warps of one CTA) and start in order, so every predecessor
+// makes progress.  Called by one full warp; it inspects 32 predecessors per
+// round.  The words are zeroed before the launch.
+__device__ uint32_t chunk_prefix(unsigned long long* st, uint32_t chunk, uint32_t local) {
+    const uint32_t lane = threadIdx.x & 31;
+    const volatile unsigned long long* vs = st;
+    if (chunk == 0) {
+        if (lane == 0) atomicExch(st, (2ull << 32) | local);
+        return 0;
+    }
+    if (lane == 0) atomicExch(st + chunk, (1ull << 32) | local);
+    uint32_t excl = 0;
+    for (int j = (int)chunk - 1;; j -= 32) {
+        const int idx = j - (int)lane;  // lane 0: nearest predecessor
+        unsigned long long w = idx >= 0 ? vs[idx] : (2ull << 32);
+        while (__any_sync(0xffffffffu, (w >> 32) == 0))
+            if ((w >> 32) == 0) w = vs[idx];
+        const uint32_t inc = __ballot_sync(0xffffffffu, (w >> 32) == 2);
+        if (inc) {
+            const uint32_t first = __ffs(inc) - 1;
+            excl += warp_sum(lane <= first ? (uint32_t)w : 0u);
+            break;
+        }
+        excl += warp_sum((uint32_t)w);
+    }
+    if (lane == 0) atomicExch(st + chunk, (2ull << 32) | (excl + local));
+    return excl;
+}
+
 // cp.async (Ampere-style LDGSTS) helpers: global -> shared without registers
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);

@@ -26,6 +26,14 @@ __host__ __device__ inline uint32_t rows_per_chunk(uint32_t K) {
     return r < 1 ? 1u : (r > (uint32_t)ROW_CHUNK ? (uint32_t)ROW_CHUNK : r);
 }
 
+// Rows per chunk of the decode pipeline's row kernels: u8 symbols with
+// K in {1, 2, 4} go to k_rows_small8 (SMALL_ROWS), everything else (and the
+// stage API) to the kernels chunked by rows_per_chunk.
+constexpr uint32_t SMALL_ROWS = 2048;
+__host__ __device__ inline uint32_t dec_chunk_rows(uint32_t K, uint32_t sym_bytes, bool stage) {
+    return (!stage && sym_bytes == 1 && (K == 1 || K == 2 || K == 4)) ? SMALL_ROWS : rows_per_chunk(K);
+}
+
 // float32((float64(v) - z) * scale) (tensor.py:154).  The 256-entry LUT covers
 // every u8 symbol; wider symbols >= 256 (only in hand-made streams) take an
 // out-of-line fp64 path so it is never if-converted into the hot loop.
@@ -54,37 +62,6 @@ struct RowParams {
     uint32_t* q_out;        // stage API: symbols
     uint8_t* mask_out;      // stage API: zero mask
 };
-
-// Decoupled look-back (single-pass scan) over the chunks of one tensor.
-// Word = flag << 32 | value; flag 1: the chunk's own row-count sum, flag 2:
-// inclusive prefix.  Chunks of a tensor are consecutive blockIdx.x of one
-// grid and start in order, so every predecessor makes progress.  Called by
-// one full warp; it inspects 32 predecessors per round.
-__device__ uint32_t chunk_prefix(unsigned long long* st, uint32_t chunk, uint32_t local) {
-    const uint32_t lane = threadIdx.x & 31;
-    const volatile unsigned long long* vs = st;
-    if (chunk == 0) {
-        if (lane == 0) atomicExch(st, (2ull << 32) | local);
-        return 0;
-    }
-    if (lane == 0) atomicExch(st + chunk, (1ull << 32) | local);
-    uint32_t excl = 0;
-    for (int j = (int)chunk - 1;; j -= 32) {
-        const int idx = j - (int)lane;  // lane 0: nearest predecessor
-        unsigned long long w = idx >= 0 ? vs[idx] : (2ull << 32);
-        while (__any_sync(0xffffffffu, (w >> 32) == 0))
-            if ((w >> 32) == 0) w = vs[idx];
-        const uint32_t inc = __ballot_sync(0xffffffffu, (w >> 32) == 2);
-        if (inc) {
-            const uint32_t first = __ffs(inc) - 1;
-            excl += warp_sum(lane <= first ? (uint32_t)w : 0u);
-            break;
-        }
-        excl += warp_sum((uint32_t)w);
-    }
-    if (lane == 0) atomicExch(st + chunk, (2ull << 32) | (excl + local));
-    return excl;
-}
 
 // A chunk of a tensor already marked bad (possibly by another chunk of this
 // very launch) still publishes, so later chunks never wait on it forever.
@@ -340,6 +317,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (in.sym_bytes != sizeof(S) || in.n_cols != (uint32_t)KK) return;
+    if (sizeof(S) == 1) return;                  // k_rows_small8 handles u8
     constexpr uint32_t R = (uint32_t)ROW_CHUNK;  // == rows_per_chunk(KK) for KK <= 4
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
@@ -429,6 +407,132 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
     __syncthreads();
     if (threadIdx.x == 0 && s_bad) p.status[b] = SCZ_CORRUPT_STREAM;
 }
+// Copy n bytes starting at an arbitrary global address into shared memory
+// with aligned 16-byte loads: byte i lands at dst[sh + i], sh = src & 15
+// (returned).  dst must hold n + 31 bytes; the over-read of up to 15 bytes
+// either side stays inside the caller's allocation.
+__device__ __forceinline__ uint32_t stage_window(uint8_t* dst, const uint8_t* src, uint32_t n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(src) - a);
+    const uint32_t n16 = (sh + n + 15) >> 4;
+    for (uint32_t i = threadIdx.x; i < n16; i += ROW_THREADS)
+        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(a) + i);
+    return sh;
+}
+
+// 4 consecutive bytes at byte offset o of a shared array (any alignment).
+__device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(s) + (o >> 2);
+    return __funnelshift_r(w[0], w[1], (o & 3) * 8);
+}
+
+// u8 symbols, K in {1, 2, 4} (the decode pipeline's hot case: every BASELINE
+// shape picks one of these).  A chunk is SMALL_ROWS rows.  Its row counts,
+// and after the chunk's nonzero offset is known its column and value
+// segments, are staged into shared memory with aligned 16-byte loads; a row
+// then reads its <= 4 columns and values as one funnel-shifted word each, so
+// a row costs a handful of instructions.  Consecutive threads own
+// consecutive rows: every store instruction of a warp is one contiguous,
+// coalesced span of 32 rows.  Checks as sparse.py:84-97.
+template <int KK>
+__global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
+    static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
+    pdl_wait();
+    const uint32_t b = blockIdx.y, chunk = blockIdx.x;
+    const scz_info& in = p.info[b];
+    if (in.sym_bytes != 1 || in.n_cols != (uint32_t)KK) return;
+    constexpr uint32_t R = SMALL_ROWS;
+    constexpr uint32_t PER = R / ROW_THREADS;
+    constexpr uint32_t MAXE = R * KK;  // nonzeros of a valid chunk
+    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
+    if (r0 >= N) return;
+    if (chunk_dead(p, b, chunk)) return;
+    const uint64_t nnz = in.nnz;
+    const uint8_t* d = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    __shared__ __align__(16) uint8_t s_r[R + 32];
+    __shared__ __align__(16) uint8_t s_c[MAXE + 32];
+    __shared__ __align__(16) uint8_t s_v[MAXE + 32];
+    __shared__ uint16_t s_off[R];
+    __shared__ uint32_t s_scan[33];
+    __shared__ float s_lut[256];
+    __shared__ int s_bad;
+    const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
+    build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
+    if (threadIdx.x == 0) s_bad = 0;
+    const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);
+    __syncthreads();
+    // thread t sums rows [PER t, PER t + PER) of the chunk
+    uint32_t loc[PER], sum = 0;
+    bool rbad = false;
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) {
+        const uint32_t i = threadIdx.x * PER + j;
+        const uint32_t v = i < nrow ? (uint32_t)s_r[rsh + i] : 0u;
+        rbad |= v > (uint32_t)KK;  // sparse.py:88-89
+        loc[j] = min(v, (uint32_t)KK + 1);
+        sum += loc[j];
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
+    if (rbad) s_bad = 1;
+    const uint32_t cbase = block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
+    if (s_bad) {  // from here on tot <= nrow * KK and cbase + tot <= nnz
+        if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+        return;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) {
+        s_off[threadIdx.x * PER + j] = (uint16_t)ex;
+        ex += loc[j];
+    }
+    const uint32_t csh = stage_window(s_c, d + nnz + cbase, tot);
+    const uint32_t vsh = stage_window(s_v, d + cbase, tot);
+    __syncthreads();
+    float* orow0 = p.out + p.out_off[b] + r0 * KK;
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
+    bool bad = false;
+#pragma unroll 2
+    for (uint32_t j = 0; j < PER; ++j) {
+        const uint32_t li = j * ROW_THREADS + threadIdx.x;
+        if (li >= nrow) break;
+        const uint32_t off = s_off[li], r = s_r[rsh + li];
+        const uint32_t cw = smem_word_at(s_c, csh + off);  // bytes past r are ignored
+        const uint32_t vw = smem_word_at(s_v, vsh + off);
+        uint32_t mask = 0, prev = 0;
+#pragma unroll
+        for (int e = 0; e < KK; ++e) {
+            const uint32_t c = (cw >> (8 * e)) & 0xFFu;
+            const bool live = (uint32_t)e < r;
+            bad |= live & ((c >= (uint32_t)KK) | ((e > 0) & (c <= prev)));  // sparse.py:90-97
+            mask |= live ? (1u << (c & (KK - 1))) : 0u;
+            prev = c;
+        }
+        float o[KK];
+#pragma unroll
+        for (int col = 0; col < KK; ++col) {
+            const uint32_t k = __popc(mask & ((1u << col) - 1u));  // entries left of col
+            const float val = s_lut[(vw >> (8 * k)) & 0xFFu];
+            o[col] = (mask >> col) & 1u ? val : 0.0f;
+        }
+        float* orow = orow0 + (uint64_t)li * KK;
+        if constexpr (KK == 4) {
+            if (vec_ok) __stcs(reinterpret_cast<float4*>(orow), make_float4(o[0], o[1], o[2], o[3]));
+            else { orow[0] = o[0]; orow[1] = o[1]; orow[2] = o[2]; orow[3] = o[3]; }
+        } else if constexpr (KK == 2) {
+            if (vec_ok) __stcs(reinterpret_cast<float2*>(orow), make_float2(o[0], o[1]));
+            else { orow[0] = o[0]; orow[1] = o[1]; }
+        } else {
+            __stcs(orow, o[0]);
+        }
+    }
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_bad) p.status[b] = SCZ_CORRUPT_STREAM;
+}
+template __global__ void k_rows_small8<1>(RowParams);
+template __global__ void k_rows_small8<2>(RowParams);
+template __global__ void k_rows_small8<4>(RowParams);
+
 #define SCZ_INST_SMALL(S)                                      \
     template __global__ void k_rows_small<S, 1>(RowParams);    \
     template __global__ void k_rows_small<S, 2>(RowParams);    \

@@ -442,8 +442,7 @@ __device__ __forceinline__ void store_sym(void* base, uint64_t i, uint32_t v) {
 }
 
 template <typename S>
-__global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
-    pdl_wait();
+__device__ __forceinline__ void materialize_body(const MatParams& p) {
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
@@ -502,6 +501,20 @@ __global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
         for (uint64_t i = i0 + threadIdx.x; i < i1; i += TILE_THREADS)
             cr[nnz + i] = (S)range_popc(bm, i * K, K);
     }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
+    pdl_wait();
+    materialize_body<S>(p);
+}
+
+// The pipeline's launch: u8 and u16 classes in one grid (see k_rans_enc_v2_u8u16).
+__global__ void __launch_bounds__(TILE_THREADS) k_materialize_u8u16(MatParams p8, MatParams p16) {
+    pdl_wait();
+    const uint32_t w = p8.state[blockIdx.y].sym_bytes;
+    if (w == 2) materialize_body<uint16_t>(p16);
+    else if (w == 1) materialize_body<uint8_t>(p8);
 }
 
 template __global__ void k_materialize<uint8_t>(MatParams);

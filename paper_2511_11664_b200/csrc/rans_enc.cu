@@ -21,6 +21,89 @@ namespace scz {
 constexpr int ENC2_WPB = 4;                  // warps (= blocks) per CTA
 constexpr uint32_t ENC_TAB_SMEM_MAX = 8192;  // table entries staged in smem (128 KB)
 
+// In-kernel packing (pipeline launches; payload == nullptr for the stage
+// API): once a warp has coded its block it publishes the block's byte length,
+// finds the block's payload offset by decoupled look-back over the tensor's
+// earlier blocks (chunk_prefix), and copies the block from its slot into the
+// tensor's payload region [b * pcap, b * pcap + payload_len).  The tensor's
+// last block then knows the payload length and writes the header (scz_info).
+struct PackParams {
+    uint8_t* payload;          // [B][pcap]
+    uint64_t pcap;
+    unsigned long long* lb;    // [B][slots_per_tensor] look-back words (zeroed)
+    scz_info* info;            // [B]
+    uint64_t total;
+    int q_bits;
+    int write_failed;          // this launch writes the headers of failed tensors
+};
+
+// The header of tensor b from its device state (container.py:32-70 fields).
+__device__ __forceinline__ void write_info(scz_info& in, const TensorState& st, int32_t status, int format,
+                                           int q_bits, int precision, uint64_t total, uint32_t block_syms,
+                                           uint32_t nb, uint64_t plen, uint64_t payload_off, uint32_t acap,
+                                           uint32_t slots_per_tensor, uint32_t b) {
+    in.status = status;
+    in.version = (uint8_t)format;
+    in.q_bits = (uint8_t)q_bits;
+    in.precision = (uint8_t)precision;
+    in.sym_bytes = (uint8_t)st.sym_bytes;
+    in.total = total;
+    in.n_rows = st.n_rows;
+    in.n_cols = st.n_cols;
+    in.nnz = st.nnz;
+    in.scale = st.scale;
+    in.zero_point = st.zero_point;
+    in.alphabet = st.alphabet;
+    in.lanes = format == 2 ? 32 : 1;
+    in.block_syms = format == 2 ? block_syms : (uint32_t)st.stream_len;
+    in.n_blocks = nb;
+    in.payload_len = plen;
+    in.payload_off = payload_off;
+    in.freqs_off = (uint64_t)b * acap;
+    in.blocks_off = (uint64_t)b * slots_per_tensor;
+    in.search_flags = st.search_flags;
+    in.n_evaluated = st.n_evaluated;
+}
+
+// status after the encoder's overflow / uncodable flags (rans.py:176-179)
+__device__ __forceinline__ int32_t final_status(const TensorState& st, uint32_t errbits) {
+    if (st.status != SCZ_OK) return st.status;
+    if (errbits & 1u) return SCZ_ALPHABET_OVERFLOW;
+    if (errbits & 2u) return SCZ_UNCODABLE_SYMBOL;
+    return SCZ_OK;
+}
+
+// Copy len bytes src -> dst (any alignments) with one warp: bytes up to a
+// 4-aligned destination, funnel-shifted words, then the tail.  src is a slot
+// (padded: the word after the last is readable).
+__device__ __forceinline__ void warp_copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t len, uint32_t lane) {
+    uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
+    head = head < len ? head : len;
+    if (lane < head) dst[lane] = src[lane];
+    const uint8_t* s2 = src + head;
+    uint32_t* d2 = reinterpret_cast<uint32_t*>(dst + head);
+    const uint32_t nwords = (len - head) / 4;
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(s2) & 3) * 8;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s2) & ~(uintptr_t)3);
+    // eight words per lane in flight per round: at B = 1 this copy sits on
+    // the latency path, one L2 round trip per round
+    for (uint32_t w0 = 0; w0 < nwords; w0 += 256) {
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t w = w0 + 32 * k + lane;
+            lo[k] = w < nwords ? sw[w] : 0u;
+            hi[k] = w < nwords ? sw[w + 1] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t w = w0 + 32 * k + lane;
+            if (w < nwords) d2[w] = sh ? __funnelshift_r(lo[k], hi[k], sh) : lo[k];
+        }
+    }
+    for (uint32_t i = head + 4 * nwords + lane; i < len; i += 32) dst[i] = src[i];
+}
+
 template <typename S>
 struct SplitCursor {
     const uint8_t* v;
@@ -117,11 +200,15 @@ __device__ __forceinline__ void enc_apply(EncLane& L, const EncTab& t, bool live
 }
 
 template <class Src, bool SMEM, bool CHECK>
-__global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src src) {
-    pdl_wait();
+__device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, const PackParams& pk) {
     const uint32_t b = blockIdx.y;
     TensorState& st = p.state[b];
-    if (st.status != SCZ_OK) return;
+    if (st.status != SCZ_OK) {
+        if (pk.payload && pk.write_failed && blockIdx.x == 0 && threadIdx.x == 0)
+            write_info(pk.info[b], st, st.status, 2, pk.q_bits, p.precision, pk.total, p.block_syms, 0, 0,
+                       (uint64_t)b * pk.pcap, p.acap, p.slots_per_tensor, b);
+        return;
+    }
     if (Src::width && st.sym_bytes != (uint32_t)Src::width) return;  // other width variant
     const uint64_t L = st.stream_len;
     const uint32_t nblk = L ? ceil_div_u32(L, p.block_syms) : 1;
@@ -232,11 +319,43 @@ __global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src 
         p.block_len[(uint64_t)b * p.slots_per_tensor + blk] = blen;
         if (CHECK && E.err) atomicOr(&st.errbits, E.err);
     }
+    if (pk.payload) {
+        __threadfence();  // error bits before the length is published
+        __syncwarp();     // the slot bytes of every lane are visible to the warp
+        const uint32_t excl = chunk_prefix(pk.lb + (uint64_t)b * p.slots_per_tensor, blk, blen);
+        warp_copy_bytes(pk.payload + (uint64_t)b * pk.pcap + excl, start, blen, lane);
+        if (blk == nblk - 1 && lane == 0) {
+            __threadfence();  // every block published: their error bits are visible
+            const uint32_t eb = *(volatile uint32_t*)&st.errbits;
+            write_info(pk.info[b], st, final_status(st, eb), 2, pk.q_bits, p.precision, pk.total, p.block_syms,
+                       nblk, (uint64_t)excl + blen, (uint64_t)b * pk.pcap, p.acap, p.slots_per_tensor, b);
+        }
+    }
 }
 
-#define SCZ_INST_ENC2(SRC, CHK)                                                  \
-    template __global__ void k_rans_enc_v2<SRC, true, CHK>(EncParams, SRC);     \
-    template __global__ void k_rans_enc_v2<SRC, false, CHK>(EncParams, SRC);
+template <class Src, bool SMEM, bool CHECK>
+__global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src src, PackParams pk) {
+    pdl_wait();
+    enc_v2_body<Src, SMEM, CHECK>(p, src, pk);
+}
+
+// The pipeline's launch: u8 and u16 symbol classes in one grid (a tensor's
+// class is known only after k_select), so no launch is spent on an empty
+// class.  u32 tensors (K > 65535) go to k_rans_enc_v2<SplitSrc<uint32_t>>.
+template <bool SMEM>
+__global__ void __launch_bounds__(ENC2_WPB * 32)
+    k_rans_enc_v2_u8u16(EncParams p, Contig8Src s8, SplitSrc<uint16_t> s16, PackParams pk) {
+    pdl_wait();
+    const TensorState& st = p.state[blockIdx.y];
+    if (st.status == SCZ_OK && st.sym_bytes == 2) enc_v2_body<SplitSrc<uint16_t>, SMEM, false>(p, s16, pk);
+    else enc_v2_body<Contig8Src, SMEM, false>(p, s8, pk);  // also writes failed tensors' headers
+}
+template __global__ void k_rans_enc_v2_u8u16<true>(EncParams, Contig8Src, SplitSrc<uint16_t>, PackParams);
+template __global__ void k_rans_enc_v2_u8u16<false>(EncParams, Contig8Src, SplitSrc<uint16_t>, PackParams);
+
+#define SCZ_INST_ENC2(SRC, CHK)                                                              \
+    template __global__ void k_rans_enc_v2<SRC, true, CHK>(EncParams, SRC, PackParams);     \
+    template __global__ void k_rans_enc_v2<SRC, false, CHK>(EncParams, SRC, PackParams);
 SCZ_INST_ENC2(Contig8Src, false)
 SCZ_INST_ENC2(SplitSrc<uint8_t>, false)
 SCZ_INST_ENC2(SplitSrc<uint16_t>, false)

@@ -15,6 +15,7 @@ from paper_2511_11664_b200.synth import make_input  # noqa: E402
 
 dims = (1, 256, 56, 56)
 T = int(np.prod(dims))
+BS = int(os.environ.get("BLOCK_SYMS", "8192"))
 x = torch.from_numpy(make_input(dict(kind="relu-laplace", dims=dims, sparsity=0.5, seed=0))).cuda()
 out = torch.empty_like(x)
 ctx = _native.context(0)
@@ -27,7 +28,7 @@ for it in range(60):
     a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     t0 = time.perf_counter()
     a.record(stream)
-    ctx.check(lib.scz_encode_batch(ctx.h, ctypes.c_void_p(x.data_ptr()), T, 1, 8, -1, 14, 2, 32, 8192,
+    ctx.check(lib.scz_encode_batch(ctx.h, ctypes.c_void_p(x.data_ptr()), T, 1, 8, -1, 14, 2, 32, BS,
                                    ctypes.byref(batch)))
     t1 = time.perf_counter()
     ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), info))
