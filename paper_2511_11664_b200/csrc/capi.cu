@@ -34,6 +34,7 @@ std::atomic<uint64_t> g_alloc_gen{1};
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    bool fresh = false;  // allocated since the owner last cleared it
     cudaError_t ensure(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFree(p);
@@ -41,7 +42,10 @@ struct DevBuf {
         cap = 0;
         size_t want = std::max<size_t>(n + n / 8, 4096);
         cudaError_t e = cudaMalloc(&p, want);
-        if (e == cudaSuccess) cap = want;
+        if (e == cudaSuccess) {
+            cap = want;
+            fresh = true;
+        }
         g_alloc_gen.fetch_add(1);
         return e;
     }
@@ -622,15 +626,35 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     CK(ctx->info.ensure((size_t)B * sizeof(scz_info)));
     CK(ctx->payload.ensure((size_t)B * pl.payload_cap + 4096));
     CK(ctx->ticket.ensure(64));
-    CK(cudaMemsetAsync(ctx->state.p, 0, (size_t)B * sizeof(TensorState), s));
-    CK(cudaMemsetAsync(ctx->vhist.p, 0, (size_t)B * 256 * 4, s));
-    CK(cudaMemsetAsync(ctx->ticket.p, 0, 64, s));
+    // Scratch that must start at zero: the per-tensor state (k_stats re-arms
+    // its fields), the k_finalize ticket (re-armed) and the select tickets
+    // (re-armed) once after allocation; the accumulation targets below are
+    // zeroed by k_stats itself (ZeroSpec), so no memset sits on the path.
+    for (DevBuf* z : {&ctx->state, &ctx->ticket}) {
+        if (z->fresh) CK(cudaMemsetAsync(z->p, 0, z->cap, s));
+        z->fresh = false;
+    }
     bool need_hist = false;
     for (uint64_t n : pl.rows) need_hist |= (T / n) > 1;
+    ZeroSpec zs{};
+    zs.ptr[0] = ctx->vhist.as<uint32_t>();
+    zs.words[0] = 256;
     if (need_hist) {
-        CK(cudaMemsetAsync(ctx->hp.p, 0, (size_t)B * pl.period * 4, s));
-        CK(cudaMemsetAsync(ctx->rhist.p, 0, (size_t)B * rh_total * 4, s));
+        zs.ptr[1] = ctx->hp.as<uint32_t>();
+        zs.words[1] = (uint32_t)pl.period;
+        zs.ptr[2] = ctx->rhist.as<uint32_t>();
+        zs.words[2] = (uint32_t)rh_total;
     }
+    if (pl.format == 2) {
+        CK(ctx->lbwords.ensure((size_t)B * pl.nblk_cap * 8));
+        zs.ptr[3] = ctx->lbwords.as<uint32_t>();
+        zs.words[3] = 2 * pl.nblk_cap;
+    }
+    CK(ctx->selbuf.ensure((size_t)B * (MAX_CAND * 20 + 16)));  // select tickets live at its end
+    uint32_t* sel_ticket = reinterpret_cast<uint32_t*>(ctx->selbuf.as<double>() + (size_t)B * MAX_CAND * 2) +
+                           (size_t)B * MAX_CAND;
+    zs.ptr[4] = sel_ticket;
+    zs.words[4] = 1;
 
     // K1+K2+K3: fused single-read front end when every tensor's tiles fit in
     // one co-resident grid (cooperative launch), else stats then quantise.
@@ -644,6 +668,9 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     if (ctx->use_front && pl.n_tiles <= ctx->front_grid && ctx->front_grid > 1) {
         CK(ctx->ready.ensure((size_t)B * 4));
         CK(cudaMemsetAsync(ctx->ready.p, 0, (size_t)B * 4, s));
+        CK(cudaMemsetAsync(ctx->state.p, 0, (size_t)B * sizeof(TensorState), s));
+        for (int r = 0; r < 5; ++r)  // k_front does not take a ZeroSpec
+            if (zs.ptr[r]) CK(cudaMemsetAsync(zs.ptr[r], 0, (size_t)B * zs.words[r] * 4, s));
         FrontParams fp{d_x, T, pl.n_tiles, pl.words_pad, B, pl.q_bits, ctx->bitmap.as<uint32_t>(),
                        ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(),
                        ctx->ready.as<uint32_t>(), ctx->v8.as<uint8_t>(), ctx->vhist.as<uint32_t>(), dstride};
@@ -653,7 +680,8 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         LAUNCHED("k_front");
     } else {
         StatsParams sp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
-                       ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>()};
+                       ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(),
+                       zs};
         CK(launch_pdl(k_stats, dim3(pl.n_tiles, B), TILE_THREADS, 0, s, sp));
         LAUNCHED("k_stats");
         QuantParams qp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
@@ -761,12 +789,10 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         const uint32_t room = std::max<uint32_t>(1, (uint32_t)(2 * ctx->num_sms) / B);
         sel.groups = std::max<uint32_t>(1, std::min(want, room));
     }
-    if (sel.groups > 1) {
-        CK(ctx->selbuf.ensure((size_t)B * (MAX_CAND * 20 + 16)));
+    if (sel.groups > 1) {  // (the tickets were zeroed by k_stats)
         sel.gcost = ctx->selbuf.as<double>();
         sel.gacnt = reinterpret_cast<uint32_t*>(sel.gcost + (size_t)B * MAX_CAND * 2);
-        sel.ticket = sel.gacnt + (size_t)B * MAX_CAND;
-        CK(cudaMemsetAsync(sel.ticket, 0, (size_t)B * 4, s));
+        sel.ticket = sel_ticket;
     }
     const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)rh_total) : 0;
     if (sel_smem > 0)  // static BlockScratch + dynamic may pass 48 KB: always opt in
@@ -794,9 +820,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
 
     // v2: blocks are packed into the payload inside the encoder (PackParams)
     PackParams pk{};
-    if (pl.format == 2) {
-        CK(ctx->lbwords.ensure((size_t)B * pl.nblk_cap * 8));
-        CK(cudaMemsetAsync(ctx->lbwords.p, 0, (size_t)B * pl.nblk_cap * 8, s));
+    if (pl.format == 2) {  // (look-back words zeroed by k_stats)
         pk = PackParams{ctx->payload.as<uint8_t>(), pl.payload_cap, ctx->lbwords.as<unsigned long long>(),
                         ctx->info.as<scz_info>(), T, pl.q_bits, 1};
     }

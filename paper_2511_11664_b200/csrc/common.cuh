@@ -164,6 +164,27 @@ __device__ uint32_t chunk_prefix(unsigned long long* st, uint32_t chunk, uint32_
     return excl;
 }
 
+// Copy len bytes from shared memory (16-byte aligned, >= len + 4 bytes
+// readable) to global memory at any alignment: a head to the first 16-byte
+// boundary of dst, then 16-byte stores assembled from funnel-shifted shared
+// words, then the tail.  All NT threads of the block call it.
+template <int NT>
+__device__ __forceinline__ void block_copy_s2g(uint8_t* dst, const uint8_t* s_src, uint32_t len) {
+    uint32_t head = (uint32_t)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15);
+    head = head < len ? head : len;
+    if (threadIdx.x < head) dst[threadIdx.x] = s_src[threadIdx.x];
+    const uint32_t n16 = (len - head) >> 4;
+    const uint32_t sh = (head & 3) * 8;
+    for (uint32_t c = threadIdx.x; c < n16; c += NT) {
+        const uint32_t o = head + 16 * c;
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(s_src) + (o >> 2);
+        const uint32_t a0 = w[0], a1 = w[1], a2 = w[2], a3 = w[3], a4 = w[4];
+        *reinterpret_cast<uint4*>(dst + o) = make_uint4(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh),
+                                                        __funnelshift_r(a2, a3, sh), __funnelshift_r(a3, a4, sh));
+    }
+    for (uint32_t i = head + 16 * n16 + threadIdx.x; i < len; i += NT) dst[i] = s_src[i];
+}
+
 // cp.async (Ampere-style LDGSTS) helpers: global -> shared without registers
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);

@@ -14,6 +14,14 @@
 
 namespace scz {
 
+// Per-tensor scratch regions zeroed by k_stats for the kernels after it
+// (replaces memset launches on the latency path): region r of tensor b is
+// ptr[r][b * words[r], (b + 1) * words[r]), split over the tensor's tiles.
+struct ZeroSpec {
+    uint32_t* ptr[5];
+    uint32_t words[5];
+};
+
 struct StatsParams {
     const float* x;
     uint64_t total;       // T
@@ -24,6 +32,7 @@ struct StatsParams {
     float4* tile_stats;   // [B][n_tiles] {min, max, nnz(bits), nonfinite(bits)}
     uint32_t* tile_off;   // [B][n_tiles] exclusive nnz prefix
     TensorState* state;   // [B]
+    ZeroSpec zero;        // optional (pipeline launches)
 };
 
 // Load 4 consecutive elements starting at idx (idx % 4 == 0); out-of-range
@@ -90,6 +99,15 @@ __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
 #pragma unroll
     for (int it = 0; it < 8; ++it)
         vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &vvalid[it]);
+    // scratch zeroing for the later kernels, while the loads are in flight
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        if (!p.zero.ptr[r]) continue;
+        const uint32_t w = p.zero.words[r], per = (w + p.n_tiles - 1) / p.n_tiles;
+        uint32_t* z = p.zero.ptr[r] + (uint64_t)b * w;
+        const uint32_t i1 = min(w, (tile + 1) * per);
+        for (uint32_t i = tile * per + threadIdx.x; i < i1; i += TILE_THREADS) z[i] = 0u;
+    }
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
         const uint32_t valid = vvalid[it];
@@ -192,6 +210,8 @@ __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
         st.nonfinite = gbad;
         st.nnz = carry;
         st.tiles_done = 0;  // re-arm for the next launch
+        st.errbits = 0;
+        st.status = SCZ_OK;
         if (gbad) {
             st.status = SCZ_INVALID_INPUT;
             st.scale = 1.0;
@@ -243,10 +263,12 @@ __device__ __noinline__ uint32_t quant_exact(float x, double scale, double zf, d
 __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, int qmax,
                                                double scale, double zf, bool fast) {
     if (fast) {
-        float y = fmaf(x, r32, zf32);
-        float fr = y - floorf(y);
-        if (fabsf(fr - 0.5f) > 0x1p-12f) {
-            int q = __float2int_rn(y);
+        // d = y - rint(y) is exact; y lies within 2^-12 of a half-integer
+        // iff |d| >= 1/2 - 2^-12, and only those take the exact path
+        const float y = fmaf(x, r32, zf32);
+        const float rq = rintf(y);
+        if (fabsf(y - rq) < 0.5f - 0x1p-12f) {
+            const int q = (int)rq;
             return (uint32_t)min(max(q, 0), qmax);
         }
     }
@@ -269,6 +291,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     __shared__ uint32_t s_wbits[TILE_WORDS];
     __shared__ uint32_t s_scan[33];
     __shared__ uint32_t s_hist[4][256];  // one copy per warp pair: less atomic contention
+    __shared__ __align__(16) uint8_t s_v[TILE + 32];  // the tile's value symbols, rank order
     const int nbins = 1 << p.q_bits;
     for (int i = threadIdx.x; i < 4 * 256; i += TILE_THREADS) (&s_hist[0][0])[i] = 0;
     // all eight 16-byte loads in flight first
@@ -290,30 +313,57 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     const int qmax = nbins - 1;
     uint8_t* v8 = p.v8 + (uint64_t)b * p.v8_stride;
 
+    // Branch-free over all 32 elements of the thread: the fp32 estimate for
+    // every element, the store and the histogram count predicated on the
+    // element's bitmap bit; elements near a rounding boundary (or every
+    // element when the scale is out of the fp32 range) are collected in
+    // `slow` and redone with the exact fp64 sequence afterwards.
+    uint32_t slow = 0;  // bit 4 * it + j: element needs the exact path
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
-        const uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4;
-        const uint32_t valid = vvalid[it];
         const float4 v = vv[it];
-        float e[4] = {v.x, v.y, v.z, v.w};
+        const float e[4] = {v.x, v.y, v.z, v.w};
         const int word = warp * 32 + it * 4 + (lane >> 3);
-        const uint32_t wbits = s_wbits[word];
         const int bit0 = 4 * (lane & 7);
-        uint32_t rank = base_rank + s_wpre[word] + __popc(wbits & ((1u << bit0) - 1u));
+        const uint32_t wbits = s_wbits[word];
+        const uint32_t nib = (wbits >> bit0) & 0xFu;  // nonzero flags (bitmap == x != 0, valid only)
+        uint32_t rank = s_wpre[word] + __popc(wbits & ((1u << bit0) - 1u));  // tile-local
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if ((valid >> j & 1) && e[j] != 0.0f) {
-                uint32_t q = quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
-                v8[rank++] = (uint8_t)q;
-                atomicAdd(&s_hist[warp & 3][q], 1u);
-                if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + idx + j] = q;
-            } else if (SYM_OUT && (valid >> j & 1)) {
-                p.sym_out[(uint64_t)b * p.total + idx + j] =
-                    quant_fast(e[j], r32, zf32, qmax, scale, zf, fast);
+            const float y = fmaf(e[j], r32, zf32);
+            const float rq = rintf(y);
+            const bool ok = fast && fabsf(y - rq) < 0.5f - 0x1p-12f;
+            const uint32_t q = (uint32_t)min(max((int)rq, 0), qmax);
+            const bool nz = (nib >> j) & 1u;
+            slow |= (uint32_t)(!ok && ((vvalid[it] >> j) & 1u)) << (4 * it + j);
+            if (nz) {
+                s_v[rank] = (uint8_t)q;
+                if (ok) atomicAdd(&s_hist[warp & 3][q], 1u);
             }
+            if constexpr (SYM_OUT)
+                if ((vvalid[it] >> j) & 1u)
+                    p.sym_out[(uint64_t)b * p.total + tile_base + warp * 1024 + it * 128 + lane * 4 + j] = q;
+            rank += nz;
         }
     }
+    while (slow) {  // rare: exact fp64 path (tensor.py:130-140), x re-read
+        const int k = __ffs(slow) - 1;
+        slow &= slow - 1;
+        const int it = k >> 2, j = k & 3;
+        const uint32_t off = warp * 1024 + it * 128 + lane * 4 + j;
+        const int word = warp * 32 + it * 4 + (lane >> 3);
+        const int bit = 4 * (lane & 7) + j;
+        const uint32_t wbits = s_wbits[word];
+        const uint32_t q = quant_exact(xb[tile_base + off], scale, zf, (double)qmax);
+        if ((wbits >> bit) & 1u) {
+            s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
+            atomicAdd(&s_hist[warp & 3][q], 1u);
+        }
+        if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + tile_base + off] = q;
+    }
     __syncthreads();
+    // the tile's values go out with coalesced 16-byte stores
+    block_copy_s2g<TILE_THREADS>(v8 + base_rank, s_v, tot);
     uint32_t* gh = p.vhist + (uint64_t)b * 256;
     for (int i = threadIdx.x; i < nbins; i += TILE_THREADS) {
         const uint32_t t = s_hist[0][i] + s_hist[1][i] + s_hist[2][i] + s_hist[3][i];
