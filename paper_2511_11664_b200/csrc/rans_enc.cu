@@ -199,6 +199,43 @@ __device__ __forceinline__ void enc_apply(EncLane& L, const EncTab& t, bool live
     if (live) L.x = x;
 }
 
+// The u8 pipeline path's step: table entries pre-transformed at staging
+// (freq -> bound = f << (31 - n), cum -> bias, shift -> shift | cmpl << 16
+// with cmpl = 2^n - f; f = 1 as rcp = 2^32 - 1, shift 0, bias = cum + 2^n - 1),
+// so x' = x + bias + q * cmpl with q = umulhi(x, rcp) >> shift equals
+// (x / f << n) + cum + x % f (rans.py:143-144) for every f >= 1 -- three
+// dependent operations on the state.  Bytes go to a per-warp shared ring
+// (ob, RB bytes, same backwards order as the slot), flushed in 16-byte chunks.
+constexpr uint32_t ENC_RB = 2048;
+__device__ __forceinline__ EncTab enc_tab_fast(const EncTab& e, int n) {
+    EncTab f;
+    f.freq = e.freq << (31 - n);
+    if (e.shift == 0xFFFFFFFFu) {  // f <= 1
+        f.cum = e.cum + (1u << n) - 1u;
+        f.rcp = 0xFFFFFFFFu;
+        f.shift = ((1u << n) - 1u) << 16;
+    } else {
+        f.cum = e.cum;
+        f.rcp = e.rcp;
+        f.shift = e.shift | (((1u << n) - e.freq) << 16);
+    }
+    return f;
+}
+__device__ __forceinline__ void enc_apply_ring(EncLane& L, const EncTab& t, bool live, uint32_t gtm, uint8_t* ob) {
+    const bool e1 = live && L.x >= t.freq;
+    const bool e2 = live && (L.x >> 8) >= t.freq;
+    const uint32_t b1 = __ballot_sync(0xffffffffu, e1);
+    const uint32_t b2 = __ballot_sync(0xffffffffu, e2);
+    const uint32_t pos = L.emitted + __popc(b1 & gtm) + __popc(b2 & gtm) + 1;
+    if (e1) ob[(0u - pos) & (ENC_RB - 1)] = (uint8_t)L.x;
+    if (e2) ob[(0u - pos - 1) & (ENC_RB - 1)] = (uint8_t)(L.x >> 8);
+    L.emitted += __popc(b1) + __popc(b2);
+    const uint32_t x = e2 ? (L.x >> 16) : (e1 ? (L.x >> 8) : L.x);
+    const uint32_t q = __funnelshift_r(__umulhi(x, t.rcp), 0u, t.shift);
+    const uint32_t xn = x + t.cum + q * (t.shift >> 16);
+    if (live) L.x = xn;
+}
+
 template <class Src, bool SMEM, bool CHECK>
 __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, const PackParams& pk) {
     const uint32_t b = blockIdx.y;
@@ -217,8 +254,10 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
     extern __shared__ EncTab s_tab[];  // A entries when SMEM (host: A <= p.tab_smem)
     const uint32_t A = st.alphabet;
     const EncTab* gt = p.enctab + (uint64_t)b * p.acap;
+    constexpr bool RING = std::is_same<Src, Contig8Src>::value && SMEM && !CHECK;
     if constexpr (SMEM) {
-        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) s_tab[i] = gt[i];
+        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x)
+            s_tab[i] = RING ? enc_tab_fast(gt[i], p.precision) : gt[i];
         __syncthreads();
     }
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -232,12 +271,23 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
     const uint32_t gtm = lanemask_gt();
     uint8_t* slot_end = p.slots + ((uint64_t)b * p.slots_per_tensor + blk + 1) * p.slot_cap;
     EncLane E{STATE_LOW, 0u, 0u};
-    if constexpr (std::is_same<Src, Contig8Src>::value && SMEM && !CHECK) {
+    if constexpr (RING) {
         // u8 symbols staged through a per-warp 2 x 1 KB shared ring (chunk g =
         // steps [32g, 32g + 32) = block bytes [1024g, 1024g + 1024)), fetched
         // one chunk ahead with cp.async; the table entry of the next step is
-        // loaded while the current one is coded.
+        // loaded while the current one is coded.  Output bytes collect in a
+        // per-warp shared ring and leave in 16-byte chunks every 16 steps.
         __shared__ __align__(16) uint8_t s_ring[ENC2_WPB][2][1024];
+        __shared__ __align__(16) uint8_t s_ob[ENC2_WPB][ENC_RB];
+        uint8_t* ob = s_ob[warp];
+        uint32_t flushed = 0;  // bytes already in the slot (multiple of 16)
+        auto flush = [&]() {   // every complete 16-byte chunk since the last flush
+            const uint32_t upto = E.emitted & ~15u;
+            for (uint32_t c = flushed + 16 * lane; c < upto; c += 512)
+                *reinterpret_cast<uint4*>(slot_end - c - 16) =
+                    *reinterpret_cast<const uint4*>(ob + ((0u - c - 16) & (ENC_RB - 1)));
+            flushed = upto;
+        };
         const uint8_t* gsym = cur.d;
         auto fetch = [&](int g) {
             if (g >= 0) {
@@ -256,30 +306,39 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
                 cp_async_wait<1>();
                 __syncwarp();
                 const uint8_t* rs = s_ring[warp][g & 1] + lane;
-                const int s_lo = g * 32;
-                int s = g == g_top ? s_top : s_lo + 31;
-                EncTab t;
-                if (g == g_top) {  // the highest step may be partial
-                    const bool act = (uint32_t)s * 32 + lane < len;
-                    t = s_tab[act ? rs[(s & 31) * 32] : 0];
-                    enc_apply(E, t, act, n, sh_bound, gtm, slot_end);
-                    --s;
-                }
-                if (s >= s_lo) {
-                    t = s_tab[rs[(s & 31) * 32]];
-#pragma unroll 4
-                    for (; s > s_lo; --s) {
-                        const EncTab tn = s_tab[rs[((s - 1) & 31) * 32]];
-                        enc_apply(E, t, true, n, sh_bound, gtm, slot_end);
-                        t = tn;
+#pragma unroll 1
+                for (int h = 1; h >= 0; --h) {  // half-chunks of 16 steps
+                    const int lo = g * 32 + 16 * h;
+                    int s = min(lo + 15, s_top);
+                    if (s < lo) continue;
+                    EncTab t;
+                    if (s == s_top) {  // the highest step may be partial
+                        const bool act = (uint32_t)s * 32 + lane < len;
+                        t = s_tab[act ? rs[(s & 31) * 32] : 0];
+                        enc_apply_ring(E, t, act, gtm, ob);
+                        --s;
                     }
-                    enc_apply(E, t, true, n, sh_bound, gtm, slot_end);
+                    if (s >= lo) {
+                        t = s_tab[rs[(s & 31) * 32]];
+#pragma unroll 4
+                        for (; s > lo; --s) {
+                            const EncTab tn = s_tab[rs[((s - 1) & 31) * 32]];
+                            enc_apply_ring(E, t, true, gtm, ob);
+                            t = tn;
+                        }
+                        enc_apply_ring(E, t, true, gtm, ob);
+                    }
+                    __syncwarp();
+                    flush();
                 }
                 __syncwarp();
                 fetch(g - 2);
             }
         }
         cp_async_wait<0>();
+        // the last partial chunk, byte by byte
+        const uint32_t k = flushed + lane;
+        if (k < E.emitted) slot_end[-(int32_t)k - 1] = ob[(0u - k - 1) & (ENC_RB - 1)];
     } else if (steps > 0) {
         // the highest step may be partial: peel it
         const int s_top = steps - 1;
