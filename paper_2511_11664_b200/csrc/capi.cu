@@ -957,7 +957,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         acap = std::max(acap, hi[b].alphabet);
         maxA = std::max<uint64_t>(maxA, hi[b].alphabet);
         nblk_cap = std::max(nblk_cap, hi[b].version == 2 ? hi[b].n_blocks : 1u);
-        Lmax = std::max<uint64_t>(Lmax, 2 * hi[b].nnz + hi[b].n_rows);
+        Lmax = std::max<uint64_t>(Lmax, (2 * hi[b].nnz + hi[b].n_rows + 15) & ~15ull);  // 16-byte rows
         nchunk_cap = std::max(nchunk_cap, ceil_div_u32(hi[b].n_rows, dec_chunk_rows(hi[b].n_cols, hi[b].sym_bytes, stage)));
         maxK = std::max(maxK, hi[b].n_cols);
         {   // which CSR-decode variants this batch needs (K 1 / 2 / 4 / other)
@@ -999,7 +999,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
                  ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
                  ctx->dstatus.as<int32_t>(), ctx->dlut.as<uint8_t>(), lut_stride,
-                 ctx->chunk_sum.as<unsigned long long>(), nchunk_cap};
+                 ctx->chunk_sum.as<unsigned long long>(), nchunk_cap, stage ? 0 : 1};
     CK(launch_pdl(k_dec_prepare, dim3(1 + lut_slices, B), 256, 0, s, dp));
     LAUNCHED("k_dec_prepare");
     RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<unsigned long long>(), nchunk_cap,

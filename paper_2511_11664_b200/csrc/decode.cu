@@ -29,7 +29,7 @@ __host__ __device__ inline uint32_t rows_per_chunk(uint32_t K) {
 // Rows per chunk of the decode pipeline's row kernels: u8 symbols with
 // K in {1, 2, 4} go to k_rows_small8 (SMALL_ROWS), everything else (and the
 // stage API) to the kernels chunked by rows_per_chunk.
-constexpr uint32_t SMALL_ROWS = 2048;
+constexpr uint32_t SMALL_ROWS = SMALL_ROWS_DEC;  // chunk sums from the v2 decoder
 __host__ __device__ inline uint32_t dec_chunk_rows(uint32_t K, uint32_t sym_bytes, bool stage) {
     return (!stage && sym_bytes == 1 && (K == 1 || K == 2 || K == 4)) ? SMALL_ROWS : rows_per_chunk(K);
 }
@@ -446,9 +446,23 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
     constexpr uint32_t MAXE = R * KK;  // nonzeros of a valid chunk
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
-    if (chunk_dead(p, b, chunk)) return;
+    // v2 tensors: the decoder summed every chunk's row counts (no look-back)
+    const bool sums = in.version == 2;
+    if (sums) {
+        if (*(const volatile int32_t*)(p.status + b) != SCZ_OK) return;
+    } else if (chunk_dead(p, b, chunk)) {
+        return;
+    }
     const uint64_t nnz = in.nnz;
     const uint8_t* d = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    __shared__ uint32_t s_base;
+    if (sums && threadIdx.x < 32) {  // prefix of the earlier chunks, issued before the staging
+        const unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
+        unsigned long long acc = 0;
+        for (uint32_t j = threadIdx.x; j < chunk; j += 32) acc += cs[j];
+        acc = warp_sum(acc);
+        if (threadIdx.x == 0) s_base = (uint32_t)min(acc, 0xFFFFFFFFull);
+    }
     __shared__ __align__(16) uint8_t s_r[R + 32];
     __shared__ __align__(16) uint8_t s_c[MAXE + 32];
     __shared__ __align__(16) uint8_t s_v[MAXE + 32];
@@ -473,9 +487,18 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
         sum += loc[j];
     }
     uint32_t tot;
-    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
+    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);  // (syncs: s_base visible)
     if (rbad) s_bad = 1;
-    const uint32_t cbase = block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
+    uint32_t cbase;
+    if (sums) {
+        cbase = s_base;
+        if (threadIdx.x == 0 &&
+            ((uint64_t)cbase + tot > nnz || (r0 + nrow == N && (uint64_t)cbase + tot != nnz)))  // sparse.py:84-87
+            s_bad = 1;
+        __syncthreads();
+    } else {
+        cbase = block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
+    }
     if (s_bad) {  // from here on tot <= nrow * KK and cbase + tot <= nnz
         if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
         return;

@@ -160,6 +160,10 @@ struct DecParams {
     uint64_t lut_stride;         // bytes per tensor
     unsigned long long* chunk_state;  // [B][nchunk_cap] CSR look-back words, zeroed here
     uint32_t nchunk_cap;
+    // 1: the v2 decoder adds the row counts of every SMALL_ROWS-row chunk of
+    // u8 tensors with K in {1, 2, 4} into chunk_state (k_rows_small8 reads
+    // the prefix instead of looking back)
+    int chunk_sums;
 };
 
 constexpr uint32_t LUT_SLICE = 2048;  // slots per k_dec_prepare slice CTA

@@ -12,6 +12,7 @@
 
 namespace scz {
 
+constexpr uint32_t SMALL_ROWS_DEC = 2048;  // == SMALL_ROWS (decode.cu)
 constexpr int DEC2_WPB = 16;         // warps (= blocks) per CTA, throughput mode
 constexpr int DEC2_WPB_SMALL = 4;    // latency mode (grid would not fill the GPU)
 constexpr int DCHUNK = 256;          // bytes per cp.async chunk (8 per lane)
@@ -155,6 +156,33 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
         if (full < steps) step(full * 32 + lane < len);  // partial last step
     }
     cp_async_wait<0>();
+    // Row-count sums per SMALL_ROWS-row chunk for k_rows_small8 (u8, K in
+    // {1, 2, 4}): the block's symbols in the r segment [2 nnz, 2 nnz + N)
+    // are re-read (just written by this warp) and added per chunk.
+    if (sizeof(S) == 1 && p.chunk_sums && (in.n_cols == 1 || in.n_cols == 2 || in.n_cols == 4)) {
+        const uint64_t r0 = 2 * in.nnz;
+        const uint64_t lo = max(base, r0), hi = base + len;
+        if (lo < hi) {
+            __syncwarp();  // every lane's symbol stores are visible to the warp
+            const uint8_t* d8 = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+            unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
+            for (uint64_t c = (lo - r0) / SMALL_ROWS_DEC; r0 + c * SMALL_ROWS_DEC < hi; ++c) {
+                const uint64_t a = max(lo, r0 + c * SMALL_ROWS_DEC);
+                const uint64_t e = min(hi, r0 + (c + 1) * SMALL_ROWS_DEC);
+                uint32_t acc = 0;
+                // aligned words covering [a, e), bytes outside masked off
+                for (uint64_t w = (a >> 2) + lane; w <= ((e - 1) >> 2); w += 32) {
+                    uint32_t v = reinterpret_cast<const uint32_t*>(d8)[w];
+                    const uint64_t wb = w << 2;
+                    if (wb < a) v &= 0xFFFFFFFFu << (8 * (uint32_t)(a - wb));
+                    if (wb + 4 > e) v &= 0xFFFFFFFFu >> (8 * (uint32_t)(wb + 4 - e));
+                    acc = __dp4a(v, 0x01010101u, acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0 && acc) atomicAdd(cs + c, (unsigned long long)acc);
+            }
+        }
+    }
     // rans.py:211-212: every lane back at L and every byte consumed
     const bool bad = __any_sync(0xffffffffu, x != STATE_LOW) || cur != end;
     if (bad && lane == 0) p.status[b] = SCZ_CORRUPT_STREAM;
