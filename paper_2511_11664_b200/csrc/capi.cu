@@ -655,6 +655,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
                            (size_t)B * MAX_CAND;
     zs.ptr[4] = sel_ticket;
     zs.words[4] = 1;
+    for (int r = 0; r < 5; ++r) zs.per[r] = ceil_div_u32(zs.words[r], pl.n_tiles);
 
     // K1+K2+K3: fused single-read front end when every tensor's tiles fit in
     // one co-resident grid (cooperative launch), else stats then quantise.
@@ -1042,23 +1043,26 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         } else {
             if constexpr (sizeof(S) <= 2) {
                 if (kmask & 1u) {
-                    if constexpr (sizeof(S) == 1)
-                        CK(launch_pdl(k_rows_small8<1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
-                    else
+                    if constexpr (sizeof(S) == 1) {
+                        if (any_v2) CK(launch_pdl(k_rows_small8<1, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v1) CK(launch_pdl(k_rows_small8<1, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    } else
                         CK(launch_pdl(k_rows_small<S, 1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 2u) {
-                    if constexpr (sizeof(S) == 1)
-                        CK(launch_pdl(k_rows_small8<2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
-                    else
+                    if constexpr (sizeof(S) == 1) {
+                        if (any_v2) CK(launch_pdl(k_rows_small8<2, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v1) CK(launch_pdl(k_rows_small8<2, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    } else
                         CK(launch_pdl(k_rows_small<S, 2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }
                 if (kmask & 4u) {
-                    if constexpr (sizeof(S) == 1)
-                        CK(launch_pdl(k_rows_small8<4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
-                    else
+                    if constexpr (sizeof(S) == 1) {
+                        if (any_v2) CK(launch_pdl(k_rows_small8<4, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v1) CK(launch_pdl(k_rows_small8<4, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                    } else
                         CK(launch_pdl(k_rows_small<S, 4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
                 }

@@ -434,8 +434,8 @@ __device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
 // a row costs a handful of instructions.  Consecutive threads own
 // consecutive rows: every store instruction of a warp is one contiguous,
 // coalesced span of 32 rows.  Checks as sparse.py:84-97.
-template <int KK>
-__global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
+template <int KK, bool SUMS>  // SUMS: v2 tensors (decoder chunk sums); else v1 (look-back)
+__global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowParams p) {
     static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
@@ -447,22 +447,15 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
     // v2 tensors: the decoder summed every chunk's row counts (no look-back)
-    const bool sums = in.version == 2;
-    if (sums) {
+    constexpr bool sums = SUMS;
+    if ((in.version == 2) != SUMS) return;  // the other variant's tensor
+    if constexpr (SUMS) {
         if (*(const volatile int32_t*)(p.status + b) != SCZ_OK) return;
     } else if (chunk_dead(p, b, chunk)) {
         return;
     }
     const uint64_t nnz = in.nnz;
     const uint8_t* d = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
-    __shared__ uint32_t s_base;
-    if (sums && threadIdx.x < 32) {  // prefix of the earlier chunks, issued before the staging
-        const unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
-        unsigned long long acc = 0;
-        for (uint32_t j = threadIdx.x; j < chunk; j += 32) acc += cs[j];
-        acc = warp_sum(acc);
-        if (threadIdx.x == 0) s_base = (uint32_t)min(acc, 0xFFFFFFFFull);
-    }
     __shared__ __align__(16) uint8_t s_r[R + 32];
     __shared__ __align__(16) uint8_t s_c[MAXE + 32];
     __shared__ __align__(16) uint8_t s_v[MAXE + 32];
@@ -470,30 +463,67 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
     __shared__ uint32_t s_scan[33];
     __shared__ float s_lut[256];
     __shared__ int s_bad;
+    __shared__ uint32_t s_base, s_own;
     const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
-    build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
     if (threadIdx.x == 0) s_bad = 0;
-    const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);
+    uint32_t cbase = 0, own = 0;
+    const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);  // in flight with the sums
+    if (sums) {
+        // chunk offset = sum of the earlier chunks' row counts, and this
+        // chunk's own count, both from the decoder: the r, c and v windows
+        // are then staged together (one memory round trip)
+        if (threadIdx.x < 32) {
+            const unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
+            const unsigned long long mine = threadIdx.x == 0 ? cs[chunk] : 0ull;
+            unsigned long long acc = 0;
+            for (uint32_t j0 = 0; j0 < chunk; j0 += 128) {  // four loads in flight per lane
+                unsigned long long v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t j = j0 + 32 * k + threadIdx.x;
+                    v[k] = j < chunk ? cs[j] : 0ull;
+                }
+                acc += (v[0] + v[1]) + (v[2] + v[3]);
+            }
+            acc = warp_sum(acc);
+            if (threadIdx.x == 0) {
+                s_base = (uint32_t)min(acc, 0xFFFFFFFFull);
+                s_own = (uint32_t)min(mine, 0xFFFFFFFFull);
+            }
+        }
+        build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
+        __syncthreads();
+        cbase = s_base;
+        own = s_own;
+        if (own > nrow * KK || (uint64_t)cbase + own > nnz) {  // uniform
+            if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+            return;
+        }
+    } else {
+        build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
+    }
+    uint32_t csh = 0, vsh = 0;
+    if (sums) {
+        csh = stage_window(s_c, d + nnz + cbase, own);
+        vsh = stage_window(s_v, d + cbase, own);
+    }
     __syncthreads();
-    // thread t sums rows [PER t, PER t + PER) of the chunk
-    uint32_t loc[PER], sum = 0;
+    // thread t sums rows [PER t, PER t + PER) of the chunk (re-read after
+    // the scan rather than held in registers)
+    uint32_t sum = 0;
     bool rbad = false;
 #pragma unroll
     for (uint32_t j = 0; j < PER; ++j) {
         const uint32_t i = threadIdx.x * PER + j;
         const uint32_t v = i < nrow ? (uint32_t)s_r[rsh + i] : 0u;
         rbad |= v > (uint32_t)KK;  // sparse.py:88-89
-        loc[j] = min(v, (uint32_t)KK + 1);
-        sum += loc[j];
+        sum += min(v, (uint32_t)KK + 1);
     }
     uint32_t tot;
-    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);  // (syncs: s_base visible)
+    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
     if (rbad) s_bad = 1;
-    uint32_t cbase;
     if (sums) {
-        cbase = s_base;
-        if (threadIdx.x == 0 &&
-            ((uint64_t)cbase + tot > nnz || (r0 + nrow == N && (uint64_t)cbase + tot != nnz)))  // sparse.py:84-87
+        if (threadIdx.x == 0 && (tot != own || (r0 + nrow == N && (uint64_t)cbase + tot != nnz)))  // sparse.py:84-87
             s_bad = 1;
         __syncthreads();
     } else {
@@ -505,16 +535,19 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
     }
 #pragma unroll
     for (uint32_t j = 0; j < PER; ++j) {
-        s_off[threadIdx.x * PER + j] = (uint16_t)ex;
-        ex += loc[j];
+        const uint32_t i = threadIdx.x * PER + j;
+        s_off[i] = (uint16_t)ex;
+        ex += i < nrow ? (uint32_t)s_r[rsh + i] : 0u;  // <= KK here (checked)
     }
-    const uint32_t csh = stage_window(s_c, d + nnz + cbase, tot);
-    const uint32_t vsh = stage_window(s_v, d + cbase, tot);
+    if (!sums) {  // look-back path: the windows are known only now
+        csh = stage_window(s_c, d + nnz + cbase, tot);
+        vsh = stage_window(s_v, d + cbase, tot);
+    }
     __syncthreads();
     float* orow0 = p.out + p.out_off[b] + r0 * KK;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
     bool bad = false;
-#pragma unroll 2
+#pragma unroll 1
     for (uint32_t j = 0; j < PER; ++j) {
         const uint32_t li = j * ROW_THREADS + threadIdx.x;
         if (li >= nrow) break;
@@ -552,9 +585,12 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small8(RowParams p) {
     __syncthreads();
     if (threadIdx.x == 0 && s_bad) p.status[b] = SCZ_CORRUPT_STREAM;
 }
-template __global__ void k_rows_small8<1>(RowParams);
-template __global__ void k_rows_small8<2>(RowParams);
-template __global__ void k_rows_small8<4>(RowParams);
+template __global__ void k_rows_small8<1, true>(RowParams);
+template __global__ void k_rows_small8<2, true>(RowParams);
+template __global__ void k_rows_small8<4, true>(RowParams);
+template __global__ void k_rows_small8<1, false>(RowParams);
+template __global__ void k_rows_small8<2, false>(RowParams);
+template __global__ void k_rows_small8<4, false>(RowParams);
 
 #define SCZ_INST_SMALL(S)                                      \
     template __global__ void k_rows_small<S, 1>(RowParams);    \

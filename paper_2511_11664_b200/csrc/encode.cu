@@ -20,6 +20,7 @@ namespace scz {
 struct ZeroSpec {
     uint32_t* ptr[5];
     uint32_t words[5];
+    uint32_t per[5];  // words per tile CTA: ceil(words / n_tiles)
 };
 
 struct StatsParams {
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
         if (!p.zero.ptr[r]) continue;
-        const uint32_t w = p.zero.words[r], per = (w + p.n_tiles - 1) / p.n_tiles;
+        const uint32_t w = p.zero.words[r], per = p.zero.per[r];
         uint32_t* z = p.zero.ptr[r] + (uint64_t)b * w;
         const uint32_t i1 = min(w, (tile + 1) * per);
         for (uint32_t i = tile * per + threadIdx.x; i < i1; i += TILE_THREADS) z[i] = 0u;
@@ -148,43 +149,53 @@ __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
         s_bad[warp] = bad;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; ++w) {
-            mn = fminf(mn, s_mn[w]);
-            mx = fmaxf(mx, s_mx[w]);
-            nnz += s_nnz[w];
-            bad |= s_bad[w];
-        }
+    // warp 0 alone publishes the tile, takes the ticket and, in the tensor's
+    // last CTA, reduces all tiles: the other warps retire right away
+    if (warp != 0) return;
+    mn = lane < 8 ? s_mn[lane] : INFINITY;
+    mx = lane < 8 ? s_mx[lane] : -INFINITY;
+    nnz = lane < 8 ? s_nnz[lane] : 0u;
+    bad = lane < 8 ? s_bad[lane] : 0u;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    uint32_t last = 0;
+    if (lane == 0) {
         p.tile_stats[(uint64_t)b * p.n_tiles + tile] =
             make_float4(mn, mx, __uint_as_float(nnz), __uint_as_float(bad));
         __threadfence();
-        uint32_t t = atomicAdd(&p.state[b].tiles_done, 1u);
-        s_last = (t == p.n_tiles - 1);
+        last = atomicAdd(&p.state[b].tiles_done, 1u) == p.n_tiles - 1;
     }
-    __syncthreads();
-    if (!s_last) return;
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
     __threadfence();
 
-    // ---- last CTA of tensor b: reduce tiles, scan nnz, compute params ----
-    __shared__ uint32_t s_scan[33];
+    // ---- last CTA of tensor b (warp 0): reduce tiles, scan nnz, params ----
     const float4* ts = p.tile_stats + (uint64_t)b * p.n_tiles;
     uint32_t* toff = p.tile_off + (uint64_t)b * p.n_tiles;
     float gmn = INFINITY, gmx = -INFINITY;
     uint32_t gbad = 0, carry = 0;
-    for (uint32_t base = 0; base < p.n_tiles; base += TILE_THREADS) {
-        uint32_t i = base + threadIdx.x;
+    for (uint32_t base = 0; base < p.n_tiles; base += 32) {
+        const uint32_t i = base + lane;
         uint32_t c = 0;
         if (i < p.n_tiles) {
-            float4 s = __ldcg(ts + i);
-            gmn = fminf(gmn, s.x);
-            gmx = fmaxf(gmx, s.y);
-            c = __float_as_uint(s.z);
-            gbad |= __float_as_uint(s.w);
+            const float4 t4 = __ldcg(ts + i);
+            gmn = fminf(gmn, t4.x);
+            gmx = fmaxf(gmx, t4.y);
+            c = __float_as_uint(t4.z);
+            gbad |= __float_as_uint(t4.w);
         }
-        uint32_t tot;
-        uint32_t ex = block_exclusive_scan<TILE_THREADS>(c, s_scan, &tot);
-        if (i < p.n_tiles) toff[i] = carry + ex;
-        carry += tot;
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        if (i < p.n_tiles) toff[i] = carry + inc - c;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -193,17 +204,6 @@ __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
         gbad |= __shfl_xor_sync(0xffffffffu, gbad, o);
     }
     if (lane == 0) {
-        s_mn[warp] = gmn;
-        s_mx[warp] = gmx;
-        s_bad[warp] = gbad;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; ++w) {
-            gmn = fminf(gmn, s_mn[w]);
-            gmx = fmaxf(gmx, s_mx[w]);
-            gbad |= s_bad[w];
-        }
         TensorState& st = p.state[b];
         st.xmin = gmn;
         st.xmax = gmx;
@@ -290,10 +290,10 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     __shared__ uint32_t s_wpre[TILE_WORDS];
     __shared__ uint32_t s_wbits[TILE_WORDS];
     __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_hist[4][256];  // one copy per warp pair: less atomic contention
+    __shared__ uint32_t s_hist[8][256];  // one copy per warp: no inter-warp atomic contention
     __shared__ __align__(16) uint8_t s_v[TILE + 32];  // the tile's value symbols, rank order
     const int nbins = 1 << p.q_bits;
-    for (int i = threadIdx.x; i < 4 * 256; i += TILE_THREADS) (&s_hist[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < 8 * 256; i += TILE_THREADS) (&s_hist[0][0])[i] = 0;
     // all eight 16-byte loads in flight first
     float4 vv[8];
     uint32_t vvalid[8];
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
             slow |= (uint32_t)(!ok && ((vvalid[it] >> j) & 1u)) << (4 * it + j);
             if (nz) {
                 s_v[rank] = (uint8_t)q;
-                if (ok) atomicAdd(&s_hist[warp & 3][q], 1u);
+                if (ok) atomicAdd(&s_hist[warp][q], 1u);
             }
             if constexpr (SYM_OUT)
                 if ((vvalid[it] >> j) & 1u)
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
         const uint32_t q = quant_exact(xb[tile_base + off], scale, zf, (double)qmax);
         if ((wbits >> bit) & 1u) {
             s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
-            atomicAdd(&s_hist[warp & 3][q], 1u);
+            atomicAdd(&s_hist[warp][q], 1u);
         }
         if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + tile_base + off] = q;
     }
@@ -366,7 +366,8 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     block_copy_s2g<TILE_THREADS>(v8 + base_rank, s_v, tot);
     uint32_t* gh = p.vhist + (uint64_t)b * 256;
     for (int i = threadIdx.x; i < nbins; i += TILE_THREADS) {
-        const uint32_t t = s_hist[0][i] + s_hist[1][i] + s_hist[2][i] + s_hist[3][i];
+        const uint32_t t = (s_hist[0][i] + s_hist[1][i]) + (s_hist[2][i] + s_hist[3][i]) +
+                           (s_hist[4][i] + s_hist[5][i]) + (s_hist[6][i] + s_hist[7][i]);
         if (t) atomicAdd(gh + i, t);
     }
 }
