@@ -711,48 +711,62 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         CK(launch_pdl(k_colhist, g, 128, 0, s, cp));
         LAUNCHED("k_colhist");
 
+    }
+    // Lazy search: the first pass prices the NA_FIRST candidates with the
+    // smallest K (the scan usually stops among them); the rest are priced
+    // only for tensors whose scan did not stop (sel_pending).
+    constexpr uint32_t NA_FIRST = 5;
+    const bool split = pl.searching && !cand_out && pl.acap <= SEL_WARP_ACAP && ncand > NA_FIRST;
+    const uint32_t n_first = split ? NA_FIRST : ncand;
+    // row-count histograms (+ column folds) of candidates [c0, c1)
+    auto rowhist_pass = [&](uint32_t c0, uint32_t c1, bool pending_only) -> int {
+        if (!need_hist) return SCZ_OK;
         RowHist2Params rp;
         memset(&rp, 0, sizeof rp);
         rp.bitmap = ctx->bitmap.as<uint32_t>();
         rp.words_pad = pl.words_pad;
         rp.n_words = ceil_div_u32(T, 32);
-        rp.n_cand = ncand;
+        rp.n_cand = c1 - c0;
+        rp.state = ctx->state.as<TensorState>();
+        rp.pending_only = pending_only ? 1 : 0;
         uint32_t chunks = 0, maxbins = 0;
         // chunk sizes: 16 words / 32 rows per thread, shrunk for small batches
         // until the grid covers the GPU twice
         for (uint32_t div = 1;; div *= 2) {
             chunks = 0;
             maxbins = 0;
-            for (uint32_t c = 0; c < ncand; ++c) {
+            for (uint32_t i = 0; i < c1 - c0; ++i) {
+                const uint32_t c = c0 + i;
                 uint32_t K = (uint32_t)(T / pl.rows[c]);
-                rp.cand_k[c] = K;
-                rp.cand_rows[c] = (uint32_t)pl.rows[c];
-                rp.rhist_off[c] = rh_off[c];
-                rp.chunk_start[c] = chunks;
+                rp.cand_k[i] = K;
+                rp.cand_rows[i] = (uint32_t)pl.rows[c];
+                rp.rhist_off[i] = rh_off[c];
+                rp.chunk_start[i] = chunks;
                 if (K == 2 || K == 4 || K == 8) {
-                    rp.units_per_chunk[c] = RH_THREADS * 16 / div;  // bitmap words
-                    chunks += ceil_div_u32(rp.n_words, rp.units_per_chunk[c]);
+                    rp.units_per_chunk[i] = RH_THREADS * 16 / div;  // bitmap words
+                    chunks += ceil_div_u32(rp.n_words, rp.units_per_chunk[i]);
                 } else if (K > 1) {
-                    rp.units_per_chunk[c] = RH_THREADS * 32 / div;  // rows
-                    chunks += ceil_div_u32(pl.rows[c], rp.units_per_chunk[c]);
+                    rp.units_per_chunk[i] = RH_THREADS * 32 / div;  // rows
+                    chunks += ceil_div_u32(pl.rows[c], rp.units_per_chunk[i]);
                     if (K + 1 > RH_PRIV_BINS) maxbins = std::max(maxbins, K + 1);
                 }
             }
             if ((uint64_t)chunks * B >= 2ull * ctx->num_sms || div >= 16) break;
         }
-        rp.chunk_start[ncand] = chunks;
+        rp.chunk_start[c1 - c0] = chunks;
         rp.rhist = ctx->rhist.as<uint32_t>();
         rp.rhist_stride = (uint32_t)rh_total;
         rp.hp = ctx->hp.as<uint32_t>();
         rp.hp_stride = (uint32_t)pl.period;
         rp.period = (uint32_t)pl.period;
         rp.fold_start = chunks;  // + one column-fold CTA per candidate
-        {
-            size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
-            CK(launch_pdl(k_rowhist2, dim3(chunks + ncand, B), RH_THREADS, smem, s, rp));
-            LAUNCHED("k_rowhist");
-        }
-    }
+        size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
+        CK(launch_pdl(k_rowhist2, dim3(chunks + (c1 - c0), B), RH_THREADS, smem, s, rp));
+        LAUNCHED("k_rowhist");
+        return SCZ_OK;
+    };
+    int rst = rowhist_pass(0, n_first, false);
+    if (rst != SCZ_OK) return rst;
 
     SelectParams sel;
     memset(&sel, 0, sizeof sel);
@@ -786,11 +800,11 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     if (pl.searching && pl.acap <= SEL_WARP_ACAP) {
         // small batches: spread the candidates over several CTAs per tensor
         const uint32_t per_cta = SEL_THREADS / 32;
-        const uint32_t want = ceil_div_u32(ncand, per_cta);
+        const uint32_t want = ceil_div_u32(n_first, per_cta);
         const uint32_t room = std::max<uint32_t>(1, (uint32_t)(2 * ctx->num_sms) / B);
         sel.groups = std::max<uint32_t>(1, std::min(want, room));
     }
-    if (sel.groups > 1) {  // (the tickets were zeroed by k_stats)
+    {   // (the tickets were zeroed by k_stats)
         sel.gcost = ctx->selbuf.as<double>();
         sel.gacnt = reinterpret_cast<uint32_t*>(sel.gcost + (size_t)B * MAX_CAND * 2);
         sel.ticket = sel_ticket;
@@ -804,8 +818,22 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         CK(cudaMemsetAsync(ctx->probe.p, 0, (size_t)B * sel.groups * 16 * 8, s));
         sel.probe = ctx->probe.as<unsigned long long>();
     }
+    sel.pass = split ? 1 : 0;
+    sel.c_begin = 0;
+    sel.c_end = n_first;
     CK(launch_pdl(k_select, dim3(sel.groups, B), SEL_THREADS, sel_smem, s, sel));
     LAUNCHED("k_select");
+    if (split) {  // the rest of the candidates, pending tensors only
+        if ((rst = rowhist_pass(n_first, ncand, true)) != SCZ_OK) return rst;
+        SelectParams sel2 = sel;
+        sel2.pass = 2;
+        sel2.c_begin = n_first;
+        sel2.c_end = ncand;
+        const uint32_t room = std::max<uint32_t>(1, (uint32_t)(2 * ctx->num_sms) / B);
+        sel2.groups = std::max<uint32_t>(1, std::min(ceil_div_u32(ncand - n_first, SEL_THREADS / 32), room));
+        CK(launch_pdl(k_select, dim3(sel2.groups, B), SEL_THREADS, sel_smem, s, sel2));
+        LAUNCHED("k_select/2");
+    }
     if (probe) {
         std::vector<unsigned long long> h((size_t)B * sel.groups * 16);
         CK(cudaMemcpyAsync(h.data(), sel.probe, h.size() * 8, cudaMemcpyDeviceToHost, s));

@@ -45,6 +45,7 @@ struct TensorState {
     uint32_t n_blocks;
     uint32_t sym_bytes;    // width of the c/r symbols of the chosen K (1, 2, 4)
     uint32_t errbits;      // encoder flags (ERR_OVERFLOW | ERR_UNCODABLE)
+    uint32_t sel_pending;  // lazy search: the first pass did not stop, price the rest
 };
 
 struct EncTab {  // per-symbol encoder table entry (16 B)

@@ -38,6 +38,8 @@ struct RowHist2Params {
     const uint32_t* hp;                // [B][hp_stride] nonzeros per (p mod P)
     uint32_t hp_stride, period;
     uint32_t fold_start;               // chunks >= fold_start: fold CTA of candidate chunk - fold_start
+    const TensorState* state;          // pending_only: skip tensors whose search already stopped
+    int pending_only;
 };
 
 __device__ void fold_columns(const RowHist2Params& p, uint32_t b, uint32_t c) {
@@ -114,6 +116,7 @@ __device__ void rowhist_swar(const uint32_t* bm, uint32_t w0, uint32_t w1, uint3
 __global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__ RowHist2Params p) {
     pdl_wait();
     const uint32_t chunk = blockIdx.x, b = blockIdx.y;
+    if (p.pending_only && !p.state[b].sel_pending) return;
     if (chunk >= p.fold_start) {
         fold_columns(p, b, chunk - p.fold_start);
         return;

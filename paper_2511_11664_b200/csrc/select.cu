@@ -44,6 +44,13 @@ struct SelectParams {
     uint32_t* gacnt;            // [B][MAX_CAND] alphabet per candidate
     // SCZ_SELECT_PROBE=1: %globaltimer stamps per CTA (debug timeline)
     unsigned long long* probe;
+    // Lazy search (pass 1 / 2; 0 = everything in one pass): pass 1 prices
+    // candidates [0, c_end) and decides if the early-stopped scan stops among
+    // them, else flags sel_pending; pass 2 (pending tensors only) prices
+    // [c_begin, c_end) and replays the scan over all of them.  Every priced
+    // (entropy, cost, alphabet) is kept in gcost / gacnt between the passes.
+    uint32_t c_begin, c_end;
+    int pass;
 };
 __device__ __forceinline__ unsigned long long sel_timer() {
     unsigned long long t;
@@ -408,7 +415,8 @@ __device__ uint8_t* warp_parallel_costs(const SelectParams& p, uint32_t b, uint3
     const uint32_t nv = 1u << p.q_bits;
     const uint32_t* vh = s_vh;
     constexpr uint32_t NW = SEL_THREADS / 32;
-    for (uint32_t c = g * NW + warp; c < p.n_cand; c += NW * p.groups) {
+    const bool keep = p.groups > 1 || p.pass != 0;  // costs go to gcost for another CTA / pass
+    for (uint32_t c = p.c_begin + g * NW + warp; c < p.c_end; c += NW * p.groups) {
         const uint32_t K = p.cand_k[c], N = p.cand_n[c];
         const uint32_t ub = max(nv, K + 1);
         const uint32_t* rh = rhb + p.rhist_off[c];
@@ -444,7 +452,7 @@ __device__ uint8_t* warp_parallel_costs(const SelectParams& p, uint32_t b, uint3
         }
         if (lane == 0) {
             s.acnt[c] = A;
-            if (p.groups > 1) p.gacnt[(uint64_t)b * MAX_CAND + c] = A;
+            if (keep) p.gacnt[(uint64_t)b * MAX_CAND + c] = A;
         }
         // entropy over the positive counts in index order (rans.py:219-223)
         const uint64_t len = 2 * nnz + N;
@@ -474,7 +482,7 @@ __device__ uint8_t* warp_parallel_costs(const SelectParams& p, uint32_t b, uint3
             const double h = -pairwise_sum(terms, m);
             s.ents[c] = h;
             s.costs[c] = __dmul_rn((double)len, h);
-            if (p.groups > 1) {
+            if (keep) {
                 double* gc = p.gcost + ((uint64_t)b * MAX_CAND + c) * 2;
                 gc[0] = h;
                 gc[1] = s.costs[c];
@@ -490,14 +498,22 @@ __device__ uint8_t* warp_parallel_costs(const SelectParams& p, uint32_t b, uint3
 // Multi-CTA pricing: true in the CTA that arrives last for tensor b, which
 // then holds every candidate's (entropy, cost, alphabet) in `s`.
 __device__ bool gather_costs(const SelectParams& p, uint32_t b, BlockScratch& s) {
-    if (p.groups <= 1) return true;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s.alph[3] = atomicAdd(p.ticket + b, 1u) == p.groups - 1;
-    __syncthreads();
-    if (!s.alph[3]) return false;
-    __threadfence();
-    for (uint32_t c = threadIdx.x; c < p.n_cand; c += SEL_THREADS) {
+    if (p.groups > 1) {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s.alph[3] = atomicAdd(p.ticket + b, 1u) == p.groups - 1;
+            if (s.alph[3]) p.ticket[b] = 0;  // re-armed for the next pass
+        }
+        __syncthreads();
+        if (!s.alph[3]) return false;
+        __threadfence();
+    }
+    // from gcost: this pass's candidates when several CTAs priced them, and
+    // in pass 2 the first pass's candidates
+    const uint32_t lo = p.pass == 2 ? 0 : p.c_begin;
+    const uint32_t hi = p.groups > 1 ? p.c_end : (p.pass == 2 ? p.c_begin : 0);
+    for (uint32_t c = lo + threadIdx.x; c < hi; c += SEL_THREADS) {
         const volatile double* gc = p.gcost + ((uint64_t)b * MAX_CAND + c) * 2;
         s.ents[c] = gc[0];
         s.costs[c] = gc[1];
@@ -513,6 +529,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const __grid_constant__ 
     SEL_PROBE(0);
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
+    if (p.pass == 2 && !st.sel_pending) return;  // decided by the first pass
     __shared__ BlockScratch s;
     uint32_t* counts = p.counts + (uint64_t)b * p.acap;
     double* terms = p.terms + (uint64_t)b * p.acap;
@@ -549,7 +566,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const __grid_constant__ 
                 if (a == 0.0 && bb == 0.0) return false;
                 return fabs(a - bb) <= 1e-12 * fmax(fabs(a), fabs(bb));
             };
-            for (uint32_t c = 0; c < p.n_cand; ++c) {
+            for (uint32_t c = 0; c < p.c_end; ++c) {
                 double v = s.costs[c];
                 ++evaluated;
                 if (near(v, best) || near(v, prev)) flags |= SCZ_SEARCH_NEAR_TIE;
@@ -565,6 +582,9 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const __grid_constant__ 
             }
             if (stopped) flags |= SCZ_SEARCH_EARLY_STOPPED;
             flags |= SCZ_SEARCH_USED;
+            // first pass that did not stop among its candidates: price the rest
+            s.alph[4] = (p.pass == 1 && !stopped && p.c_end < p.n_cand) ? 1u : 0u;
+            if (p.pass == 1) st.sel_pending = s.alph[4];
             if (p.cand_out) {
                 double* co = p.cand_out + (uint64_t)b * MAX_CAND * 2;
                 for (uint32_t c = 0; c < p.n_cand; ++c) {
@@ -580,7 +600,9 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const __grid_constant__ 
         chosen = s.alph[0];
         flags = s.alph[1];
         evaluated = s.alph[2];
+        const bool pending = s.alph[4] != 0;
         __syncthreads();
+        if (pending) return;  // pass 2 decides
     }
     // chosen candidate: histogram -> normalised table -> encoder table
     uint32_t A;

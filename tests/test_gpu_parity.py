@@ -491,3 +491,20 @@ def test_chunked_host_batch_calls(tmp_path):
     env["SCZ_CHUNK_BYTES"] = str(3 * 32 * 28 * 28 * 4)  # 3 tensors per chunk -> 7 chunks
     out = subprocess.run([sys.executable, "-c", code % root], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_lazy_search_mixed_batch_vs_oracle():
+    """The search prices the first candidates in one pass and the rest only
+    for tensors whose early-stopped scan has not stopped yet (sel_pending):
+    a batch mixing shallow (sparsity 0.5: stops after 4 candidates) and deep
+    (0.9+: 10 or more) searches must give every tensor the reference's N and
+    container bytes."""
+    sp = [0.5, 0.92, 0.5, 0.95, 0.88, 0.3]
+    ts = [sz.gen_synthetic("relu-laplace", [1, 128, 28, 28], s, 700 + i) for i, s in enumerate(sp)]
+    many = container.compress_many(ts, 8, format=2, block_syms=2048)
+    depths = []
+    for t, c in zip(ts, many):
+        ref = orc.compress(t.data, t.dims, 8, None, 14, fmt=2, lanes=32, block_syms=2048)
+        assert container.to_bytes(c) == orc.to_bytes(ref)
+        depths.append(len(optimizer.search(t, 8)[1].candidates))
+    assert min(depths) <= 5 < max(depths), depths  # both passes exercised
