@@ -492,8 +492,10 @@ __device__ __forceinline__ void store_sym(void* base, uint64_t i, uint32_t v) {
     reinterpret_cast<S*>(base)[i] = (S)v;
 }
 
+// s_buf: TILE * 2 + 64 bytes of shared memory (u8: columns then row counts;
+// u16: columns), shared by the width instances of one kernel
 template <typename S>
-__device__ __forceinline__ void materialize_body(const MatParams& p) {
+__device__ __forceinline__ void materialize_body(const MatParams& p, uint8_t* s_buf) {
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
@@ -505,7 +507,7 @@ __device__ __forceinline__ void materialize_body(const MatParams& p) {
     __shared__ uint32_t s_scan[33];
     __shared__ uint32_t s_w[TILE_WORDS + 2];  // this tile's bitmap + the next two words
     __shared__ uint8_t s_mod[64];             // i mod K for i < 64 (K <= 32)
-    __shared__ S s_c[TILE];                   // column indices staged in rank order
+    S* s_c = reinterpret_cast<S*>(s_buf);     // column indices staged in rank order
     const uint64_t word = (uint64_t)tile * TILE_WORDS + threadIdx.x;
     uint32_t w = bm[word];
     s_w[threadIdx.x] = w;
@@ -527,20 +529,44 @@ __device__ __forceinline__ void materialize_body(const MatParams& p) {
         if (rr < 0) rr += K;
         if (rr >= K) rr -= K;
         const uint32_t m = (uint32_t)rr;
-        while (w) {
-            const int bit = __ffs(w) - 1;
-            w &= w - 1;
-            uint32_t c = m + bit;
-            c = (K <= 32) ? s_mod[c] : (c >= K ? c - K : c);
-            s_c[lrank++] = (S)c;
+        if ((K & (K - 1)) == 0 && K <= 32) {  // K | 32: m == 0, c = bit mod K
+            while (w) {
+                const int bit = __ffs(w) - 1;
+                w &= w - 1;
+                s_c[lrank++] = (S)(bit & (K - 1));
+            }
+        } else {
+            while (w) {
+                const int bit = __ffs(w) - 1;
+                w &= w - 1;
+                uint32_t c = m + bit;
+                c = (K <= 32) ? s_mod[c] : (c >= K ? c - K : c);
+                s_c[lrank++] = (S)c;
+            }
         }
+    }
+    // row counts for the rows starting in this tile (sparse.py:68)
+    const uint64_t ts = (uint64_t)tile * TILE, te = min(ts + TILE, p.total);
+    const uint64_t i0 = (ts + K - 1) / K, i1 = (te + K - 1) / K;
+    if (sizeof(S) == 1 && K <= 32) {
+        // u8: row counts staged too; c and r leave with 16-byte stores
+        uint8_t* s_rc = s_buf + TILE + 32;  // (u8 columns use the first TILE + 32 bytes)
+        const uint32_t kmask = K == 32 ? 0xffffffffu : ((1u << K) - 1u);
+        const uint32_t nr = (uint32_t)(i1 - i0);
+        for (uint32_t j = threadIdx.x; j < nr; j += TILE_THREADS) {
+            const uint32_t start = (uint32_t)((i0 + j) * K - ts);  // < TILE
+            const uint32_t wi = start >> 5, sh = start & 31;
+            s_rc[j] = (uint8_t)__popc(__funnelshift_r(s_w[wi], s_w[wi + 1], sh) & kmask);
+        }
+        __syncthreads();
+        block_copy_s2g<TILE_THREADS>(reinterpret_cast<uint8_t*>(cr + base_rank),
+                                     reinterpret_cast<const uint8_t*>(s_c), tot);
+        block_copy_s2g<TILE_THREADS>(reinterpret_cast<uint8_t*>(cr + nnz + i0), s_rc, nr);
+        return;
     }
     __syncthreads();
     S* dst = cr + base_rank;
     for (uint32_t i = threadIdx.x; i < tot; i += TILE_THREADS) dst[i] = s_c[i];  // coalesced
-    // row counts for the rows starting in this tile (sparse.py:68)
-    const uint64_t ts = (uint64_t)tile * TILE, te = min(ts + TILE, p.total);
-    const uint64_t i0 = (ts + K - 1) / K, i1 = (te + K - 1) / K;
     if (K <= 32) {
         const uint32_t kmask = K == 32 ? 0xffffffffu : ((1u << K) - 1u);
         for (uint64_t i = i0 + threadIdx.x; i < i1; i += TILE_THREADS) {
@@ -557,15 +583,17 @@ __device__ __forceinline__ void materialize_body(const MatParams& p) {
 template <typename S>
 __global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
     pdl_wait();
-    materialize_body<S>(p);
+    __shared__ __align__(16) uint8_t s_buf[TILE * (sizeof(S) < 2 ? 2 : sizeof(S)) + 64];
+    materialize_body<S>(p, s_buf);
 }
 
 // The pipeline's launch: u8 and u16 classes in one grid (see k_rans_enc_v2_u8u16).
-__global__ void __launch_bounds__(TILE_THREADS) k_materialize_u8u16(MatParams p8, MatParams p16) {
+__global__ void __launch_bounds__(TILE_THREADS, 6) k_materialize_u8u16(MatParams p8, MatParams p16) {
     pdl_wait();
+    __shared__ __align__(16) uint8_t s_buf[TILE * 2 + 64];
     const uint32_t w = p8.state[blockIdx.y].sym_bytes;
-    if (w == 2) materialize_body<uint16_t>(p16);
-    else if (w == 1) materialize_body<uint8_t>(p8);
+    if (w == 2) materialize_body<uint16_t>(p16, s_buf);
+    else if (w == 1) materialize_body<uint8_t>(p8, s_buf);
 }
 
 template __global__ void k_materialize<uint8_t>(MatParams);
