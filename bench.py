@@ -314,28 +314,72 @@ def run_ours(args):
         return float(t.item())
 
     # ---- device-resident timed region -------------------------------------
+    # Two library contexts (own stream + scratch each) alternate between
+    # steps: step i + 1's encode is queued before the host reads step i's
+    # headers (scz_batch_sync) and queues its decode, so the GPU never idles
+    # on the host round trip.  Every step still compresses and decompresses
+    # the whole batch; the timing is CUDA events on both streams.
+    ctxs = [ctx, _native.Context(local)]
+    streams = [stream, torch.cuda.ExternalStream(ctxs[1].stream, device=torch.device("cuda", local))]
+    batches = [_native.Batch(), _native.Batch()]
+    infos = [(_native.Info * B)(), (_native.Info * B)()]
+    outs = [out_dev, torch.empty_like(x_dev)]
+
+    def enc(k):
+        c = ctxs[k]
+        c.check(lib.scz_encode_batch(c.h, ctypes.c_void_p(x_dev.data_ptr()), T, B, wl["q"], -1, 14,
+                                     args.format, 32, args.block_syms, ctypes.byref(batches[k])))
+
+    def dec(k):
+        c = ctxs[k]
+        c.check(lib.scz_batch_sync(c.h, ctypes.byref(batches[k]), infos[k]))
+        c.check(lib.scz_decode_batch_async(c.h, infos[k], B, ctypes.c_void_p(batches[k].d_freqs),
+                                           ctypes.c_void_p(batches[k].d_block_bytes),
+                                           ctypes.c_void_p(batches[k].d_payload),
+                                           ctypes.c_void_p(outs[k].data_ptr())))
+
+    def pipelined(n, clocks=None):
+        enc(0)
+        for i in range(n):
+            if i + 1 < n:
+                enc((i + 1) % 2)
+            dec(i % 2)
+            if clocks:
+                clocks.sample()
+
+    for _ in range(max(1, args.warmup // 2)):
+        pipelined(2)  # every context's graphs captured
     for _ in range(args.warmup):
         device_step()
     barrier()
-    ctx.set_timing(True)
-    ctx.read_timing()
-    l0 = ctx.launches
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches + ctxs[1].launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     clocks = ClockSampler(local)
     with clocks:
         barrier()
-        ev0.record(stream)
-        for i in range(args.steps):
-            device_step()
-            clocks.sample()  # work of this step is still queued / running
-        ev1.record(stream)
+        ev0.record(streams[0])
+        streams[1].wait_event(ev0)
+        pipelined(args.steps, clocks)
+        for k in range(2):
+            ev_end[k].record(streams[k])
         barrier()
-    launches = ctx.launches - l0
-    kt = ctx.read_timing()
-    ctx.set_timing(False)
-    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = ctx.launches + ctxs[1].launches - l0
+    ms = max(ev0.elapsed_time(e) for e in ev_end) / args.steps
     ms = max_over_ranks(ms)
     value = 4.0 * T * B * world / (ms * 1e-3) / 1e9
+
+    # ---- per-kernel times (separate pass: per-launch events, no graphs) ----
+    ctx.set_timing(True)
+    ctx.read_timing()
+    for _ in range(3):
+        device_step()
+    torch.cuda.synchronize()
+    kt = ctx.read_timing()
+    ctx.set_timing(False)
+    device_step()  # outputs of the default context for the checks below
+    torch.cuda.synchronize()
+    kt_steps = 3
 
     status = (ctypes.c_int32 * B)()
     ctx.check(lib.scz_decode_status(ctx.h, B, status))
@@ -365,7 +409,7 @@ def run_ours(args):
         kernel_share = {k: round(v[0] / step_ms_sum, 4) for k, v in sorted(kt.items(), key=lambda kv: -kv[1][0])}
         name, (tot_ms, n) = dom
         per_launch_ms = tot_ms / n
-        launches_per_step = n / args.steps
+        launches_per_step = n / kt_steps
         ab = algorithmic_bytes(name, infos, T, None)
         achieved = (ab / launches_per_step) / (per_launch_ms * 1e-3) / 1e9 if ab else None
         traffic = None
