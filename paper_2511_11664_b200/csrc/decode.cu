@@ -466,6 +466,20 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
     __shared__ uint32_t s_base, s_own;
     const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
     if (threadIdx.x == 0) s_bad = 0;
+    // per column-presence mask: the sorted column packing and the PRMT
+    // selector that moves the k-th value byte to its column (4 = zero byte)
+    __shared__ uint32_t s_pk[1 << KK], s_sel[1 << KK];
+    if (threadIdx.x < (1u << KK)) {
+        uint32_t pk = 0, sel = 0, k = 0;
+        for (uint32_t j = 0; j < 4; ++j) {
+            const bool here = j < (uint32_t)KK && ((threadIdx.x >> j) & 1u);
+            if (here) pk |= j << (8 * k);
+            sel |= (here ? k : 4u) << (4 * j);
+            k += here;
+        }
+        s_pk[threadIdx.x] = pk;
+        s_sel[threadIdx.x] = sel;
+    }
     uint32_t cbase = 0, own = 0;
     const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);  // in flight with the sums
     if (sums) {
@@ -554,20 +568,20 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
         const uint32_t off = s_off[li], r = s_r[rsh + li];
         const uint32_t cw = smem_word_at(s_c, csh + off);  // bytes past r are ignored
         const uint32_t vw = smem_word_at(s_v, vsh + off);
-        uint32_t mask = 0, prev = 0;
+        // column-presence mask of the row; a row is valid (sparse.py:90-97:
+        // columns < K, strictly increasing) iff its live column bytes equal
+        // the sorted packing of its mask and the mask has r bits
+        uint32_t mask = 0;
 #pragma unroll
-        for (int e = 0; e < KK; ++e) {
-            const uint32_t c = (cw >> (8 * e)) & 0xFFu;
-            const bool live = (uint32_t)e < r;
-            bad |= live & ((c >= (uint32_t)KK) | ((e > 0) & (c <= prev)));  // sparse.py:90-97
-            mask |= live ? (1u << (c & (KK - 1))) : 0u;
-            prev = c;
-        }
+        for (int e = 0; e < KK; ++e) mask |= (uint32_t)((uint32_t)e < r) << ((cw >> (8 * e)) & (KK - 1));
+        const uint32_t live = r >= 4 ? 0xFFFFFFFFu : ((1u << (8 * r)) - 1u);
+        bad |= ((cw & live) != s_pk[mask]) | ((uint32_t)__popc(mask) != r);
+        // value byte of every present column in column order (PRMT), 0 elsewhere
+        const uint32_t vs = __byte_perm(vw, 0u, s_sel[mask]);
         float o[KK];
 #pragma unroll
         for (int col = 0; col < KK; ++col) {
-            const uint32_t k = __popc(mask & ((1u << col) - 1u));  // entries left of col
-            const float val = s_lut[(vw >> (8 * k)) & 0xFFu];
+            const float val = s_lut[(vs >> (8 * col)) & 0xFFu];
             o[col] = (mask >> col) & 1u ? val : 0.0f;
         }
         float* orow = orow0 + (uint64_t)li * KK;

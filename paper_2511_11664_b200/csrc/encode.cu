@@ -294,12 +294,14 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     __shared__ __align__(16) uint8_t s_v[TILE + 32];  // the tile's value symbols, rank order
     const int nbins = 1 << p.q_bits;
     for (int i = threadIdx.x; i < 8 * 256; i += TILE_THREADS) (&s_hist[0][0])[i] = 0;
-    // all eight 16-byte loads in flight first
+    // all eight 16-byte loads in flight first (out-of-range lanes read 0:
+    // their bitmap bits are 0 and the exact path re-checks the index)
     float4 vv[8];
-    uint32_t vvalid[8];
 #pragma unroll
-    for (int it = 0; it < 8; ++it)
-        vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &vvalid[it]);
+    for (int it = 0; it < 8; ++it) {
+        uint32_t valid;
+        vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &valid);
+    }
     uint32_t myword = bm[threadIdx.x];
     s_wbits[threadIdx.x] = myword;
     uint32_t tot;
@@ -314,10 +316,10 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     uint8_t* v8 = p.v8 + (uint64_t)b * p.v8_stride;
 
     // Branch-free over all 32 elements of the thread: the fp32 estimate for
-    // every element, the store and the histogram count predicated on the
-    // element's bitmap bit; elements near a rounding boundary (or every
-    // element when the scale is out of the fp32 range) are collected in
-    // `slow` and redone with the exact fp64 sequence afterwards.
+    // every element and a store predicated on its bitmap bit; elements near a
+    // rounding boundary (or every element when the scale is out of the fp32
+    // range) are collected in `slow` and redone with the exact fp64 sequence
+    // afterwards.  The histogram is taken from the staged symbols.
     uint32_t slow = 0;  // bit 4 * it + j: element needs the exact path
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
@@ -330,19 +332,20 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
         uint32_t rank = s_wpre[word] + __popc(wbits & ((1u << bit0) - 1u));  // tile-local
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+            // rint via the 1.5 * 2^23 magic constant (|y| < 2^22 whenever
+            // `fast`): full-rate FADDs instead of FRND / F2I conversions
             const float y = fmaf(e[j], r32, zf32);
-            const float rq = rintf(y);
-            const bool ok = fast && fabsf(y - rq) < 0.5f - 0x1p-12f;
-            const uint32_t q = (uint32_t)min(max((int)rq, 0), qmax);
+            const float t = __fadd_rn(y, 0x1.8p23f);
+            const float rq = __fsub_rn(t, 0x1.8p23f);
+            const bool ok = fast && fabsf(__fsub_rn(y, rq)) < 0.5f - 0x1p-12f;
+            const uint32_t q = (uint32_t)min(max(__float_as_int(t) - 0x4B400000, 0), qmax);
             const bool nz = (nib >> j) & 1u;
-            slow |= (uint32_t)(!ok && ((vvalid[it] >> j) & 1u)) << (4 * it + j);
-            if (nz) {
-                s_v[rank] = (uint8_t)q;
-                if (ok) atomicAdd(&s_hist[warp][q], 1u);
+            slow |= (uint32_t)!ok << (4 * it + j);
+            if (nz) s_v[rank] = (uint8_t)q;
+            if constexpr (SYM_OUT) {
+                const uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4 + j;
+                if (idx < p.total) p.sym_out[(uint64_t)b * p.total + idx] = q;
             }
-            if constexpr (SYM_OUT)
-                if ((vvalid[it] >> j) & 1u)
-                    p.sym_out[(uint64_t)b * p.total + tile_base + warp * 1024 + it * 128 + lane * 4 + j] = q;
             rank += nz;
         }
     }
@@ -351,15 +354,22 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
         slow &= slow - 1;
         const int it = k >> 2, j = k & 3;
         const uint32_t off = warp * 1024 + it * 128 + lane * 4 + j;
+        if (tile_base + off >= p.total) continue;
         const int word = warp * 32 + it * 4 + (lane >> 3);
         const int bit = 4 * (lane & 7) + j;
         const uint32_t wbits = s_wbits[word];
         const uint32_t q = quant_exact(xb[tile_base + off], scale, zf, (double)qmax);
-        if ((wbits >> bit) & 1u) {
-            s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
-            atomicAdd(&s_hist[warp][q], 1u);
-        }
+        if ((wbits >> bit) & 1u) s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
         if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + tile_base + off] = q;
+    }
+    __syncthreads();
+    // value histogram of the tile's symbols (per-warp copies)
+    for (uint32_t i = 4 * threadIdx.x; i < tot; i += 4 * TILE_THREADS) {
+        const uint32_t w4 = *reinterpret_cast<const uint32_t*>(s_v + i);
+        const uint32_t n4 = min(4u, tot - i);
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k)
+            if (k < n4) atomicAdd(&s_hist[warp][(w4 >> (8 * k)) & 0xFFu], 1u);
     }
     __syncthreads();
     // the tile's values go out with coalesced 16-byte stores
