@@ -109,27 +109,53 @@ __global__ void __launch_bounds__(TILE_THREADS) k_stats(StatsParams p) {
         const uint32_t i1 = min(w, (tile + 1) * per);
         for (uint32_t i = tile * per + threadIdx.x; i < i1; i += TILE_THREADS) z[i] = 0u;
     }
+    if (aligned && tile_base + TILE <= p.total) {
+        // full tile (all but a tensor's last): no per-element validity; a
+        // non-finite element turns acc = sum of e * 0 into NaN (one FMA per
+        // element instead of a compare and a select)
+        float acc = 0.0f;
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
-        const uint32_t valid = vvalid[it];
-        const float4 v = vv[it];
-        float e[4] = {v.x, v.y, v.z, v.w};
-        uint32_t nib = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (valid >> j & 1) {
-                if (!isfinite(e[j])) bad = 1;
-                mn = fminf(mn, e[j]);
-                mx = fmaxf(mx, e[j]);
-                nib |= (uint32_t)(e[j] != 0.0f) << j;
-            }
+        for (int it = 0; it < 8; ++it) {
+            const float4 v = vv[it];
+            mn = fminf(mn, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+            mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+            acc = __fmaf_rn(v.x, 0.0f, acc);
+            acc = __fmaf_rn(v.y, 0.0f, acc);
+            acc = __fmaf_rn(v.z, 0.0f, acc);
+            acc = __fmaf_rn(v.w, 0.0f, acc);
+            const uint32_t nib = (uint32_t)(v.x != 0.0f) | ((uint32_t)(v.y != 0.0f) << 1) |
+                                 ((uint32_t)(v.z != 0.0f) << 2) | ((uint32_t)(v.w != 0.0f) << 3);
+            nnz += __popc(nib);
+            uint32_t w = nib << (4 * (lane & 7));
+            w |= __shfl_xor_sync(0xffffffffu, w, 1);
+            w |= __shfl_xor_sync(0xffffffffu, w, 2);
+            w |= __shfl_xor_sync(0xffffffffu, w, 4);
+            if ((lane & 7) == 0) bm[warp * 32 + it * 4 + (lane >> 3)] = w;
         }
-        nnz += __popc(nib);
-        uint32_t w = nib << (4 * (lane & 7));
-        w |= __shfl_xor_sync(0xffffffffu, w, 1);
-        w |= __shfl_xor_sync(0xffffffffu, w, 2);
-        w |= __shfl_xor_sync(0xffffffffu, w, 4);
-        if ((lane & 7) == 0) bm[warp * 32 + it * 4 + (lane >> 3)] = w;
+        bad = acc != acc;
+    } else {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            const uint32_t valid = vvalid[it];
+            const float4 v = vv[it];
+            float e[4] = {v.x, v.y, v.z, v.w};
+            uint32_t nib = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (valid >> j & 1) {
+                    if (!isfinite(e[j])) bad = 1;
+                    mn = fminf(mn, e[j]);
+                    mx = fmaxf(mx, e[j]);
+                    nib |= (uint32_t)(e[j] != 0.0f) << j;
+                }
+            }
+            nnz += __popc(nib);
+            uint32_t w = nib << (4 * (lane & 7));
+            w |= __shfl_xor_sync(0xffffffffu, w, 1);
+            w |= __shfl_xor_sync(0xffffffffu, w, 2);
+            w |= __shfl_xor_sync(0xffffffffu, w, 4);
+            if ((lane & 7) == 0) bm[warp * 32 + it * 4 + (lane >> 3)] = w;
+        }
     }
     // block reduce
 #pragma unroll
