@@ -318,16 +318,20 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
                         enc_apply_ring(E, t, act, gtm, ob);
                         --s;
                     }
-                    if (s >= lo) {
-                        t = s_tab[rs[(s & 31) * 32]];
-#pragma unroll 4
-                        for (; s > lo; --s) {
-                            const EncTab tn = s_tab[rs[((s - 1) & 31) * 32]];
-                            enc_apply_ring(E, t, true, gtm, ob);
-                            t = tn;
-                        }
-                        enc_apply_ring(E, t, true, gtm, ob);
+                    // groups of four steps: the four table entries are loaded
+                    // up front (symbols do not depend on the state)
+#pragma unroll 1
+                    for (; s - 3 >= lo; s -= 4) {
+                        const EncTab t0 = s_tab[rs[(s & 31) * 32]];
+                        const EncTab t1 = s_tab[rs[((s - 1) & 31) * 32]];
+                        const EncTab t2 = s_tab[rs[((s - 2) & 31) * 32]];
+                        const EncTab t3 = s_tab[rs[((s - 3) & 31) * 32]];
+                        enc_apply_ring(E, t0, true, gtm, ob);
+                        enc_apply_ring(E, t1, true, gtm, ob);
+                        enc_apply_ring(E, t2, true, gtm, ob);
+                        enc_apply_ring(E, t3, true, gtm, ob);
                     }
+                    for (; s >= lo; --s) enc_apply_ring(E, s_tab[rs[(s & 31) * 32]], true, gtm, ob);
                     __syncwarp();
                     flush();
                 }
