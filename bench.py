@@ -236,6 +236,20 @@ class ClockSampler:
                     source="NVML, polled every ~2 ms during the timed region")
 
 
+def gpu_local_cpus(torch, device):
+    """CPUs NVML reports as local to `device` (empty set if unknown)."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda._get_nvml_device_index(device))
+        n = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        return {i for i in range(n) if (words[i // 64] >> (i % 64)) & 1}
+    except Exception:
+        return set()
+
+
 # -------------------------------------------------------------- our arm
 def algorithmic_bytes(name, infos, T, nblk_bytes):
     """Bytes a kernel must move per launch, batch-summed."""
@@ -275,6 +289,14 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2511_11664_b200 import _native
+
+    # Host threads (and the pinned buffers they touch first) on the GPU's own
+    # NUMA node: the e2e path is PCIe-bound, and DMA to far-socket memory
+    # crosses the inter-socket link.  The CPU baseline gets all cores back.
+    all_cpus = os.sched_getaffinity(0)
+    near = gpu_local_cpus(torch, local) & all_cpus
+    if near:
+        os.sched_setaffinity(0, near)
 
     wl = WORKLOADS[args.workload]
     T = int(np.prod(wl["dims"]))
@@ -445,7 +467,8 @@ def run_ours(args):
                    d2h_bytes_per_step=io["d2h"], ms_per_step=e2e_ms, stage_ms=io["stage_ms"],
                    path="scz_compress_batch + scz_decompress_batch, pinned host buffers",
                    schedule="2-stage pipeline: decompress(step i) || compress(step i+1)",
-                   timing="host clock between decompress completions in steady state")
+                   timing="host clock between decompress completions in steady state",
+                   host_cpus=f"{len(near)} GPU-local CPUs (NVML affinity)" if near else "unrestricted")
 
     extras = {}
     if not args.no_extras and rank == 0:
@@ -453,6 +476,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.sched_setaffinity(0, all_cpus)
         cpu, _ = cpu_baseline(args.workload, args.cpu_seconds)
 
     if rank == 0:
