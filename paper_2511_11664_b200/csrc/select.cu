@@ -457,25 +457,19 @@ __device__ uint8_t* warp_parallel_costs(const SelectParams& p, uint32_t b, uint3
         // entropy over the positive counts in index order (rans.py:219-223)
         const uint64_t len = 2 * nnz + N;
         const double total = (double)len;
-        // two rounds of 4 independent divisions / logarithms per lane (ILP)
+        // one division + logarithm per lane per 32 symbols; kept compact
+        // (not unrolled, log2 out of line): at small batches this kernel runs
+        // once per tensor and instruction-cache misses, not arithmetic, set
+        // its latency
         uint32_t m = 0;
-        for (uint32_t base = 0; base < A; base += 128) {
-            double pp[4];
-            uint32_t pos[4];
-            bool has[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t i = base + 32 * u + lane;
-                const uint32_t cnt = i < A ? cb[i] : 0;
-                const uint32_t bal = __ballot_sync(0xffffffffu, cnt > 0);
-                has[u] = cnt > 0;
-                pos[u] = m + __popc(bal & lanemask_lt());
-                m += __popc(bal);
-                pp[u] = __ddiv_rn((double)(cnt | !has[u]), total);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (has[u]) terms[pos[u]] = __dmul_rn(pp[u], log2(pp[u]));
+#pragma unroll 1
+        for (uint32_t i0 = 0; i0 < A; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const uint32_t cnt = i < A ? cb[i] : 0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, cnt > 0);
+            const uint32_t pos = m + __popc(bal & lanemask_lt());
+            m += __popc(bal);
+            if (cnt > 0) terms[pos] = plog2p(__ddiv_rn((double)cnt, total));
         }
         __syncwarp();
         if (lane == 0) {
