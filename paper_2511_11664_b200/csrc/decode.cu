@@ -435,7 +435,7 @@ __device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
 // consecutive rows: every store instruction of a warp is one contiguous,
 // coalesced span of 32 rows.  Checks as sparse.py:84-97.
 template <int KK, bool SUMS>  // SUMS: v2 tensors (decoder chunk sums); else v1 (look-back)
-__global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowParams p) {
+__global__ void __launch_bounds__(ROW_THREADS, SUMS ? 5 : 1) k_rows_small8(RowParams p) {
     static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
     float* orow0 = p.out + p.out_off[b] + r0 * KK;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
     bool bad = false;
-#pragma unroll 1
+#pragma unroll 2
     for (uint32_t j = 0; j < PER; ++j) {
         const uint32_t li = j * ROW_THREADS + threadIdx.x;
         if (li >= nrow) break;
