@@ -43,6 +43,12 @@ def short(name):
             break
     if stem in ("k_rows_small", "k_rows_fast"):
         stem = "k_rows_out"
+    if stem == "k_rows_small8":  # u8 only
+        return "k_rows_out/u8"
+    if stem == "k_rans_enc_v2_u8u16":
+        return "k_rans_enc_v2/u8u16"
+    if stem == "k_materialize_u8u16":
+        return "k_materialize"
     if stem == "k_rowhist2":
         stem = "k_rowhist"
     if stem in ("k_rans_enc_v2", "k_rans_dec_v2", "k_rans_enc_v1", "k_rans_dec_v1", "k_materialize",
