@@ -92,8 +92,10 @@ enum {
 /* Device-resident outputs of scz_encode_batch, owned by the context until
  * its next encode call.  Tensor i's payload is d_payload[info.payload_off
  * .. + payload_len), its table d_freqs[info.freqs_off .. + alphabet) and its
- * v2 block lengths d_block_bytes[info.blocks_off .. + n_blocks).  The payloads
- * are packed back to back, so one copy of payload_total bytes moves all. */
+ * v2 block lengths d_block_bytes[info.blocks_off .. + n_blocks).  v1 payloads
+ * are packed back to back; v2 payloads sit at a fixed per-tensor stride (the
+ * encoder packs each tensor's blocks in place), so payload_total spans the
+ * strided region and the host path copies them with one pitched copy. */
 typedef struct scz_batch {
     uint32_t batch;
     scz_info* d_info;
@@ -149,6 +151,13 @@ int scz_decode_batch_async(scz_ctx* ctx, const scz_info* h_info, uint32_t batch,
                            const uint32_t* d_freqs, const uint32_t* d_block_bytes,
                            const uint8_t* d_payload, float* d_out);
 int scz_decode_status(scz_ctx* ctx, uint32_t batch, int32_t* h_status);
+/* Decode, without any host round trip, the batch that the last
+ * scz_encode_batch of this context produced (its headers stay on the device;
+ * launch geometry is bounded by that call's plan) into d_out (tensor i at
+ * d_out + i * total).  Same checks as the host-header path, done on the
+ * device; statuses via scz_decode_status.  The bench's device-resident
+ * round trip: encode + decode queue back to back with no synchronisation. */
+int scz_decode_batch_device(scz_ctx* ctx, float* d_out);
 
 /* ---- batch over HOST buffers (the e2e path) ---------------------------- */
 /* compress `batch` tensors of `total` float32 (contiguous at h_x; pinned

@@ -76,7 +76,7 @@ assert INFO_DTYPE.itemsize == ctypes.sizeof(Info)
 EXPORTS = (
     "scz_abi_version", "scz_ctx_create", "scz_ctx_destroy", "scz_last_error", "scz_ctx_stream",
     "scz_launch_count", "scz_compress", "scz_decompress", "scz_encode_batch", "scz_batch_sync",
-    "scz_decode_batch", "scz_decode_batch_async", "scz_decode_status", "scz_quantize",
+    "scz_decode_batch", "scz_decode_batch_async", "scz_decode_status", "scz_decode_batch_device", "scz_quantize",
     "scz_quantize_params", "scz_dequantize", "scz_csr_encode", "scz_csr_decode", "scz_build_counts",
     "scz_normalize", "scz_rans_encode", "scz_rans_decode", "scz_search", "scz_compress_batch",
     "scz_decompress_batch", "scz_ctx_set_timing", "scz_ctx_read_timing",
@@ -112,6 +112,7 @@ def load_library():
             "scz_decode_batch": (I32, [P, P, U32, P, P, P, P, P]),
             "scz_decode_batch_async": (I32, [P, P, U32, P, P, P, P]),
             "scz_decode_status": (I32, [P, U32, P]),
+            "scz_decode_batch_device": (I32, [P, P]),
             "scz_quantize": (I32, [P, P, U64, I32, P, P, P, P, P]),
             "scz_quantize_params": (I32, [P, P, U64, I32, D, I64, P, P]),
             "scz_dequantize": (I32, [P, P, P, U64, I32, D, I64, P]),

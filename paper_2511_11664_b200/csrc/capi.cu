@@ -212,6 +212,8 @@ struct scz_ctx {
     };
     std::vector<Graph> graphs;
     std::vector<std::pair<std::string, EncPlan>> plans;  // plan_encode_cached
+    EncPlan last_plan;           // of the last scz_encode_batch (scz_decode_batch_device)
+    bool have_last_plan = false;
     cudaEvent_t sync_ev = nullptr;                               // scz_batch_sync
     bool use_graphs = getenv("SCZ_NO_GRAPHS") == nullptr;
     uint32_t front_grid = 0;  // co-resident CTAs of k_front (0 = not queried)
@@ -968,6 +970,52 @@ int validate_header(scz_ctx* ctx, const scz_info& in) {
     return SCZ_OK;
 }
 
+// Device-side counterpart of validate_header + dec_class for headers that
+// never left the device (scz_decode_batch_device): the encoder's scz_info
+// array becomes the decoder's, with the symbol class, the output offsets
+// (uniform T) and the initial statuses (the checks of validate_header).
+__global__ void k_dec_headers(const scz_info* enc, uint32_t B, scz_info* dinfo, uint64_t* out_off,
+                              int32_t* status) {
+    pdl_wait();
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    scz_info in = enc[b];
+    int32_t st = in.status;
+    if (st == SCZ_OK) {
+        const uint64_t L = 2 * in.nnz + in.n_rows;
+        if (in.version != 1 && in.version != 2) st = SCZ_UNSUPPORTED_VERSION;
+        else if ((uint64_t)in.n_rows * in.n_cols != in.total) st = SCZ_INVALID_CONTAINER;
+        else if (in.alphabet < 1 || in.precision > 31 || in.nnz > in.total) st = SCZ_CORRUPT_STREAM;
+        else if (in.version == 2 && (in.lanes != 32 || in.precision > 16)) st = SCZ_UNSUPPORTED;
+        else if (in.version == 2 && (in.block_syms < in.lanes || in.block_syms % in.lanes ||
+                                     in.n_blocks != ceil_div_u32(L, in.block_syms)))
+            st = SCZ_CORRUPT_STREAM;
+        else if (in.payload_len < 4) st = SCZ_CORRUPT_STREAM;
+    }
+    // dec_class: 1 = u8 LUT, 2 = u16 LUT, 4 = binary search
+    if (in.precision <= 15 && in.alphabet <= 256) in.sym_bytes = 1;
+    else if (in.precision <= 15 && in.alphabet <= 4096 && (in.precision <= 14 || in.alphabet <= 2048))
+        in.sym_bytes = 2;
+    else in.sym_bytes = 4;
+    in.status = st;
+    dinfo[b] = in;
+    out_off[b] = (uint64_t)b * in.total;
+    status[b] = st;
+}
+
+// Launch geometry of one decode batch (from the host headers, or bounded by
+// the encode plan when the headers stay on the device).
+struct DecCaps {
+    uint32_t acap = 1, nblk_cap = 1, nchunk_cap = 1, widths = 0, maxK = 1, kmask = 0;
+    uint64_t Lmax = 1, maxA = 1;
+    int maxn = 1, lut_n = 0;
+    bool any_v1 = false, any_v2 = false;
+};
+
+int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* d_freqs, const uint32_t* d_blocks,
+                    const uint8_t* d_payload, float* d_out, bool stage, uint32_t* q_out, uint8_t* mask_out,
+                    const scz_info* h_hdr, const scz_info* d_enc_info, const std::string& key);
+
 int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t* d_freqs,
                const uint32_t* d_blocks, const uint8_t* d_payload, float* d_out, bool stage,
                uint32_t* q_out, uint8_t* mask_out) {
@@ -999,7 +1047,38 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
         off += hi[b].total;
     }
     // headers, output offsets and statuses in one block, as laid out in
-    // h_misc: one H2D copy instead of three on the decode path
+    // h_misc: one H2D copy (decode_launches) instead of three
+    // v2 decode tables: (4 + 2) bytes per slot covers both LUT classes
+    int lut_n = 0;  // largest precision among v2 tensors of the LUT classes
+    for (uint32_t b = 0; b < B; ++b)
+        if (hi[b].version == 2 && hi[b].sym_bytes < 4) lut_n = std::max(lut_n, (int)hi[b].precision);
+    bool any_v1 = false, any_v2 = false;
+    for (uint32_t b = 0; b < B; ++b) (hi[b].version == 2 ? any_v2 : any_v1) = true;
+    (void)s;
+    DecCaps c;
+    c.acap = acap; c.nblk_cap = nblk_cap; c.nchunk_cap = nchunk_cap; c.widths = widths; c.maxK = maxK;
+    c.kmask = kmask; c.Lmax = Lmax; c.maxA = maxA; c.maxn = maxn; c.lut_n = lut_n;
+    c.any_v1 = any_v1; c.any_v2 = any_v2;
+    // everything below is stream-ordered (pinned H2D of the prepared infos +
+    // launches) and replays from the graph cache for a repeated batch shape
+    const std::string key = key_of(
+        "dec", {B, acap, nblk_cap, nchunk_cap, widths, maxK, kmask, Lmax, maxA, (uint64_t)maxn, (uint64_t)lut_n,
+                (uint64_t)any_v1 | ((uint64_t)any_v2 << 1) | ((uint64_t)stage << 2),
+                (uint64_t)(uintptr_t)d_freqs, (uint64_t)(uintptr_t)d_blocks, (uint64_t)(uintptr_t)d_payload,
+                (uint64_t)(uintptr_t)d_out, (uint64_t)(uintptr_t)q_out, (uint64_t)(uintptr_t)mask_out,
+                (uint64_t)(uintptr_t)hi});
+    return decode_launches(ctx, B, c, d_freqs, d_blocks, d_payload, d_out, stage, q_out, mask_out, hi, nullptr, key);
+}
+
+int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* d_freqs, const uint32_t* d_blocks,
+                    const uint8_t* d_payload, float* d_out, bool stage, uint32_t* q_out, uint8_t* mask_out,
+                    const scz_info* h_hdr, const scz_info* d_enc_info, const std::string& key) {
+    cudaStream_t s = ctx->stream;
+    const uint32_t acap = c.acap, nblk_cap = c.nblk_cap, nchunk_cap = c.nchunk_cap, widths = c.widths,
+                   maxK = c.maxK, kmask = c.kmask;
+    const uint64_t Lmax = c.Lmax, maxA = c.maxA;
+    const int maxn = c.maxn, lut_n = c.lut_n;
+    const bool any_v1 = c.any_v1, any_v2 = c.any_v2;
     const size_t hdr_bytes = (size_t)B * (sizeof(scz_info) + 8 + 4);
     CK(ctx->dinfo.ensure(hdr_bytes));
     scz_info* d_hi = ctx->dinfo.as<scz_info>();
@@ -1009,26 +1088,17 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     CK(ctx->cumtab.ensure((size_t)B * (acap + 1) * 4));
     CK(ctx->dblk_off.ensure((size_t)B * nblk_cap * 4));
     CK(ctx->dsym.ensure((size_t)B * Lmax * 4));
-    CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 8));  // look-back words
-    // v2 decode tables: (4 + 2) bytes per slot covers both LUT classes
-    int lut_n = 0;  // largest precision among v2 tensors of the LUT classes
-    for (uint32_t b = 0; b < B; ++b)
-        if (hi[b].version == 2 && hi[b].sym_bytes < 4) lut_n = std::max(lut_n, (int)hi[b].precision);
+    CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 8));  // look-back words / chunk sums
     const uint64_t lut_stride = ((6ull << lut_n) + 15) & ~15ull;
     CK(ctx->dlut.ensure((size_t)B * lut_stride + 64));
     const uint32_t lut_slices = lut_n ? std::max<uint32_t>(1, (1u << lut_n) / LUT_SLICE) : 0;
-    bool any_v1 = false, any_v2 = false;
-    for (uint32_t b = 0; b < B; ++b) (hi[b].version == 2 ? any_v2 : any_v1) = true;
-    // everything below is stream-ordered (pinned H2D of the prepared infos +
-    // launches) and replays from the graph cache for a repeated batch shape
-    const std::string key = key_of(
-        "dec", {B, acap, nblk_cap, nchunk_cap, widths, maxK, kmask, Lmax, maxA, (uint64_t)maxn, (uint64_t)lut_n,
-                (uint64_t)any_v1 | ((uint64_t)any_v2 << 1) | ((uint64_t)stage << 2),
-                (uint64_t)(uintptr_t)d_freqs, (uint64_t)(uintptr_t)d_blocks, (uint64_t)(uintptr_t)d_payload,
-                (uint64_t)(uintptr_t)d_out, (uint64_t)(uintptr_t)q_out, (uint64_t)(uintptr_t)mask_out,
-                (uint64_t)(uintptr_t)hi});
     return graph_run(ctx, key, [&]() -> int {
-    CK(cudaMemcpyAsync(ctx->dinfo.p, hi, hdr_bytes, cudaMemcpyHostToDevice, s));
+    if (h_hdr) {
+        CK(cudaMemcpyAsync(ctx->dinfo.p, h_hdr, hdr_bytes, cudaMemcpyHostToDevice, s));
+    } else {
+        CK(launch_pdl(k_dec_headers, dim3(ceil_div_u32(B, 256)), 256, 0, s, d_enc_info, B, d_hi, d_off, d_st));
+        LAUNCHED("k_dec_headers");
+    }
     DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
                  ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
                  d_st, ctx->dlut.as<uint8_t>(), lut_stride,
@@ -1198,6 +1268,8 @@ int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t ba
                                            (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format,
                                            lanes, block_syms});
     if ((st = graph_run(ctx, key, [&] { return run_encode(ctx, d_x, pl, nullptr); })) != SCZ_OK) return st;
+    ctx->last_plan = pl;
+    ctx->have_last_plan = true;
     out->batch = batch;
     out->d_info = ctx->info.as<scz_info>();
     out->d_freqs = ctx->freqs.as<uint32_t>();
@@ -1240,6 +1312,46 @@ int scz_decode_batch_async(scz_ctx* ctx, const scz_info* h_info, uint32_t batch,
         if (st) return st;
     }
     return run_decode(ctx, h_info, batch, d_freqs, d_block_bytes, d_payload, d_out, false, nullptr, nullptr);
+}
+
+int scz_decode_batch_device(scz_ctx* ctx, float* d_out) {
+    if (!ctx || !d_out) return SCZ_INVALID_INPUT;
+    if (!ctx->have_last_plan) return ctx->fail(SCZ_INVALID_INPUT, "no scz_encode_batch on this context");
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    const EncPlan& pl = ctx->last_plan;
+    const uint32_t B = pl.B;
+    // geometry bounds over every candidate reshape of the plan (the chosen
+    // one is known only on the device): alphabet <= max(2^Q, K + 1)
+    DecCaps c;
+    c.acap = pl.acap;
+    c.maxA = pl.acap;
+    c.nblk_cap = pl.format == 2 ? pl.nblk_cap : 1;
+    c.Lmax = (pl.L_max + 15) & ~15ull;
+    c.maxn = pl.precision;
+    c.lut_n = pl.format == 2 ? pl.precision : 0;
+    c.any_v1 = pl.format == 1;
+    c.any_v2 = pl.format == 2;
+    for (uint64_t n : pl.rows) {
+        const uint32_t K = (uint32_t)(pl.T / n);
+        const uint64_t abound = std::max<uint64_t>(1ull << pl.q_bits, (uint64_t)K + 1);
+        scz_info probe{};
+        probe.precision = (uint8_t)pl.precision;
+        probe.alphabet = (uint32_t)abound;
+        uint8_t w = 1;
+        dec_class(probe, &w);
+        c.widths |= w | (w >= 2 ? 1u : 0u) | (w == 4 ? 2u : 0u);  // a smaller alphabet takes a smaller class
+        c.maxK = std::max(c.maxK, K);
+        c.kmask |= K == 1 ? 1u : (K == 2 ? 2u : (K == 4 ? 4u : 8u));
+        c.nchunk_cap = std::max(c.nchunk_cap, ceil_div_u32(n, dec_chunk_rows(K, K <= 4 ? 1 : w, false)));
+    }
+    if (c.lut_n && !(c.widths & 3)) c.lut_n = 0;
+    const std::string key = key_of("decdev", {B, pl.T, (uint64_t)pl.q_bits, (uint64_t)pl.precision,
+                                              (uint64_t)pl.format, pl.block_syms, (uint64_t)pl.rows.size(),
+                                              pl.rows.front(), (uint64_t)(uintptr_t)d_out});
+    return decode_launches(ctx, B, c, ctx->freqs.as<uint32_t>(), ctx->block_len.as<uint32_t>(),
+                           ctx->payload.as<uint8_t>(), d_out, false, nullptr, nullptr, nullptr,
+                           ctx->info.as<scz_info>(), key);
 }
 
 int scz_decode_status(scz_ctx* ctx, uint32_t batch, int32_t* h_status) {

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     // One step: pop the lane's symbol (rans.py:147-152) and refill.  A
     // stream that runs past its block end keeps decoding ring garbage and is
     // rejected by the final cur == end check (rans.py:203-205 underrun).
-    auto step = [&](bool active) {
+    auto step = [&](bool active) -> uint32_t {
         uint32_t cnt = 0, sym = 0;
         if (active) {
             const uint32_t slot = x & mask;
@@ -136,24 +136,57 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
         const uint32_t sel = cnt == 2 ? 0x1045u : (cnt == 1 ? 0x2104u : 0x3210u);
         x = __byte_perm(x, v, sel);
         cur += __popc(b1) + __popc(b2);
-        if (active) *out = (S)sym;
-        out += 32;
+        return sym;
     };
-    if (steps > 0) {
+    if constexpr (sizeof(S) == 1) {
+        // u8 symbols collect in a per-warp 16-step shared buffer and leave
+        // with one 16-byte store per lane (instead of a byte store per step)
+        __shared__ __align__(16) uint8_t s_sym[WPB][16 * 32];
+        uint8_t* ob = s_sym[warp];
+        uint8_t* gout = reinterpret_cast<uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride + base;  // 16-aligned
+        const uint32_t full = len / 32;
+        uint32_t s = 0;
+        for (; s + 16 <= full; s += 16) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ob[(4 * q + u) * 32 + lane] = (uint8_t)step(true);
+                advance();
+            }
+            __syncwarp();
+            *reinterpret_cast<uint4*>(gout + (size_t)s * 32 + 16 * lane) =
+                *reinterpret_cast<const uint4*>(ob + 16 * lane);
+            __syncwarp();
+        }
+        for (uint32_t j = s; j < steps; ++j) {
+            const bool act = j * 32 + lane < len;  // only the last step can be partial
+            const uint32_t sym = step(act);
+            if (act) ob[(j - s) * 32 + lane] = (uint8_t)sym;
+            if (j < full) advance();
+        }
+        __syncwarp();
+        const uint32_t rem = len - s * 32;  // symbols still in the buffer (< 512)
+        for (uint32_t i = lane; i < rem; i += 32) gout[(size_t)s * 32 + i] = ob[i];
+        __syncwarp();
+    } else if (steps > 0) {
         const uint32_t full = len / 32;
         uint32_t s = 0;
         for (; s + 4 <= full; s += 4) {
-            step(true);
-            step(true);
-            step(true);
-            step(true);
+            *out = (S)step(true); out += 32;
+            *out = (S)step(true); out += 32;
+            *out = (S)step(true); out += 32;
+            *out = (S)step(true); out += 32;
             advance();
         }
         for (; s < full; ++s) {
-            step(true);
+            *out = (S)step(true); out += 32;
             advance();
         }
-        if (full < steps) step(full * 32 + lane < len);  // partial last step
+        if (full < steps) {  // partial last step
+            const bool act = full * 32 + lane < len;
+            const uint32_t sym = step(act);
+            if (act) *out = (S)sym;
+        }
     }
     cp_async_wait<0>();
     // Row-count sums per SMALL_ROWS-row chunk for k_rows_small8 (u8, K in

@@ -508,3 +508,39 @@ def test_lazy_search_mixed_batch_vs_oracle():
         assert container.to_bytes(c) == orc.to_bytes(ref)
         depths.append(len(optimizer.search(t, 8)[1].candidates))
     assert min(depths) <= 5 < max(depths), depths  # both passes exercised
+
+
+def test_device_header_decode_matches_host_header_path():
+    """scz_decode_batch_device (headers never leave the device) reconstructs
+    exactly what the host-header path does, for v1 and v2, mixed K and a
+    tensor with non-finite input (its status is reported, others decode)."""
+    import ctypes
+
+    import torch
+
+    from paper_2511_11664_b200 import _native
+
+    dims = (1, 64, 28, 28)
+    T = int(np.prod(dims))
+    xs = [make_input(dict(kind="relu-laplace", dims=dims, sparsity=s, seed=90 + i))
+          for i, s in enumerate([0.5, 0.9, 0.2, 0.6])]
+    xs[2][17] = np.nan
+    x = torch.from_numpy(np.stack(xs)).cuda()
+    for fmt in (1, 2):
+        ctx = _native.Context(0)
+        lib = ctx.lib
+        batch = _native.Batch()
+        ctx.check(lib.scz_encode_batch(ctx.h, ctypes.c_void_p(x.data_ptr()), T, 4, 8, -1, 14, fmt, 32, 2048,
+                                       ctypes.byref(batch)))
+        out_dev = torch.full_like(x, -1.0)
+        ctx.check(lib.scz_decode_batch_device(ctx.h, ctypes.c_void_p(out_dev.data_ptr())))
+        st_dev = (ctypes.c_int32 * 4)()
+        ctx.check(lib.scz_decode_status(ctx.h, 4, st_dev))
+        info = (_native.Info * 4)()
+        ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), info))
+        assert [info[i].status for i in range(4)] == [0, 0, 1, 0]
+        assert list(st_dev) == [0, 0, 1, 0]
+        for i in (0, 1, 3):
+            c = sz.compress(sz.FeatureTensor(dims, xs[i]), 8, format=fmt, block_syms=2048)
+            want = sz.decompress(c).data
+            assert np.array_equal(out_dev[i].cpu().numpy().view(np.uint32), want.view(np.uint32)), (fmt, i)
