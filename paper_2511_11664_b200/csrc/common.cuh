@@ -151,8 +151,12 @@ __device__ uint32_t chunk_prefix(unsigned long long* st, uint32_t chunk, uint32_
     for (int j = (int)chunk - 1;; j -= 32) {
         const int idx = j - (int)lane;  // lane 0: nearest predecessor
         unsigned long long w = idx >= 0 ? vs[idx] : (2ull << 32);
-        while (__any_sync(0xffffffffu, (w >> 32) == 0))
+        // back off while predecessors are still running, so waiting warps
+        // leave the issue slots to the ones doing work
+        for (uint32_t ns = 32; __any_sync(0xffffffffu, (w >> 32) == 0); ns = ns < 1024 ? 2 * ns : ns) {
+            __nanosleep(ns);
             if ((w >> 32) == 0) w = vs[idx];
+        }
         const uint32_t inc = __ballot_sync(0xffffffffu, (w >> 32) == 2);
         if (inc) {
             const uint32_t first = __ffs(inc) - 1;
