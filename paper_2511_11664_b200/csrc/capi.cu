@@ -17,7 +17,6 @@
 #include "encode.cu"
 #include "select.cu"
 #include "rans.cu"
-#include "front.cu"
 #include "rans_enc.cu"
 #include "rans_dec.cu"
 #include "rowhist.cu"
@@ -200,7 +199,7 @@ struct scz_ctx {
         }
         return SCZ_OK;
     }
-    DevBuf ready, candcnt, selbuf, dlut, probe, lbwords;
+    DevBuf candcnt, selbuf, dlut, probe, lbwords;
     // CUDA-graph cache: a launch sequence seen twice with the same key and
     // allocation generation is captured once and replayed afterwards.
     struct Graph {
@@ -216,8 +215,6 @@ struct scz_ctx {
     bool have_last_plan = false;
     cudaEvent_t sync_ev = nullptr;                               // scz_batch_sync
     bool use_graphs = getenv("SCZ_NO_GRAPHS") == nullptr;
-    uint32_t front_grid = 0;  // co-resident CTAs of k_front (0 = not queried)
-    bool use_front = getenv("SCZ_FUSED_FRONT") != nullptr;  // experimental (slower today)
 
     // Optional per-kernel timing with CUDA events on this stream: kernel i
     // spans [end event of the previous launch (or the API-entry mark), its
@@ -660,29 +657,11 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     zs.words[4] = 1;
     for (int r = 0; r < 5; ++r) zs.per[r] = ceil_div_u32(zs.words[r], pl.n_tiles);
 
-    // K1+K2+K3: fused single-read front end when every tensor's tiles fit in
-    // one co-resident grid (cooperative launch), else stats then quantise.
-    if (ctx->front_grid == 0) {
-        int per_sm = 0, coop = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_front, TILE_THREADS, 0);
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
-        ctx->front_grid = coop ? (uint32_t)(per_sm * ctx->num_sms) : 1u;
-    }
-    const uint64_t items = (uint64_t)B * pl.n_tiles;
-    if (ctx->use_front && pl.n_tiles <= ctx->front_grid && ctx->front_grid > 1) {
-        CK(ctx->ready.ensure((size_t)B * 4));
-        CK(cudaMemsetAsync(ctx->ready.p, 0, (size_t)B * 4, s));
-        CK(cudaMemsetAsync(ctx->state.p, 0, (size_t)B * sizeof(TensorState), s));
-        for (int r = 0; r < 5; ++r)  // k_front does not take a ZeroSpec
-            if (zs.ptr[r]) CK(cudaMemsetAsync(zs.ptr[r], 0, (size_t)B * zs.words[r] * 4, s));
-        FrontParams fp{d_x, T, pl.n_tiles, pl.words_pad, B, pl.q_bits, ctx->bitmap.as<uint32_t>(),
-                       ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(),
-                       ctx->ready.as<uint32_t>(), ctx->v8.as<uint8_t>(), ctx->vhist.as<uint32_t>(), dstride};
-        void* args[] = {&fp};
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(items, ctx->front_grid);
-        CK(cudaLaunchCooperativeKernel((void*)k_front, dim3(grid), dim3(TILE_THREADS), args, 0, s));
-        LAUNCHED("k_front");
-    } else {
+    // K1+K2: statistics, bitmap, params; K3: quantise + compact.  (A fused
+    // single-read front end -- cooperative or TMA-pipelined persistent --
+    // was measured slower: both phases are issue-bound, and the per-tensor
+    // barrier serialises the phases of a CTA.)
+    {
         StatsParams sp{d_x, T, pl.n_tiles, pl.words_pad, pl.q_bits, ctx->bitmap.as<uint32_t>(),
                        ctx->tile_stats.as<float4>(), ctx->tile_off.as<uint32_t>(), ctx->state.as<TensorState>(),
                        zs};
@@ -1232,7 +1211,7 @@ void scz_ctx_destroy(scz_ctx* ctx) {
                       &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
                       &ctx->info, &ctx->payload, &ctx->ticket, &ctx->selbuf, &ctx->dlut, &ctx->probe, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
                       &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
-                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->ready, &ctx->candcnt, &ctx->lbwords})
+                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->candcnt, &ctx->lbwords})
         b->release();
     for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
                        &ctx->h_misc, &ctx->hb_info, &ctx->hb_payload, &ctx->hb_freqs, &ctx->hb_blocks})

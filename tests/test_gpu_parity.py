@@ -426,30 +426,6 @@ def test_batch_api_matches_single_tensor_path():
     assert all(c.n_cols == 8 for c in many)
 
 
-def test_fused_front_end_matches_default(tmp_path):
-    """SCZ_FUSED_FRONT=1 (cooperative single-read front end) gives the same bytes."""
-    import subprocess
-    import sys
-
-    code = (
-        "import sys; sys.path.insert(0, %r); import paper_2511_11664_b200 as sz\n"
-        "from paper_2511_11664_b200 import container\n"
-        "ts = [sz.gen_synthetic('relu-laplace', [1, 128, 28, 28], 0.5, s) for s in range(5)]\n"
-        "open(%r, 'wb').write(b''.join(container.to_bytes(c) for c in container.compress_many(ts, 8)))\n"
-    )
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = []
-    for env_on in (False, True):
-        path = tmp_path / f"out_{int(env_on)}.bin"
-        env = dict(os.environ)
-        env.pop("SCZ_FUSED_FRONT", None)
-        if env_on:
-            env["SCZ_FUSED_FRONT"] = "1"
-        subprocess.check_call([sys.executable, "-c", code % (root, str(path))], env=env, timeout=300)
-        outs.append(path.read_bytes())
-    assert outs[0] == outs[1]
-
-
 def test_graph_replay_tracks_new_inputs_and_reallocation():
     """Repeated shapes replay a captured CUDA graph: every replay must see the
     new input values (device) and new headers (decode), and a buffer
