@@ -63,6 +63,8 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--format", type=int, default=2, choices=[1, 2])
     ap.add_argument("--block-syms", type=int, default=8192)
+    ap.add_argument("--contexts", type=int, default=int(os.environ.get("SCZ_BENCH_CONTEXTS", "2")),
+                    help="library contexts the device-resident steps rotate over (>= 2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="bounded CPU-baseline sample (rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -345,11 +347,13 @@ def run_ours(args):
     # without the headers it must launch every symbol-class / K variant the
     # plan allows; with the chosen variants known on the host this path is
     # faster for a full batch.)
-    ctxs = [ctx, _native.Context(local)]
-    streams = [stream, torch.cuda.ExternalStream(ctxs[1].stream, device=torch.device("cuda", local))]
-    batches = [_native.Batch(), _native.Batch()]
-    infos = [(_native.Info * B)(), (_native.Info * B)()]
-    outs = [out_dev, torch.empty_like(x_dev)]
+    NC = max(2, args.contexts)
+    ctxs = [ctx] + [_native.Context(local) for _ in range(NC - 1)]
+    streams = [stream] + [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local))
+                          for c in ctxs[1:]]
+    batches = [_native.Batch() for _ in range(NC)]
+    infos = [(_native.Info * B)() for _ in range(NC)]
+    outs = [out_dev] + [torch.empty_like(x_dev) for _ in range(NC - 1)]
 
     def enc(k):
         c = ctxs[k]
@@ -365,38 +369,41 @@ def run_ours(args):
                                            ctypes.c_void_p(outs[k].data_ptr())))
 
     def pipelined(n, clocks=None):
-        enc(0)
+        # step i's encode is queued NC - 1 steps ahead of its decode
+        for i in range(min(NC - 1, n)):
+            enc(i % NC)
         for i in range(n):
-            if i + 1 < n:
-                enc((i + 1) % 2)
-            dec(i % 2)
+            if i + NC - 1 < n:
+                enc((i + NC - 1) % NC)
+            dec(i % NC)
             if clocks:
                 clocks.sample()
 
     for _ in range(max(1, args.warmup // 2)):
-        pipelined(2)  # every context's graphs captured
+        pipelined(NC)  # every context's graphs captured
     for _ in range(args.warmup):
         device_step()
     barrier()
-    l0 = ctx.launches + ctxs[1].launches
+    l0 = sum(c.launches for c in ctxs)
     ev0 = torch.cuda.Event(enable_timing=True)
-    ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(NC)]
     clocks = ClockSampler(local)
     with clocks:
         barrier()
         ev0.record(streams[0])
-        streams[1].wait_event(ev0)
+        for st_ in streams[1:]:
+            st_.wait_event(ev0)
         pipelined(args.steps, clocks)
-        for k in range(2):
+        for k in range(NC):
             ev_end[k].record(streams[k])
         barrier()
-    launches = ctx.launches + ctxs[1].launches - l0
+    launches = sum(c.launches for c in ctxs) - l0
     ms = max(ev0.elapsed_time(e) for e in ev_end) / args.steps
     ms = max_over_ranks(ms)
     value = 4.0 * T * B * world / (ms * 1e-3) / 1e9
 
     statuses = (ctypes.c_int32 * B)()
-    for k in range(2):
+    for k in range(NC):
         ctxs[k].check(lib.scz_decode_status(ctxs[k].h, B, statuses))
         assert all(v == 0 for v in statuses), "decode status"
 
