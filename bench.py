@@ -606,10 +606,10 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
     o0 = ctypes.c_void_p(out_dev[0].data_ptr())
     lat_enc, lat_dec = [], []
 
-    def one(timed):
+    def one(timed, bs=args.block_syms):
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record(stream)
-        ctx.check(lib.scz_encode_batch(ctx.h, x0, T, 1, wl["q"], -1, 14, 2, 32, args.block_syms,
+        ctx.check(lib.scz_encode_batch(ctx.h, x0, T, 1, wl["q"], -1, 14, 2, 32, bs,
                                        ctypes.byref(batch)))
         ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), info1))
         b.record(stream)
@@ -638,6 +638,19 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
         encode_plus_decode=statistics.median([e + d for e, d in zip(lat_enc, lat_dec)]),
         tensor=str(wl["dims"]), format="v2", note="device-resident, includes the info D2H sync; kernel_us from a separate per-launch-event pass",
         kernel_us={k: round(1e3 * ms / n, 2) for k, (ms, n) in sorted(kt.items(), key=lambda kv: -kv[1][0])})
+    # the block-size trade-off: shorter v2 blocks shorten the serial rANS
+    # chains (more blocks in flight for one tensor) at the cost of 128 state
+    # bytes + 4 table bytes per block
+    trade = []
+    for bs in (4096, 2048):
+        lat_enc.clear()
+        lat_dec.clear()
+        for it in range(40):
+            one(it >= 10, bs)
+        size = info1[0].payload_len + 60 + 4 * len(wl["dims"]) + 2 * info1[0].alphabet + 12 + 4 * info1[0].n_blocks
+        trade.append(dict(block_syms=bs, encode_plus_decode_us=statistics.median(
+            [e + d for e, d in zip(lat_enc, lat_dec)]), bytes_per_element=size / T))
+    res["latency_us_p50"]["block_size_tradeoff"] = trade
     # v1: the reference's single-stream format, one warp per tensor
     B = x_dev.shape[0]
     h_info = (_native.Info * B)()
