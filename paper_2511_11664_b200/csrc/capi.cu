@@ -989,6 +989,7 @@ struct DecCaps {
     uint64_t Lmax = 1, maxA = 1;
     int maxn = 1, lut_n = 0;
     bool any_v1 = false, any_v2 = false;
+    bool total_mult4 = false;  // every tensor's output offset is a multiple of 4 floats
 };
 
 int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* d_freqs, const uint32_t* d_blocks,
@@ -1038,11 +1039,14 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     c.acap = acap; c.nblk_cap = nblk_cap; c.nchunk_cap = nchunk_cap; c.widths = widths; c.maxK = maxK;
     c.kmask = kmask; c.Lmax = Lmax; c.maxA = maxA; c.maxn = maxn; c.lut_n = lut_n;
     c.any_v1 = any_v1; c.any_v2 = any_v2;
+    c.total_mult4 = true;
+    for (uint32_t b = 0; b < B; ++b) c.total_mult4 &= (hoff[b] % 4) == 0;
     // everything below is stream-ordered (pinned H2D of the prepared infos +
     // launches) and replays from the graph cache for a repeated batch shape
     const std::string key = key_of(
         "dec", {B, acap, nblk_cap, nchunk_cap, widths, maxK, kmask, Lmax, maxA, (uint64_t)maxn, (uint64_t)lut_n,
-                (uint64_t)any_v1 | ((uint64_t)any_v2 << 1) | ((uint64_t)stage << 2),
+                (uint64_t)any_v1 | ((uint64_t)any_v2 << 1) | ((uint64_t)stage << 2) |
+                    ((uint64_t)c.total_mult4 << 3),
                 (uint64_t)(uintptr_t)d_freqs, (uint64_t)(uintptr_t)d_blocks, (uint64_t)(uintptr_t)d_payload,
                 (uint64_t)(uintptr_t)d_out, (uint64_t)(uintptr_t)q_out, (uint64_t)(uintptr_t)mask_out,
                 (uint64_t)(uintptr_t)hi});
@@ -1084,6 +1088,9 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
                  ctx->chunk_sum.as<unsigned long long>(), nchunk_cap, stage ? 0 : 1};
     CK(launch_pdl(k_dec_prepare, dim3(1 + lut_slices, B), 256, 0, s, dp));
     LAUNCHED("k_dec_prepare");
+    // rows of K <= 4 floats are vector-aligned when the output base is 16-byte
+    // aligned and every tensor starts at a multiple of 4 floats
+    const bool vec_rows = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && c.total_mult4;
     RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<unsigned long long>(), nchunk_cap,
                  d_st, d_out, d_off, q_out, mask_out};
     auto run_width = [&](auto tag) -> int {
@@ -1125,7 +1132,10 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
             if constexpr (sizeof(S) <= 2) {
                 if (kmask & 1u) {
                     if constexpr (sizeof(S) == 1) {
-                        if (any_v2) CK(launch_pdl(k_rows_small8<1, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v2) {
+                            if (vec_rows) CK(launch_pdl(k_rows_small8<1, true, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                            else CK(launch_pdl(k_rows_small8<1, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        }
                         if (any_v1) CK(launch_pdl(k_rows_small8<1, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     } else
                         CK(launch_pdl(k_rows_small<S, 1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
@@ -1133,7 +1143,10 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
                 }
                 if (kmask & 2u) {
                     if constexpr (sizeof(S) == 1) {
-                        if (any_v2) CK(launch_pdl(k_rows_small8<2, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v2) {
+                            if (vec_rows) CK(launch_pdl(k_rows_small8<2, true, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                            else CK(launch_pdl(k_rows_small8<2, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        }
                         if (any_v1) CK(launch_pdl(k_rows_small8<2, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     } else
                         CK(launch_pdl(k_rows_small<S, 2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
@@ -1141,7 +1154,10 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
                 }
                 if (kmask & 4u) {
                     if constexpr (sizeof(S) == 1) {
-                        if (any_v2) CK(launch_pdl(k_rows_small8<4, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v2) {
+                            if (vec_rows) CK(launch_pdl(k_rows_small8<4, true, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                            else CK(launch_pdl(k_rows_small8<4, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        }
                         if (any_v1) CK(launch_pdl(k_rows_small8<4, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     } else
                         CK(launch_pdl(k_rows_small<S, 4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
@@ -1311,6 +1327,7 @@ int scz_decode_batch_device(scz_ctx* ctx, float* d_out) {
     c.lut_n = pl.format == 2 ? pl.precision : 0;
     c.any_v1 = pl.format == 1;
     c.any_v2 = pl.format == 2;
+    c.total_mult4 = pl.T % 4 == 0;
     for (uint64_t n : pl.rows) {
         const uint32_t K = (uint32_t)(pl.T / n);
         const uint64_t abound = std::max<uint64_t>(1ull << pl.q_bits, (uint64_t)K + 1);

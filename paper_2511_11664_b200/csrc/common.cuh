@@ -190,6 +190,30 @@ __device__ __forceinline__ void block_copy_s2g(uint8_t* dst, const uint8_t* s_sr
     for (uint32_t i = head + 16 * n16 + threadIdx.x; i < len; i += NT) dst[i] = s_src[i];
 }
 
+// Shared-memory byte store / word load through an explicit 32-bit shared
+// address (from __cvta_generic_to_shared once per kernel): keeps the compiler
+// from re-deriving the shared window base per access in register-tight loops.
+__device__ __forceinline__ void sts_u8_if(uint32_t saddr, uint32_t v, bool pred) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.u8 [%0], %1;\n}\n" ::"r"(saddr),
+                 "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(saddr) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];\n" : "=r"(v) : "r"(saddr) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];\n" : "=r"(v) : "r"(saddr) : "memory");
+    return v;
+}
+
 // cp.async (Ampere-style LDGSTS) helpers: global -> shared without registers
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);

@@ -434,7 +434,10 @@ __device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
 // a row costs a handful of instructions.  Consecutive threads own
 // consecutive rows: every store instruction of a warp is one contiguous,
 // coalesced span of 32 rows.  Checks as sparse.py:84-97.
-template <int KK, bool SUMS>  // SUMS: v2 tensors (decoder chunk sums); else v1 (look-back)
+// SUMS: v2 tensors (decoder chunk sums); else v1 (look-back).  VEC: every
+// output row is KK * 4-byte aligned (host-checked), so rows leave with one
+// vector store and no alignment test.
+template <int KK, bool SUMS, bool VEC = false>
 __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 5 : 1) k_rows_small8(RowParams p) {
     static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
     pdl_wait();
@@ -559,15 +562,27 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 5 : 1) k_rows_small8(RowPa
     }
     __syncthreads();
     float* orow0 = p.out + p.out_off[b] + r0 * KK;
-    const bool vec_ok = (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
+    const bool vec_ok = VEC || (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
     bool bad = false;
+    // explicit 32-bit shared addresses (see lds_u32)
+    const uint32_t a_off = (uint32_t)__cvta_generic_to_shared(s_off);
+    const uint32_t a_r = (uint32_t)__cvta_generic_to_shared(s_r) + rsh;
+    const uint32_t a_c = (uint32_t)__cvta_generic_to_shared(s_c) + csh;
+    const uint32_t a_v = (uint32_t)__cvta_generic_to_shared(s_v) + vsh;
+    const uint32_t a_pk = (uint32_t)__cvta_generic_to_shared(s_pk);
+    const uint32_t a_sel = (uint32_t)__cvta_generic_to_shared(s_sel);
+    const uint32_t a_lut = (uint32_t)__cvta_generic_to_shared(s_lut);
+    auto word_at = [](uint32_t a) {  // 4 bytes at any shared byte address
+        const uint32_t w = a & ~3u;
+        return __funnelshift_r(lds_u32(w), lds_u32(w + 4), (a & 3) * 8);
+    };
 #pragma unroll 2
     for (uint32_t j = 0; j < PER; ++j) {
         const uint32_t li = j * ROW_THREADS + threadIdx.x;
         if (li >= nrow) break;
-        const uint32_t off = s_off[li], r = s_r[rsh + li];
-        const uint32_t cw = smem_word_at(s_c, csh + off);  // bytes past r are ignored
-        const uint32_t vw = smem_word_at(s_v, vsh + off);
+        const uint32_t off = lds_u16(a_off + 2 * li), r = lds_u8(a_r + li);
+        const uint32_t cw = word_at(a_c + off);  // bytes past r are ignored
+        const uint32_t vw = word_at(a_v + off);
         // column-presence mask of the row; a row is valid (sparse.py:90-97:
         // columns < K, strictly increasing) iff its live column bytes equal
         // the sorted packing of its mask and the mask has r bits
@@ -575,13 +590,13 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 5 : 1) k_rows_small8(RowPa
 #pragma unroll
         for (int e = 0; e < KK; ++e) mask |= (uint32_t)((uint32_t)e < r) << ((cw >> (8 * e)) & (KK - 1));
         const uint32_t live = r >= 4 ? 0xFFFFFFFFu : ((1u << (8 * r)) - 1u);
-        bad |= ((cw & live) != s_pk[mask]) | ((uint32_t)__popc(mask) != r);
+        bad |= ((cw & live) != lds_u32(a_pk + 4 * mask)) | ((uint32_t)__popc(mask) != r);
         // value byte of every present column in column order (PRMT), 0 elsewhere
-        const uint32_t vs = __byte_perm(vw, 0u, s_sel[mask]);
+        const uint32_t vs = __byte_perm(vw, 0u, lds_u32(a_sel + 4 * mask));
         float o[KK];
 #pragma unroll
         for (int col = 0; col < KK; ++col) {
-            const float val = s_lut[(vs >> (8 * col)) & 0xFFu];
+            const float val = __uint_as_float(lds_u32(a_lut + 4 * ((vs >> (8 * col)) & 0xFFu)));
             o[col] = (mask >> col) & 1u ? val : 0.0f;
         }
         float* orow = orow0 + (uint64_t)li * KK;
@@ -602,6 +617,9 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 5 : 1) k_rows_small8(RowPa
 template __global__ void k_rows_small8<1, true>(RowParams);
 template __global__ void k_rows_small8<2, true>(RowParams);
 template __global__ void k_rows_small8<4, true>(RowParams);
+template __global__ void k_rows_small8<1, true, true>(RowParams);
+template __global__ void k_rows_small8<2, true, true>(RowParams);
+template __global__ void k_rows_small8<4, true, true>(RowParams);
 template __global__ void k_rows_small8<1, false>(RowParams);
 template __global__ void k_rows_small8<2, false>(RowParams);
 template __global__ void k_rows_small8<4, false>(RowParams);

@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
     // range) are collected in `slow` and redone with the exact fp64 sequence
     // afterwards.  The histogram is taken from the staged symbols.
     uint32_t slow = 0;  // bit 4 * it + j: element needs the exact path
+    const uint32_t sv_base = (uint32_t)__cvta_generic_to_shared(s_v);
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
         const float4 v = vv[it];
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 4) k_quantize(QuantParams p) {
             const uint32_t q = (uint32_t)min(max(__float_as_int(t) - 0x4B400000, 0), qmax);
             const bool nz = (nib >> j) & 1u;
             slow |= (uint32_t)!ok << (4 * it + j);
-            if (nz) s_v[rank] = (uint8_t)q;
+            sts_u8_if(sv_base + rank, q, nz);
             if constexpr (SYM_OUT) {
                 const uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4 + j;
                 if (idx < p.total) p.sym_out[(uint64_t)b * p.total + idx] = q;
