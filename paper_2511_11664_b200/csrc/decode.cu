@@ -438,7 +438,7 @@ __device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
 // output row is KK * 4-byte aligned (host-checked), so rows leave with one
 // vector store and no alignment test.
 template <int KK, bool SUMS, bool VEC = false>
-__global__ void __launch_bounds__(ROW_THREADS, SUMS ? 5 : 1) k_rows_small8(RowParams p) {
+__global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowParams p) {
     static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
