@@ -34,6 +34,7 @@ struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
     bool fresh = false;  // allocated since the owner last cleared it
+    std::atomic<uint64_t>* gen = &g_alloc_gen;  // the owning context's allocation generation
     cudaError_t ensure(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFree(p);
@@ -45,7 +46,7 @@ struct DevBuf {
             cap = want;
             fresh = true;
         }
-        g_alloc_gen.fetch_add(1);
+        gen->fetch_add(1);
         return e;
     }
     template <typename T>
@@ -60,6 +61,7 @@ struct DevBuf {
 struct HostBuf {
     void* p = nullptr;
     size_t cap = 0;
+    std::atomic<uint64_t>* gen = &g_alloc_gen;
     cudaError_t ensure(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFreeHost(p);
@@ -68,7 +70,7 @@ struct HostBuf {
         size_t want = std::max<size_t>(n + n / 8, 4096);
         cudaError_t e = cudaMallocHost(&p, want);
         if (e == cudaSuccess) cap = want;
-        g_alloc_gen.fetch_add(1);
+        gen->fetch_add(1);
         return e;
     }
     // grow to n bytes keeping the first `used` bytes (callers sync first)
@@ -82,7 +84,7 @@ struct HostBuf {
         if (p) cudaFreeHost(p);
         p = np;
         cap = want;
-        g_alloc_gen.fetch_add(1);
+        gen->fetch_add(1);
         return cudaSuccess;
     }
     template <typename T>
@@ -200,6 +202,24 @@ struct scz_ctx {
         return SCZ_OK;
     }
     DevBuf candcnt, selbuf, dlut, probe, lbwords;
+    // Allocation generation of THIS context's buffers: a cached graph holds
+    // raw pointers into them, so it is stale once any of them reallocates
+    // (other contexts' allocations do not invalidate it).
+    std::atomic<uint64_t> alloc_gen{1};
+    template <class F>
+    void for_each_buf(F f) {
+        for (DevBuf* b : {&x_in, &bitmap, &tile_stats, &tile_off, &state, &vhist, &v8, &cr, &hp, &rhist, &counts,
+                          &terms, &freqs, &cum, &enctab, &slots, &block_len, &blk_off, &cand_out, &info, &payload,
+                          &ticket, &selbuf, &dlut, &probe, &dsym_in, &dinfo, &dfreqs, &dblocks, &dpayload, &cumtab,
+                          &dblk_off, &dsym, &chunk_sum, &dstatus, &out_off, &dout, &candcnt, &lbwords})
+            f(b);
+    }
+    template <class F>
+    void for_each_host_buf(F f) {
+        for (HostBuf* b : {&h_info, &h_payload, &h_freqs, &h_blocks, &h_status, &h_misc, &hb_info, &hb_payload,
+                           &hb_freqs, &hb_blocks})
+            f(b);
+    }
     // CUDA-graph cache: a launch sequence seen twice with the same key and
     // allocation generation is captured once and replayed afterwards.
     struct Graph {
@@ -509,7 +529,7 @@ __global__ void __launch_bounds__(256) k_pack(const scz_info* info, const uint8_
 template <class F>
 int graph_run(scz_ctx* ctx, const std::string& key, F&& body) {
     if (!ctx->use_graphs || ctx->timing) return body();
-    const uint64_t gen = g_alloc_gen.load();
+    const uint64_t gen = ctx->alloc_gen.load();
     scz_ctx::Graph* g = nullptr;
     for (auto& e : ctx->graphs)
         if (e.key == key) g = &e;
@@ -533,7 +553,7 @@ int graph_run(scz_ctx* ctx, const std::string& key, F&& body) {
     if (!g->seen || g->gen != gen) {  // first sighting under this generation: eager
         g->seen = 1;
         int st = body();
-        g->gen = g_alloc_gen.load();
+        g->gen = ctx->alloc_gen.load();
         return st;
     }
     const uint64_t l0 = ctx->launches;
@@ -557,7 +577,7 @@ int graph_run(scz_ctx* ctx, const std::string& key, F&& body) {
         return body();
     }
     g->exec = exec;
-    g->gen = g_alloc_gen.load();
+    g->gen = ctx->alloc_gen.load();
     g->nkern = ctx->launches - l0;
     CK(cudaGraphLaunch(exec, ctx->stream));
     return SCZ_OK;
@@ -1207,6 +1227,8 @@ int scz_ctx_create(int device, scz_ctx** out) {
     }
     scz_ctx* ctx = new scz_ctx();
     ctx->device = device;
+    ctx->for_each_buf([ctx](DevBuf* b) { b->gen = &ctx->alloc_gen; });
+    ctx->for_each_host_buf([ctx](HostBuf* b) { b->gen = &ctx->alloc_gen; });
     ctx->num_sms = prop.multiProcessorCount;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -1222,16 +1244,8 @@ void scz_ctx_destroy(scz_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->x_in, &ctx->bitmap, &ctx->tile_stats, &ctx->tile_off, &ctx->state, &ctx->vhist,
-                      &ctx->v8, &ctx->cr, &ctx->hp, &ctx->rhist, &ctx->counts, &ctx->terms, &ctx->freqs,
-                      &ctx->cum, &ctx->enctab, &ctx->slots, &ctx->block_len, &ctx->blk_off, &ctx->cand_out,
-                      &ctx->info, &ctx->payload, &ctx->ticket, &ctx->selbuf, &ctx->dlut, &ctx->probe, &ctx->dsym_in, &ctx->dinfo, &ctx->dfreqs,
-                      &ctx->dblocks, &ctx->dpayload, &ctx->cumtab, &ctx->dblk_off, &ctx->dsym,
-                      &ctx->chunk_sum, &ctx->dstatus, &ctx->out_off, &ctx->dout, &ctx->candcnt, &ctx->lbwords})
-        b->release();
-    for (HostBuf* b : {&ctx->h_info, &ctx->h_payload, &ctx->h_freqs, &ctx->h_blocks, &ctx->h_status,
-                       &ctx->h_misc, &ctx->hb_info, &ctx->hb_payload, &ctx->hb_freqs, &ctx->hb_blocks})
-        b->release();
+    ctx->for_each_buf([](DevBuf* b) { b->release(); });
+    ctx->for_each_host_buf([](HostBuf* b) { b->release(); });
     if (ctx->xfer) {
         cudaStreamSynchronize(ctx->xfer);
         cudaStreamSynchronize(ctx->xfer_out);

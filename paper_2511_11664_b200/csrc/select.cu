@@ -163,6 +163,52 @@ __device__ uint32_t block_max32(uint32_t v, BlockScratch& s) {
 // helpers are out of line.
 __device__ __noinline__ double plog2p(double pp) { return __dmul_rn(pp, log2(pp)); }
 
+// Large alphabets (A > 1024): add 1 to the `k` largest remainders (ties to
+// the lower index, np.lexsort) by an 8-pass radix select over the remainder
+// bits.  Out of line: the common small-alphabet path stays contiguous code.
+__device__ __noinline__ void deficit_radix(const double* rem, uint32_t A, unsigned long long k, uint32_t* freqs,
+                                           BlockScratch& s) {
+    unsigned long long prefix = 0, pmask = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += SEL_THREADS) s.hist[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
+            unsigned long long key = (unsigned long long)__double_as_longlong(rem[i]);
+            if ((key & pmask) == prefix) atomicAdd(&s.hist[(key >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long acc = 0;
+            int d = 255;
+            for (; d > 0; --d) {
+                if (acc + s.hist[d] >= k) break;
+                acc += s.hist[d];
+            }
+            s.bcast64[0] = prefix | ((unsigned long long)d << shift);
+            s.bcast64[1] = k - acc;
+        }
+        __syncthreads();
+        prefix = s.bcast64[0];
+        k = s.bcast64[1];
+        pmask |= 0xFFull << shift;
+        __syncthreads();
+    }
+    // take every key > prefix, and the first k keys == prefix by index
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < A; base += SEL_THREADS) {
+        uint32_t i = base + threadIdx.x;
+        unsigned long long key =
+            i < A ? (unsigned long long)__double_as_longlong(rem[i]) : 0ull;
+        uint32_t eq = (i < A && key == prefix) ? 1u : 0u;
+        uint32_t tot;
+        uint32_t ex = block_exclusive_scan<SEL_THREADS>(eq, s.scan, &tot);
+        if (i < A) {
+            if (key > prefix || (eq && carry + ex < k)) freqs[i] += 1;
+        }
+        carry += tot;
+    }
+}
+
 __device__ __noinline__ int block_normalize(const uint32_t* counts, uint32_t A, int precision,
                                uint32_t* freqs, double* rem, uint32_t* cum, BlockScratch& s) {
     unsigned long long total = 0, npresent = 0;
@@ -191,7 +237,6 @@ __device__ __noinline__ int block_normalize(const uint32_t* counts, uint32_t A, 
         // np.lexsort((arange, -rem))[:deficit]: radix-select the deficit-th
         // largest remainder (non-negative doubles order as their bits), then
         // take ties in index order.
-        unsigned long long prefix = 0, pmask = 0;
         unsigned long long k = (unsigned long long)deficit;
         if (k >= A) {
             for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) freqs[i] += 1;
@@ -217,44 +262,7 @@ __device__ __noinline__ int block_normalize(const uint32_t* counts, uint32_t A, 
                 if (rank < k) freqs[i] += 1;
             }
         } else {
-            for (int shift = 56; shift >= 0; shift -= 8) {
-                for (int i = threadIdx.x; i < 256; i += SEL_THREADS) s.hist[i] = 0;
-                __syncthreads();
-                for (uint32_t i = threadIdx.x; i < A; i += SEL_THREADS) {
-                    unsigned long long key = (unsigned long long)__double_as_longlong(rem[i]);
-                    if ((key & pmask) == prefix) atomicAdd(&s.hist[(key >> shift) & 255], 1u);
-                }
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    unsigned long long acc = 0;
-                    int d = 255;
-                    for (; d > 0; --d) {
-                        if (acc + s.hist[d] >= k) break;
-                        acc += s.hist[d];
-                    }
-                    s.bcast64[0] = prefix | ((unsigned long long)d << shift);
-                    s.bcast64[1] = k - acc;
-                }
-                __syncthreads();
-                prefix = s.bcast64[0];
-                k = s.bcast64[1];
-                pmask |= 0xFFull << shift;
-                __syncthreads();
-            }
-            // take every key > prefix, and the first k keys == prefix by index
-            uint32_t carry = 0;
-            for (uint32_t base = 0; base < A; base += SEL_THREADS) {
-                uint32_t i = base + threadIdx.x;
-                unsigned long long key =
-                    i < A ? (unsigned long long)__double_as_longlong(rem[i]) : 0ull;
-                uint32_t eq = (i < A && key == prefix) ? 1u : 0u;
-                uint32_t tot;
-                uint32_t ex = block_exclusive_scan<SEL_THREADS>(eq, s.scan, &tot);
-                if (i < A) {
-                    if (key > prefix || (eq && carry + ex < k)) freqs[i] += 1;
-                }
-                carry += tot;
-            }
+            deficit_radix(rem, A, k, freqs, s);
         }
     }
     __syncthreads();
