@@ -17,10 +17,11 @@ constexpr int DEC2_WPB = 16;         // warps (= blocks) per CTA, throughput mod
 constexpr int DEC2_WPB_SMALL = 4;    // latency mode (grid would not fill the GPU)
 constexpr int DCHUNK = 256;          // bytes per cp.async chunk (8 per lane)
 constexpr int DRING = 4 * DCHUNK;    // per-warp ring
+constexpr int DRING_STRIDE = DRING + 16;  // + a mirror of the ring's first 8 bytes (no wrap on the 2nd word)
 constexpr uint32_t DEC_BIG_F = 256;  // symbols with more slots are filled CTA-wide
 
 // Shared-memory layout (LUT classes, L = u8 / u16):
-//   rings  [WPB][DRING] bytes
+//   rings  [WPB][DRING + 16] bytes (bytes DRING.. mirror bytes 0..7)
 //   step   [2^n] u32 (f << 16) | (slot - cum): the state update in one load
 //   sym    [2^n] L   slot -> symbol (off the state recurrence)
 // The two tables are built once per tensor by k_dec_prepare and arrive with
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint32_t blk0 = blockIdx.x * WPB;
     if (blk0 >= in.n_blocks) return;  // whole CTA idle
     uint8_t* rings = smem;
-    uint32_t* lstep = reinterpret_cast<uint32_t*>(smem + WPB * DRING);
+    uint32_t* lstep = reinterpret_cast<uint32_t*>(smem + WPB * DRING_STRIDE);
     const L* lsym = reinterpret_cast<const L*>(reinterpret_cast<const uint8_t*>(lstep) + lut_sym_off(n));
     if constexpr (sizeof(L) < 4) {
         if (threadIdx.x == 0) {
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint64_t a0 = in.payload_off + p.blk_off[(uint64_t)b * p.nblk_cap + blk];
     const uint64_t cbase = a0 & ~(uint64_t)(DCHUNK - 1);
     const uint8_t* gsrc = p.payload + cbase + 8 * lane;
-    uint8_t* ring = rings + warp * DRING;
+    uint8_t* ring = rings + warp * DRING_STRIDE;
     uint8_t* rdst = ring + 8 * lane;
     uint32_t cur = (uint32_t)(a0 - cbase);  // byte offset from cbase
     const uint32_t end = cur + blen;
@@ -70,7 +71,10 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     // chunks starting at or beyond `end` are never fetched (a 256-aligned
     // chunk holding a valid byte never leaves that byte's allocation)
     auto fetch = [&](uint32_t c) {
-        if (c * DCHUNK < end) cp_async8(rdst + (c & 3) * DCHUNK, gsrc + (size_t)c * DCHUNK);
+        if (c * DCHUNK < end) {
+            cp_async8(rdst + (c & 3) * DCHUNK, gsrc + (size_t)c * DCHUNK);
+            if ((c & 3) == 0 && lane == 0) cp_async8(ring + DRING, gsrc + (size_t)c * DCHUNK);  // mirror
+        }
         cp_async_commit();
     };
     fetch(0);
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     if constexpr (sizeof(L) < 4) mbar_wait(&s_bar, 0);
     const uint32_t mask = nslots - 1;
     const uint32_t ltm = lanemask_lt();
-    const uint32_t* ring32 = reinterpret_cast<const uint32_t*>(ring);
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     S* out = reinterpret_cast<S*>(p.dsym) + (uint64_t)b * p.dsym_stride + base + lane;
     const uint32_t steps = (len + 31) / 32;
     // One step: pop the lane's symbol (rans.py:147-152) and refill.  A
@@ -129,9 +133,11 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
         const uint32_t b1 = __ballot_sync(0xffffffffu, cnt >= 1);
         const uint32_t b2 = __ballot_sync(0xffffffffu, cnt == 2);
         const uint32_t a = cur + __popc(b1 & ltm) + __popc(b2 & ltm);
-        // bytes a, a + 1 from two aligned words; PRMT shifts them into x
-        const uint32_t w0 = ring32[(a >> 2) & (DRING / 4 - 1)];
-        const uint32_t w1 = ring32[((a >> 2) + 1) & (DRING / 4 - 1)];
+        // bytes a, a + 1 from two aligned words (the second one may be the
+        // mirror past the ring's end); PRMT shifts them into x
+        const uint32_t wa = ring_s + (a & (DRING - 4));
+        const uint32_t w0 = lds_u32(wa);
+        const uint32_t w1 = lds_u32(wa + 4);
         const uint32_t v = __funnelshift_r(w0, w1, (a & 3) * 8);
         const uint32_t sel = cnt == 2 ? 0x1045u : (cnt == 1 ? 0x2104u : 0x3210u);
         x = __byte_perm(x, v, sel);
@@ -231,7 +237,7 @@ SCZ_DEC2(uint32_t, uint32_t)
 
 // dynamic shared memory of k_rans_dec_v2 for a batch (max over tensors)
 inline size_t dec_v2_smem(int wpb, size_t lwidth, int n, uint32_t) {
-    size_t s = (size_t)wpb * DRING;
+    size_t s = (size_t)wpb * DRING_STRIDE;
     if (lwidth < 4) s += ((((size_t)1 << n) * (4 + lwidth)) + 15) & ~(size_t)15;
     return (s + 15) & ~(size_t)15;
 }
