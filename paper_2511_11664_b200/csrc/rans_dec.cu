@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     // stream that runs past its block end keeps decoding ring garbage and is
     // rejected by the final cur == end check (rans.py:203-205 underrun).
     auto step = [&](bool active) -> uint32_t {
-        uint32_t cnt = 0, sym = 0;
+        uint32_t sym = 0;
+        bool p1 = false, p2 = false;  // refill 1 byte (x < 2^23) / 2 bytes (x < 2^15)
         if (active) {
             const uint32_t slot = x & mask;
             if constexpr (sizeof(L) < 4) {
@@ -128,10 +129,11 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
                 sym = lo;
                 x = gf[sym] * (x >> n) + slot - gcum[sym];
             }
-            cnt = (x < (1u << 15)) ? 2u : ((x < STATE_LOW) ? 1u : 0u);
+            p1 = x < STATE_LOW;
+            p2 = x < (1u << 15);
         }
-        const uint32_t b1 = __ballot_sync(0xffffffffu, cnt >= 1);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, cnt == 2);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, p1);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, p2);
         const uint32_t a = cur + __popc(b1 & ltm) + __popc(b2 & ltm);
         // bytes a, a + 1 from two aligned words (the second one may be the
         // mirror past the ring's end); PRMT shifts them into x
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
         const uint32_t w0 = lds_u32(wa);
         const uint32_t w1 = lds_u32(wa + 4);
         const uint32_t v = __funnelshift_r(w0, w1, (a & 3) * 8);
-        const uint32_t sel = cnt == 2 ? 0x1045u : (cnt == 1 ? 0x2104u : 0x3210u);
+        const uint32_t sel = p2 ? 0x1045u : (p1 ? 0x2104u : 0x3210u);
         x = __byte_perm(x, v, sel);
         cur += __popc(b1) + __popc(b2);
         return sym;
