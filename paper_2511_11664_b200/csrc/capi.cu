@@ -860,7 +860,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     EncParams ep{ctx->state.as<TensorState>(), ctx->enctab.as<EncTab>(), pl.acap, pl.precision,
                  pl.block_syms, ctx->slots.as<uint8_t>(), pl.slot_cap, pl.nblk_cap,
                  ctx->block_len.as<uint32_t>(), pl.acap};
-    const dim3 g_enc2(ceil_div_u32(pl.nblk_cap, ENC2_WPB), B);
+    const dim3 g_enc2(B, ceil_div_u32(pl.nblk_cap, ENC2_WPB));
     const bool enc_smem_tab = pl.acap <= ENC_TAB_SMEM_MAX;
     const size_t enc_smem = enc_smem_tab ? (size_t)pl.acap * sizeof(EncTab) : 0;
     auto run_width = [&](auto tag) -> int {
@@ -1734,9 +1734,9 @@ int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t*
         const size_t sm = (size_t)alphabet * sizeof(EncTab);
         CK(cudaFuncSetAttribute(k_rans_enc_v2<PlainSrc, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sm));
-        k_rans_enc_v2<PlainSrc, true, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, sm, s>>>(ep, src, PackParams{});
+        k_rans_enc_v2<PlainSrc, true, true><<<dim3(1, ceil_div_u32(nblk, ENC2_WPB)), ENC2_WPB * 32, sm, s>>>(ep, src, PackParams{});
     } else if (v2) {
-        k_rans_enc_v2<PlainSrc, false, true><<<dim3(ceil_div_u32(nblk, ENC2_WPB), 1), ENC2_WPB * 32, 0, s>>>(ep, src, PackParams{});
+        k_rans_enc_v2<PlainSrc, false, true><<<dim3(1, ceil_div_u32(nblk, ENC2_WPB)), ENC2_WPB * 32, 0, s>>>(ep, src, PackParams{});
     }
     if (!v2) k_rans_enc_v1<PlainSrc><<<1, 32, 0, s>>>(ep, src);
     LAUNCHED("k_rans_enc");

@@ -238,10 +238,13 @@ __device__ __forceinline__ void enc_apply_ring(EncLane& L, const EncTab& t, bool
 
 template <class Src, bool SMEM, bool CHECK>
 __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, const PackParams& pk) {
-    const uint32_t b = blockIdx.y;
+    // grid (tensor, block group): a tensor's block groups are dispatched B CTAs
+    // apart, so a group's look-back predecessors started well before it, and
+    // the idle groups past a tensor's block count all sit at the grid's tail
+    const uint32_t b = blockIdx.x;
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) {
-        if (pk.payload && pk.write_failed && blockIdx.x == 0 && threadIdx.x == 0)
+        if (pk.payload && pk.write_failed && blockIdx.y == 0 && threadIdx.x == 0)
             write_info(pk.info[b], st, st.status, 2, pk.q_bits, p.precision, pk.total, p.block_syms, 0, 0,
                        (uint64_t)b * pk.pcap, p.acap, p.slots_per_tensor, b);
         return;
@@ -249,7 +252,7 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
     if (Src::width && st.sym_bytes != (uint32_t)Src::width) return;  // other width variant
     const uint64_t L = st.stream_len;
     const uint32_t nblk = L ? ceil_div_u32(L, p.block_syms) : 1;
-    const uint32_t blk0 = blockIdx.x * ENC2_WPB;
+    const uint32_t blk0 = blockIdx.y * ENC2_WPB;
     if (blk0 >= nblk) return;
     extern __shared__ EncTab s_tab[];  // A entries when SMEM (host: A <= p.tab_smem)
     const uint32_t A = st.alphabet;
@@ -409,7 +412,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(ENC2_WPB * 32, 10)
     k_rans_enc_v2_u8u16(EncParams p, Contig8Src s8, SplitSrc<uint16_t> s16, PackParams pk) {
     pdl_wait();
-    const TensorState& st = p.state[blockIdx.y];
+    const TensorState& st = p.state[blockIdx.x];
     if (st.status == SCZ_OK && st.sym_bytes == 2) enc_v2_body<SplitSrc<uint16_t>, SMEM, false>(p, s16, pk);
     else enc_v2_body<Contig8Src, SMEM, false>(p, s8, pk);  // also writes failed tensors' headers
 }
