@@ -705,7 +705,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
             const uint64_t gx = ceil_div_u32(cp.period_words, 128);
             const uint64_t want_gy = (296 + gx * B - 1) / (gx * B);
             uint32_t rpc = ceil_div_u32(cp.n_rows, want_gy);
-            cp.rows_per_cta = std::max(1u, std::min(64u, rpc));
+            cp.rows_per_cta = std::max(8u, std::min(64u, rpc));  // >= 8 rows: fewer same-address atomics
         }
         cp.hp = ctx->hp.as<uint32_t>();
         cp.hp_stride = (uint32_t)pl.period;
@@ -718,7 +718,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     // smallest K (the scan usually stops among them); the rest are priced
     // only for tensors whose scan did not stop (sel_pending).
     constexpr uint32_t NA_FIRST = 5;
-    const bool split = pl.searching && !cand_out && pl.acap <= SEL_WARP_ACAP && ncand > NA_FIRST;
+    const bool split = pl.searching && !cand_out && pl.acap <= SEL_WARP_ACAP && ncand > NA_FIRST && !getenv("SCZ_NO_LAZY");
     const uint32_t n_first = split ? NA_FIRST : ncand;
     // row-count histograms (+ column folds) of candidates [c0, c1)
     auto rowhist_pass = [&](uint32_t c0, uint32_t c1, bool pending_only) -> int {
@@ -761,7 +761,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         rp.hp = ctx->hp.as<uint32_t>();
         rp.hp_stride = (uint32_t)pl.period;
         rp.period = (uint32_t)pl.period;
-        rp.fold_start = chunks;  // + one column-fold CTA per candidate
+        rp.n_fold = c1 - c0;  // one column-fold CTA per candidate, ahead of the row chunks
         size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
         CK(launch_pdl(k_rowhist2, dim3(chunks + (c1 - c0), B), RH_THREADS, smem, s, rp));
         LAUNCHED("k_rowhist");

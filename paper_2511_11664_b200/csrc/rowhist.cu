@@ -37,7 +37,8 @@ struct RowHist2Params {
     uint32_t rhist_stride;
     const uint32_t* hp;                // [B][hp_stride] nonzeros per (p mod P)
     uint32_t hp_stride, period;
-    uint32_t fold_start;               // chunks >= fold_start: fold CTA of candidate chunk - fold_start
+    uint32_t n_fold;                   // CTAs [0, n_fold): column fold of candidate blockIdx.x (first in the
+                                       // grid: they are the longest CTAs and start right away)
     const TensorState* state;          // pending_only: skip tensors whose search already stopped
     int pending_only;
 };
@@ -115,12 +116,13 @@ __device__ void rowhist_swar(const uint32_t* bm, uint32_t w0, uint32_t w1, uint3
 
 __global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__ RowHist2Params p) {
     pdl_wait();
-    const uint32_t chunk = blockIdx.x, b = blockIdx.y;
+    const uint32_t b = blockIdx.y;
     if (p.pending_only && !p.state[b].sel_pending) return;
-    if (chunk >= p.fold_start) {
-        fold_columns(p, b, chunk - p.fold_start);
+    if (blockIdx.x < p.n_fold) {
+        fold_columns(p, b, blockIdx.x);
         return;
     }
+    const uint32_t chunk = blockIdx.x - p.n_fold;
     uint32_t c = 0;
     while (c + 1 < p.n_cand && p.chunk_start[c + 1] <= chunk) ++c;
     const uint32_t K = p.cand_k[c], N = p.cand_rows[c];
