@@ -520,3 +520,28 @@ def test_device_header_decode_matches_host_header_path():
             c = sz.compress(sz.FeatureTensor(dims, xs[i]), 8, format=fmt, block_syms=2048)
             want = sz.decompress(c).data
             assert np.array_equal(out_dev[i].cpu().numpy().view(np.uint32), want.view(np.uint32)), (fmt, i)
+
+
+def test_decompress_many_mixed_versions_shapes_and_widths():
+    """One batch decode over v1 and v2 containers of different shapes, K
+    (the K in {1, 2, 4} row kernels, the general one, u16 symbols) and a
+    tensor size that is not a multiple of 4 (unaligned output rows)."""
+    specs = [
+        (dict(kind="relu-laplace", dims=[1, 64, 28, 28], sparsity=0.5, seed=1), 8, None, 1),
+        (dict(kind="relu-laplace", dims=[1, 64, 28, 28], sparsity=0.5, seed=2), 8, None, 2),
+        (dict(kind="signed", dims=[3, 5, 7], seed=5), 6, None, 2),
+        (dict(kind="relu-laplace", dims=[1, 128, 28, 28], sparsity=0.93, seed=3), 8, None, 2),
+        (dict(kind="relu-laplace", dims=[1, 64, 28, 28], sparsity=0.4, seed=4), 8, 196, 2),   # K = 256: u16
+        (dict(kind="relu-laplace", dims=[601], sparsity=0.3, seed=6), 5, 1, 1),
+        (dict(kind="relu-laplace", dims=[1, 32, 20, 20], sparsity=0.6, seed=7), 4, 3200, 2),  # K = 4
+    ]
+    cs, ts = [], []
+    for spec, q, n_rows, fmt in specs:
+        t = sz.FeatureTensor(tuple(spec["dims"]), make_input(spec))
+        ts.append(t)
+        cs.append(sz.compress(t, q, n_rows, format=fmt, block_syms=1024))
+    assert len({c.n_cols for c in cs}) >= 4
+    outs = container.decompress_many(cs)
+    for c, o in zip(cs, outs):
+        want = sz.decompress(c)
+        assert np.array_equal(o.data.view(np.uint32), want.data.view(np.uint32))
