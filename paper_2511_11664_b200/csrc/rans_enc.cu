@@ -74,34 +74,50 @@ __device__ __forceinline__ int32_t final_status(const TensorState& st, uint32_t 
 }
 
 // Copy len bytes src -> dst (any alignments) with one warp: bytes up to a
-// 4-aligned destination, funnel-shifted words, then the tail.  src is a slot
-// (padded: the word after the last is readable).
+// 16-byte aligned destination, then 16-byte stores assembled from aligned
+// 16-byte loads (funnel-shifted), then the tail.  src is a slot (padded: the
+// 16 bytes after the last are readable).  Two chunks per lane in flight: at
+// B = 1 this copy sits on the latency path, one L2 round trip per round.
 __device__ __forceinline__ void warp_copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t len, uint32_t lane) {
-    uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
+    uint32_t head = (uint32_t)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15);
     head = head < len ? head : len;
     if (lane < head) dst[lane] = src[lane];
     const uint8_t* s2 = src + head;
-    uint32_t* d2 = reinterpret_cast<uint32_t*>(dst + head);
-    const uint32_t nwords = (len - head) / 4;
-    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(s2) & 3) * 8;
-    const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s2) & ~(uintptr_t)3);
-    // eight words per lane in flight per round: at B = 1 this copy sits on
-    // the latency path, one L2 round trip per round
-    for (uint32_t w0 = 0; w0 < nwords; w0 += 256) {
-        uint32_t lo[8], hi[8];
+    uint4* d2 = reinterpret_cast<uint4*>(dst + head);
+    const uint32_t n16 = (len - head) >> 4;
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(s2) & 15);  // byte shift
+    const uint4* sw = reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(s2) & ~(uintptr_t)15);
+    // 16 bytes starting at byte sh (1..15, warp-uniform) of the pair (a, b)
+    const uint32_t q = sh >> 2, r = (sh & 3) * 8;
+    auto pick = [q, r](const uint4& a, const uint4& b) -> uint4 {
+        switch (q) {
+            case 0: return make_uint4(__funnelshift_r(a.x, a.y, r), __funnelshift_r(a.y, a.z, r),
+                                      __funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r));
+            case 1: return make_uint4(__funnelshift_r(a.y, a.z, r), __funnelshift_r(a.z, a.w, r),
+                                      __funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r));
+            case 2: return make_uint4(__funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r),
+                                      __funnelshift_r(b.x, b.y, r), __funnelshift_r(b.y, b.z, r));
+            default: return make_uint4(__funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r),
+                                       __funnelshift_r(b.y, b.z, r), __funnelshift_r(b.z, b.w, r));
+        }
+    };
+    for (uint32_t c0 = 0; c0 < n16; c0 += 64) {
+        uint4 a[2], bb[2];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t w = w0 + 32 * k + lane;
-            lo[k] = w < nwords ? sw[w] : 0u;
-            hi[k] = w < nwords ? sw[w + 1] : 0u;
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t c = c0 + 32 * k + lane;
+            if (c < n16) {
+                a[k] = sw[c];
+                bb[k] = sh ? sw[c + 1] : a[k];
+            }
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t w = w0 + 32 * k + lane;
-            if (w < nwords) d2[w] = sh ? __funnelshift_r(lo[k], hi[k], sh) : lo[k];
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t c = c0 + 32 * k + lane;
+            if (c < n16) d2[c] = sh ? pick(a[k], bb[k]) : a[k];
         }
     }
-    for (uint32_t i = head + 4 * nwords + lane; i < len; i += 32) dst[i] = src[i];
+    for (uint32_t i = head + 16 * n16 + lane; i < len; i += 32) dst[i] = src[i];
 }
 
 template <typename S>
