@@ -1227,6 +1227,15 @@ int scz_ctx_create(int device, scz_ctx** out) {
     }
     scz_ctx* ctx = new scz_ctx();
     ctx->device = device;
+    {   // device tables shared by every context on this device (idempotent)
+        cudaSetDevice(device);
+        k_init_row_lut<<<5, 256>>>();
+        if (cudaDeviceSynchronize() != cudaSuccess) {
+            cudaGetLastError();
+            delete ctx;
+            return SCZ_CUDA_ERROR;
+        }
+    }
     ctx->for_each_buf([ctx](DevBuf* b) { b->gen = &ctx->alloc_gen; });
     ctx->for_each_host_buf([ctx](HostBuf* b) { b->gen = &ctx->alloc_gen; });
     ctx->num_sms = prop.multiProcessorCount;

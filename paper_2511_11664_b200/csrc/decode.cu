@@ -434,6 +434,34 @@ __device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
 // a row costs a handful of instructions.  Consecutive threads own
 // consecutive rows: every store instruction of a warp is one contiguous,
 // coalesced span of 32 rows.  Checks as sparse.py:84-97.
+// K = 4 row table: entry [r][idx], idx = the low two bits of the row's four
+// column bytes packed (c0 | c1 << 2 | c2 << 4 | c3 << 6), only the first r
+// fields meaningful.  Entry = PRMT selector (16 bits: nibble j = rank of
+// column j among the row's columns, 4 = absent) | mask << 16 (present
+// columns) | valid << 20 (the r columns strictly increase, sparse.py:90-97).
+// Initialised once per device by k_init_row_lut (scz_ctx_create).
+__device__ uint32_t g_row_lut4[5 * 256];
+
+__global__ void k_init_row_lut() {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 5 * 256) return;
+    const uint32_t r = i >> 8, idx = i & 255;
+    uint32_t mask = 0, valid = 1, prev = 0;
+    for (uint32_t e = 0; e < r; ++e) {
+        const uint32_t c = (idx >> (2 * e)) & 3u;
+        if (e > 0 && c <= prev) valid = 0;
+        mask |= 1u << c;
+        prev = c;
+    }
+    uint32_t sel = 0, k = 0;
+    for (uint32_t j = 0; j < 4; ++j) {
+        const bool here = (mask >> j) & 1u;
+        sel |= (here ? k : 4u) << (4 * j);
+        k += here;
+    }
+    g_row_lut4[i] = sel | (mask << 16) | (valid << 20);
+}
+
 // SUMS: v2 tensors (decoder chunk sums); else v1 (look-back).  VEC: every
 // output row is KK * 4-byte aligned (host-checked), so rows leave with one
 // vector store and no alignment test.
@@ -472,6 +500,9 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
     // per column-presence mask: the sorted column packing and the PRMT
     // selector that moves the k-th value byte to its column (4 = zero byte)
     __shared__ uint32_t s_pk[1 << KK], s_sel[1 << KK];
+    __shared__ uint32_t s_lut4[KK == 4 ? 5 * 256 : 1];
+    if constexpr (KK == 4)
+        for (uint32_t i = threadIdx.x; i < 5 * 256; i += ROW_THREADS) s_lut4[i] = g_row_lut4[i];
     if (threadIdx.x < (1u << KK)) {
         uint32_t pk = 0, sel = 0, k = 0;
         for (uint32_t j = 0; j < 4; ++j) {
@@ -571,6 +602,7 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
     const uint32_t a_v = (uint32_t)__cvta_generic_to_shared(s_v) + vsh;
     const uint32_t a_pk = (uint32_t)__cvta_generic_to_shared(s_pk);
     const uint32_t a_sel = (uint32_t)__cvta_generic_to_shared(s_sel);
+    const uint32_t a_lut4 = (uint32_t)__cvta_generic_to_shared(s_lut4);
     const uint32_t a_lut = (uint32_t)__cvta_generic_to_shared(s_lut);
     auto word_at = [](uint32_t a) {  // 4 bytes at any shared byte address
         const uint32_t w = a & ~3u;
@@ -583,16 +615,28 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
         const uint32_t off = lds_u16(a_off + 2 * li), r = lds_u8(a_r + li);
         const uint32_t cw = word_at(a_c + off);  // bytes past r are ignored
         const uint32_t vw = word_at(a_v + off);
-        // column-presence mask of the row; a row is valid (sparse.py:90-97:
-        // columns < K, strictly increasing) iff its live column bytes equal
-        // the sorted packing of its mask and the mask has r bits
-        uint32_t mask = 0;
-#pragma unroll
-        for (int e = 0; e < KK; ++e) mask |= (uint32_t)((uint32_t)e < r) << ((cw >> (8 * e)) & (KK - 1));
+        uint32_t mask, vs;
         const uint32_t live = r >= 4 ? 0xFFFFFFFFu : ((1u << (8 * r)) - 1u);
-        bad |= ((cw & live) != lds_u32(a_pk + 4 * mask)) | ((uint32_t)__popc(mask) != r);
-        // value byte of every present column in column order (PRMT), 0 elsewhere
-        const uint32_t vs = __byte_perm(vw, 0u, lds_u32(a_sel + 4 * mask));
+        if constexpr (KK == 4) {
+            // one table entry per row: the two low bits of the four column
+            // bytes gathered by a multiply, (r, idx) -> selector, mask, valid;
+            // a live column byte >= 4 is caught separately
+            const uint32_t idx = ((cw & 0x03030303u) * 0x01041040u) >> 24;
+            const uint32_t ent = lds_u32(a_lut4 + 4 * (r * 256 + idx));
+            mask = (ent >> 16) & 0xFu;
+            bad |= !((ent >> 20) & 1u) | ((cw & live & 0xFCFCFCFCu) != 0);  // sparse.py:90-97
+            vs = __byte_perm(vw, 0u, ent & 0xFFFFu);
+        } else {
+            // column-presence mask of the row; a row is valid (sparse.py:90-97:
+            // columns < K, strictly increasing) iff its live column bytes equal
+            // the sorted packing of its mask and the mask has r bits
+            mask = 0;
+#pragma unroll
+            for (int e = 0; e < KK; ++e) mask |= (uint32_t)((uint32_t)e < r) << ((cw >> (8 * e)) & (KK - 1));
+            bad |= ((cw & live) != lds_u32(a_pk + 4 * mask)) | ((uint32_t)__popc(mask) != r);
+            // value byte of every present column in column order (PRMT), 0 elsewhere
+            vs = __byte_perm(vw, 0u, lds_u32(a_sel + 4 * mask));
+        }
         float o[KK];
 #pragma unroll
         for (int col = 0; col < KK; ++col) {
