@@ -198,6 +198,18 @@ __device__ __forceinline__ void sts_u8_if(uint32_t saddr, uint32_t v, bool pred)
                  "r"(v), "r"((uint32_t)pred)
                  : "memory");
 }
+// Compaction step: if (flags & mask) { smem[saddr] = v (low byte); ++saddr; }
+__device__ __forceinline__ void sts_u8_bump(uint32_t& saddr, uint32_t v, uint32_t flags, uint32_t mask) {
+    asm volatile(
+        "{\n .reg .pred p;\n .reg .b32 t;\n and.b32 t, %2, %3;\n setp.ne.u32 p, t, 0;\n"
+        " @p st.shared.u8 [%0], %1;\n @p add.u32 %0, %0, 1;\n}\n"
+        : "+r"(saddr)
+        : "r"(v), "r"(flags), "r"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void red_shared_inc(uint32_t saddr) {
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(saddr) : "memory");
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(saddr) : "memory");

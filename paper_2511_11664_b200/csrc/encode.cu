@@ -302,7 +302,7 @@ __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, i
 }
 
 template <bool SYM_OUT>  // SYM_OUT: also write every element's symbol (stage API)
-__global__ void __launch_bounds__(TILE_THREADS, 6) k_quantize(QuantParams p) {
+__global__ void __launch_bounds__(TILE_THREADS, 5) k_quantize(QuantParams p) {
     pdl_wait();
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -316,17 +316,27 @@ __global__ void __launch_bounds__(TILE_THREADS, 6) k_quantize(QuantParams p) {
     __shared__ uint32_t s_wpre[TILE_WORDS];
     __shared__ uint32_t s_wbits[TILE_WORDS];
     __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_hist[8][256];  // one copy per warp: no inter-warp atomic contention
+    // one histogram copy per warp (no inter-warp atomic contention), 1 KB
+    // aligned so a bin address is the copy's base OR'd with 4 * symbol
+    __shared__ __align__(1024) uint32_t s_hist[8][256];
     __shared__ __align__(16) uint8_t s_v[TILE + 32];  // the tile's value symbols, rank order
     const int nbins = 1 << p.q_bits;
-    for (int i = threadIdx.x; i < 8 * 256; i += TILE_THREADS) (&s_hist[0][0])[i] = 0;
+    static_assert(8 * 256 == 2 * 4 * TILE_THREADS, "two 16-byte zero stores per thread");
+    reinterpret_cast<uint4*>(&s_hist[0][0])[threadIdx.x] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(&s_hist[0][0])[threadIdx.x + TILE_THREADS] = make_uint4(0, 0, 0, 0);
     // all eight 16-byte loads in flight first (out-of-range lanes read 0:
     // their bitmap bits are 0 and the exact path re-checks the index)
     float4 vv[8];
+    if (aligned && tile_base + TILE <= p.total) {  // interior tile: no bounds checks
+        const float4* x4 = reinterpret_cast<const float4*>(xb + tile_base + warp * 1024 + lane * 4);
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
-        uint32_t valid;
-        vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &valid);
+        for (int it = 0; it < 8; ++it) vv[it] = __ldg(x4 + it * 32);
+    } else {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            uint32_t valid;
+            vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &valid);
+        }
     }
     uint32_t myword = bm[threadIdx.x];
     s_wbits[threadIdx.x] = myword;
@@ -342,11 +352,16 @@ __global__ void __launch_bounds__(TILE_THREADS, 6) k_quantize(QuantParams p) {
     uint8_t* v8 = p.v8 + (uint64_t)b * p.v8_stride;
 
     // Branch-free over all 32 elements of the thread: the fp32 estimate for
-    // every element and a store predicated on its bitmap bit; elements near a
-    // rounding boundary (or every element when the scale is out of the fp32
-    // range) are collected in `slow` and redone with the exact fp64 sequence
-    // afterwards.  The histogram is taken from the staged symbols.
-    uint32_t slow = 0;  // bit 4 * it + j: element needs the exact path
+    // every element and a store predicated on its bitmap bit.  In the fast
+    // path the estimate's rint lies in [0, qmax] (y >= -1/2 and y <= qmax + 1/2
+    // up to rounding, since lo <= x <= hi and z = round(-lo / s), and elements
+    // within 2^-12 of a half-integer are excluded), so the symbol is the low
+    // byte of y + 1.5 * 2^23 and needs no clamp.  A bit per group of four
+    // collects "an element is near a rounding boundary (or the scale is out of
+    // the fp32 range)"; such groups are redone afterwards, the elements near a
+    // boundary with the exact fp64 sequence.  The histogram is taken from the
+    // staged symbols.
+    uint32_t slow = fast ? 0u : 0xFFu;  // bit it: redo group it (4 elements)
     const uint32_t sv_base = (uint32_t)__cvta_generic_to_shared(s_v);
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
@@ -355,8 +370,9 @@ __global__ void __launch_bounds__(TILE_THREADS, 6) k_quantize(QuantParams p) {
         const int word = warp * 32 + it * 4 + (lane >> 3);
         const int bit0 = 4 * (lane & 7);
         const uint32_t wbits = s_wbits[word];
-        const uint32_t nib = (wbits >> bit0) & 0xFu;  // nonzero flags (bitmap == x != 0, valid only)
-        uint32_t rank = s_wpre[word] + __popc(wbits & ((1u << bit0) - 1u));  // tile-local
+        const uint32_t nib = wbits >> bit0;  // nonzero flags (bitmap == x != 0, valid only)
+        uint32_t sa = sv_base + s_wpre[word] + __popc(wbits & ((1u << bit0) - 1u));  // rank slot
+        bool sl = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             // rint via the 1.5 * 2^23 magic constant (|y| < 2^22 whenever
@@ -364,39 +380,52 @@ __global__ void __launch_bounds__(TILE_THREADS, 6) k_quantize(QuantParams p) {
             const float y = fmaf(e[j], r32, zf32);
             const float t = __fadd_rn(y, 0x1.8p23f);
             const float rq = __fsub_rn(t, 0x1.8p23f);
-            const bool ok = fast && fabsf(__fsub_rn(y, rq)) < 0.5f - 0x1p-12f;
-            const uint32_t q = (uint32_t)min(max(__float_as_int(t) - 0x4B400000, 0), qmax);
-            const bool nz = (nib >> j) & 1u;
-            slow |= (uint32_t)!ok << (4 * it + j);
-            sts_u8_if(sv_base + rank, q, nz);
+            sl |= !(fabsf(__fsub_rn(y, rq)) < 0.5f - 0x1p-12f);
             if constexpr (SYM_OUT) {
+                // caller-supplied parameters: x may lie outside the range
+                const uint32_t q = (uint32_t)min(max(__float_as_int(t) - 0x4B400000, 0), qmax);
+                sts_u8_bump(sa, q, nib, 1u << j);
                 const uint64_t idx = tile_base + warp * 1024 + it * 128 + lane * 4 + j;
                 if (idx < p.total) p.sym_out[(uint64_t)b * p.total + idx] = q;
+            } else {
+                sts_u8_bump(sa, __float_as_uint(t), nib, 1u << j);
             }
-            rank += nz;
         }
+        slow |= (uint32_t)sl << it;
     }
     while (slow) {  // rare: exact fp64 path (tensor.py:130-140), x re-read
-        const int k = __ffs(slow) - 1;
+        const int it = __ffs(slow) - 1;
         slow &= slow - 1;
-        const int it = k >> 2, j = k & 3;
-        const uint32_t off = warp * 1024 + it * 128 + lane * 4 + j;
-        if (tile_base + off >= p.total) continue;
         const int word = warp * 32 + it * 4 + (lane >> 3);
-        const int bit = 4 * (lane & 7) + j;
         const uint32_t wbits = s_wbits[word];
-        const uint32_t q = quant_exact(xb[tile_base + off], scale, zf, (double)qmax);
-        if ((wbits >> bit) & 1u) s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
-        if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + tile_base + off] = q;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t off = warp * 1024 + it * 128 + lane * 4 + j;
+            if (tile_base + off >= p.total) continue;
+            const float x = xb[tile_base + off];
+            const float y = fmaf(x, r32, zf32);
+            const float rq = __fsub_rn(__fadd_rn(y, 0x1.8p23f), 0x1.8p23f);
+            if (fast && fabsf(__fsub_rn(y, rq)) < 0.5f - 0x1p-12f) continue;
+            const int bit = 4 * (lane & 7) + j;
+            const uint32_t q = quant_exact(x, scale, zf, (double)qmax);
+            if ((wbits >> bit) & 1u) s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
+            if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + tile_base + off] = q;
+        }
     }
     __syncthreads();
-    // value histogram of the tile's symbols (per-warp copies)
-    for (uint32_t i = 4 * threadIdx.x; i < tot; i += 4 * TILE_THREADS) {
-        const uint32_t w4 = *reinterpret_cast<const uint32_t*>(s_v + i);
-        const uint32_t n4 = min(4u, tot - i);
-#pragma unroll
-        for (uint32_t k = 0; k < 4; ++k)
-            if (k < n4) atomicAdd(&s_hist[warp][(w4 >> (8 * k)) & 0xFFu], 1u);
+    // value histogram of the tile's symbols (per-warp copies): whole words
+    // of four symbols, then the < 4 tail symbols
+    {
+        const uint32_t hb = (uint32_t)__cvta_generic_to_shared(&s_hist[warp][0]);
+        const uint32_t nfull = tot & ~3u;
+        for (uint32_t i = 4 * threadIdx.x; i < nfull; i += 4 * TILE_THREADS) {
+            const uint32_t w4 = lds_u32(sv_base + i);
+            red_shared_inc(hb | ((w4 << 2) & 0x3FCu));
+            red_shared_inc(hb | ((w4 >> 6) & 0x3FCu));
+            red_shared_inc(hb | ((w4 >> 14) & 0x3FCu));
+            red_shared_inc(hb | ((w4 >> 22) & 0x3FCu));
+        }
+        if (threadIdx.x < tot - nfull) red_shared_inc(hb | (lds_u8(sv_base + nfull + threadIdx.x) << 2));
     }
     __syncthreads();
     // the tile's values go out with coalesced 16-byte stores
