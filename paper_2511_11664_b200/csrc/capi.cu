@@ -1091,7 +1091,10 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
     CK(ctx->cumtab.ensure((size_t)B * (acap + 1) * 4));
     CK(ctx->dblk_off.ensure((size_t)B * nblk_cap * 4));
     CK(ctx->dsym.ensure((size_t)B * Lmax * 4));
-    CK(ctx->chunk_sum.ensure((size_t)B * nchunk_cap * 8));  // look-back words / chunk sums
+    // look-back words / chunk sums, then the [B][256] dequantisation tables
+    const size_t dq_at = ((size_t)B * nchunk_cap * 8 + 15) & ~(size_t)15;  // 16-byte aligned tables
+    CK(ctx->chunk_sum.ensure(dq_at + (size_t)B * 256 * 4));
+    float* d_dq = reinterpret_cast<float*>(ctx->chunk_sum.as<uint8_t>() + dq_at);
     const uint64_t lut_stride = ((6ull << lut_n) + 15) & ~15ull;
     CK(ctx->dlut.ensure((size_t)B * lut_stride + 64));
     const uint32_t lut_slices = lut_n ? std::max<uint32_t>(1, (1u << lut_n) / LUT_SLICE) : 0;
@@ -1105,14 +1108,14 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
     DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
                  ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
                  d_st, ctx->dlut.as<uint8_t>(), lut_stride,
-                 ctx->chunk_sum.as<unsigned long long>(), nchunk_cap, stage ? 0 : 1};
+                 ctx->chunk_sum.as<unsigned long long>(), nchunk_cap, stage ? 0 : 1, d_dq};
     CK(launch_pdl(k_dec_prepare, dim3(1 + lut_slices, B), 256, 0, s, dp));
     LAUNCHED("k_dec_prepare");
     // rows of K <= 4 floats are vector-aligned when the output base is 16-byte
     // aligned and every tensor starts at a multiple of 4 floats
     const bool vec_rows = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && c.total_mult4;
     RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<unsigned long long>(), nchunk_cap,
-                 d_st, d_out, d_off, q_out, mask_out};
+                 d_st, d_out, d_off, q_out, mask_out, d_dq};
     auto run_width = [&](auto tag) -> int {
         using S = decltype(tag);
         using L = S;
@@ -1153,10 +1156,10 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
                 if (kmask & 1u) {
                     if constexpr (sizeof(S) == 1) {
                         if (any_v2) {
-                            if (vec_rows) CK(launch_pdl(k_rows_small8<1, true, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
-                            else CK(launch_pdl(k_rows_small8<1, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                            if (vec_rows) CK(launch_pdl(k_rows_small8<1, true, true>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
+                            else CK(launch_pdl(k_rows_small8<1, true>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
                         }
-                        if (any_v1) CK(launch_pdl(k_rows_small8<1, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v1) CK(launch_pdl(k_rows_small8<1, false>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
                     } else
                         CK(launch_pdl(k_rows_small<S, 1>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
@@ -1164,10 +1167,10 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
                 if (kmask & 2u) {
                     if constexpr (sizeof(S) == 1) {
                         if (any_v2) {
-                            if (vec_rows) CK(launch_pdl(k_rows_small8<2, true, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
-                            else CK(launch_pdl(k_rows_small8<2, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                            if (vec_rows) CK(launch_pdl(k_rows_small8<2, true, true>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
+                            else CK(launch_pdl(k_rows_small8<2, true>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
                         }
-                        if (any_v1) CK(launch_pdl(k_rows_small8<2, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v1) CK(launch_pdl(k_rows_small8<2, false>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
                     } else
                         CK(launch_pdl(k_rows_small<S, 2>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));
@@ -1175,10 +1178,10 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
                 if (kmask & 4u) {
                     if constexpr (sizeof(S) == 1) {
                         if (any_v2) {
-                            if (vec_rows) CK(launch_pdl(k_rows_small8<4, true, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
-                            else CK(launch_pdl(k_rows_small8<4, true>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                            if (vec_rows) CK(launch_pdl(k_rows_small8<4, true, true>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
+                            else CK(launch_pdl(k_rows_small8<4, true>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
                         }
-                        if (any_v1) CK(launch_pdl(k_rows_small8<4, false>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
+                        if (any_v1) CK(launch_pdl(k_rows_small8<4, false>, dim3(nchunk_cap, B), SMALL8_THREADS, 0, s, rp));
                     } else
                         CK(launch_pdl(k_rows_small<S, 4>, dim3(nchunk_cap, B), ROW_THREADS, 0, s, rp));
                     LAUNCHED(wname<S>("k_rows_out"));

@@ -207,6 +207,11 @@ __device__ __forceinline__ void sts_u8_bump(uint32_t& saddr, uint32_t v, uint32_
         : "r"(v), "r"(flags), "r"(mask)
         : "memory");
 }
+// value of every u8 symbol: fl32((i - z) * s) in fp64 (tensor.py dequantise)
+__device__ __forceinline__ void build_dequant_lut(float* lut, double z, double scale) {
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
+        lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, z), scale));
+}
 __device__ __forceinline__ void red_shared_inc(uint32_t saddr) {
     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(saddr) : "memory");
 }

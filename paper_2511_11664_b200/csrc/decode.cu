@@ -20,6 +20,7 @@ namespace scz {
 constexpr int ROW_CHUNK = 1024;     // max rows per chunk
 constexpr int OUT_ELEMS = 4096;     // dense fp32 elements staged per chunk
 constexpr int ROW_THREADS = 256;
+constexpr int SMALL8_THREADS = 128;  // k_rows_small8: SMALL_ROWS / 8 rows per thread
 
 __host__ __device__ inline uint32_t rows_per_chunk(uint32_t K) {
     const uint32_t r = K ? (uint32_t)OUT_ELEMS / K : (uint32_t)ROW_CHUNK;
@@ -45,10 +46,6 @@ __device__ __forceinline__ float dequant(uint32_t v, const float* lut, double z,
     if constexpr (sizeof(S) == 1) return lut[v];
     else return v < 256u ? lut[v] : dequant_slow(v, z, scale);
 }
-__device__ __forceinline__ void build_dequant_lut(float* lut, double z, double scale) {
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
-        lut[i] = __double2float_rn(__dmul_rn(__dsub_rn((double)i, z), scale));
-}
 
 struct RowParams {
     const scz_info* info;   // [B]
@@ -61,6 +58,7 @@ struct RowParams {
     const uint64_t* out_off;
     uint32_t* q_out;        // stage API: symbols
     uint8_t* mask_out;      // stage API: zero mask
+    const float* dq_lut;    // [B][256] from k_dec_prepare (k_rows_small8)
 };
 
 // A chunk of a tensor already marked bad (possibly by another chunk of this
@@ -411,12 +409,14 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
 // with aligned 16-byte loads: byte i lands at dst[sh + i], sh = src & 15
 // (returned).  dst must hold n + 31 bytes; the over-read of up to 15 bytes
 // either side stays inside the caller's allocation.
+// The copies are cp.async (every 16-byte piece in flight at once, none
+// blocking the thread); the caller commits, waits and synchronises.
 __device__ __forceinline__ uint32_t stage_window(uint8_t* dst, const uint8_t* src, uint32_t n) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
     const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(src) - a);
     const uint32_t n16 = (sh + n + 15) >> 4;
-    for (uint32_t i = threadIdx.x; i < n16; i += ROW_THREADS)
-        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(a) + i);
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x)
+        cp_async16(dst + 16 * i, reinterpret_cast<const uint4*>(a) + i);
     return sh;
 }
 
@@ -440,7 +440,7 @@ __device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
 // column j among the row's columns, 4 = absent) | mask << 16 (present
 // columns) | valid << 20 (the r columns strictly increase, sparse.py:90-97).
 // Initialised once per device by k_init_row_lut (scz_ctx_create).
-__device__ uint32_t g_row_lut4[5 * 256];
+__device__ __align__(16) uint32_t g_row_lut4[5 * 256];
 
 __global__ void k_init_row_lut() {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -466,14 +466,14 @@ __global__ void k_init_row_lut() {
 // output row is KK * 4-byte aligned (host-checked), so rows leave with one
 // vector store and no alignment test.
 template <int KK, bool SUMS, bool VEC = false>
-__global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowParams p) {
+__global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 12 : 1) k_rows_small8(RowParams p) {
     static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     if (in.sym_bytes != 1 || in.n_cols != (uint32_t)KK) return;
     constexpr uint32_t R = SMALL_ROWS;
-    constexpr uint32_t PER = R / ROW_THREADS;
+    constexpr uint32_t PER = R / SMALL8_THREADS;
     constexpr uint32_t MAXE = R * KK;  // nonzeros of a valid chunk
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
@@ -490,9 +490,9 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
     __shared__ __align__(16) uint8_t s_r[R + 32];
     __shared__ __align__(16) uint8_t s_c[MAXE + 32];
     __shared__ __align__(16) uint8_t s_v[MAXE + 32];
-    __shared__ uint16_t s_off[R];
+    __shared__ __align__(16) uint32_t s_or[R];  // row: nonzero offset in the chunk | count << 16
     __shared__ uint32_t s_scan[33];
-    __shared__ float s_lut[256];
+    __shared__ __align__(1024) float s_lut[256];  // bin address = base | 4 * symbol
     __shared__ int s_bad;
     __shared__ uint32_t s_base, s_own;
     const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
@@ -500,9 +500,10 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
     // per column-presence mask: the sorted column packing and the PRMT
     // selector that moves the k-th value byte to its column (4 = zero byte)
     __shared__ uint32_t s_pk[1 << KK], s_sel[1 << KK];
-    __shared__ uint32_t s_lut4[KK == 4 ? 5 * 256 : 1];
+    __shared__ __align__(16) uint32_t s_lut4[KK == 4 ? 5 * 256 : 4];
     if constexpr (KK == 4)
-        for (uint32_t i = threadIdx.x; i < 5 * 256; i += ROW_THREADS) s_lut4[i] = g_row_lut4[i];
+        for (uint32_t i = threadIdx.x; i < 5 * 256 / 4; i += SMALL8_THREADS)
+            cp_async16(reinterpret_cast<uint4*>(s_lut4) + i, reinterpret_cast<const uint4*>(g_row_lut4) + i);
     if (threadIdx.x < (1u << KK)) {
         uint32_t pk = 0, sel = 0, k = 0;
         for (uint32_t j = 0; j < 4; ++j) {
@@ -516,6 +517,10 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
     }
     uint32_t cbase = 0, own = 0;
     const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);  // in flight with the sums
+    if (threadIdx.x < 64)  // the tensor's dequantisation table (k_dec_prepare)
+        cp_async16(reinterpret_cast<uint4*>(s_lut) + threadIdx.x,
+                   reinterpret_cast<const uint4*>(p.dq_lut + (uint64_t)b * 256) + threadIdx.x);
+    cp_async_commit();
     if (sums) {
         // chunk offset = sum of the earlier chunks' row counts, and this
         // chunk's own count, both from the decoder: the r, c and v windows
@@ -539,7 +544,7 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
                 s_own = (uint32_t)min(mine, 0xFFFFFFFFull);
             }
         }
-        build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
+        cp_async_wait<0>();
         __syncthreads();
         cbase = s_base;
         own = s_own;
@@ -547,28 +552,37 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
             if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
             return;
         }
-    } else {
-        build_dequant_lut(s_lut, (double)in.zero_point, in.scale);
     }
     uint32_t csh = 0, vsh = 0;
-    if (sums) {
+    if (sums) {  // in flight during the scan below
         csh = stage_window(s_c, d + nnz + cbase, own);
         vsh = stage_window(s_v, d + cbase, own);
+        cp_async_commit();
+    } else {
+        cp_async_wait<0>();
+        __syncthreads();
     }
-    __syncthreads();
-    // thread t sums rows [PER t, PER t + PER) of the chunk (re-read after
-    // the scan rather than held in registers)
-    uint32_t sum = 0;
-    bool rbad = false;
-#pragma unroll
-    for (uint32_t j = 0; j < PER; ++j) {
-        const uint32_t i = threadIdx.x * PER + j;
-        const uint32_t v = i < nrow ? (uint32_t)s_r[rsh + i] : 0u;
-        rbad |= v > (uint32_t)KK;  // sparse.py:88-89
-        sum += min(v, (uint32_t)KK + 1);
-    }
+    // thread t owns rows [8t, 8t + 8) of the chunk for the scan: their count
+    // bytes as two words (bytes past nrow masked off), checked, summed and
+    // prefix-summed four at a time (SWAR; counts <= K keep every byte sum
+    // below 256), then written as (offset | r << 16) entries, two 16-byte
+    // stores per thread
+    static_assert(PER == 8, "two count words per thread");
+    const uint32_t a_r = (uint32_t)__cvta_generic_to_shared(s_r) + rsh;
+    const uint32_t nt = nrow > 8 * threadIdx.x ? min(nrow - 8 * threadIdx.x, 8u) : 0u;
+    auto word_at = [](uint32_t a) {  // 4 bytes at any shared byte address
+        const uint32_t w = a & ~3u;
+        return __funnelshift_r(lds_u32(w), lds_u32(w + 4), (a & 3) * 8);
+    };
+    const uint32_t w0 = word_at(a_r + 8 * threadIdx.x) & __funnelshift_lc(0xFFFFFFFFu, 0u, 8 * min(nt, 4u));
+    const uint32_t w1 = word_at(a_r + 8 * threadIdx.x + 4) & __funnelshift_lc(0xFFFFFFFFu, 0u, 8 * (nt > 4 ? nt - 4 : 0u));
+    // a byte > K sets its top bit here (bytes >= 128 already have it)
+    constexpr uint32_t KB = (0x7Fu - (uint32_t)KK) * 0x01010101u;
+    const bool rbad = (((w0 + KB) | w0 | (w1 + KB) | w1) & 0x80808080u) != 0;  // sparse.py:88-89
+    const uint32_t s0 = __dp4a(w0, 0x01010101u, 0u);
+    const uint32_t sum = __dp4a(w1, 0x01010101u, s0);
     uint32_t tot;
-    uint32_t ex = block_exclusive_scan<ROW_THREADS>(sum, s_scan, &tot);
+    uint32_t ex = block_exclusive_scan<SMALL8_THREADS>(sum, s_scan, &tot);
     if (rbad) s_bad = 1;
     if (sums) {
         if (threadIdx.x == 0 && (tot != own || (r0 + nrow == N && (uint64_t)cbase + tot != nnz)))  // sparse.py:84-87
@@ -578,45 +592,49 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
         cbase = block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
     }
     if (s_bad) {  // from here on tot <= nrow * KK and cbase + tot <= nnz
+        cp_async_wait<0>();  // no copy may land after the CTA is gone
         if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
         return;
     }
-#pragma unroll
-    for (uint32_t j = 0; j < PER; ++j) {
-        const uint32_t i = threadIdx.x * PER + j;
-        s_off[i] = (uint16_t)ex;
-        ex += i < nrow ? (uint32_t)s_r[rsh + i] : 0u;  // <= KK here (checked)
+    {
+        // byte k of w * 0x01010100 = sum of bytes < k; byte 0 is 0, which
+        // PRMT also uses as the zero filler: entry = [pfx_k, 0, r_k, 0] + ex
+        const uint32_t p0 = w0 * 0x01010100u, p1 = w1 * 0x01010100u;
+        const uint32_t e1 = ex + s0;
+        uint4* dst = reinterpret_cast<uint4*>(s_or) + 2 * threadIdx.x;
+        dst[0] = make_uint4(__byte_perm(p0, w0, 0x0400) + ex, __byte_perm(p0, w0, 0x0501) + ex,
+                            __byte_perm(p0, w0, 0x0602) + ex, __byte_perm(p0, w0, 0x0703) + ex);
+        dst[1] = make_uint4(__byte_perm(p1, w1, 0x0400) + e1, __byte_perm(p1, w1, 0x0501) + e1,
+                            __byte_perm(p1, w1, 0x0602) + e1, __byte_perm(p1, w1, 0x0703) + e1);
     }
     if (!sums) {  // look-back path: the windows are known only now
         csh = stage_window(s_c, d + nnz + cbase, tot);
         vsh = stage_window(s_v, d + cbase, tot);
+        cp_async_commit();
     }
+    cp_async_wait<0>();
     __syncthreads();
     float* orow0 = p.out + p.out_off[b] + r0 * KK;
     const bool vec_ok = VEC || (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
     bool bad = false;
     // explicit 32-bit shared addresses (see lds_u32)
-    const uint32_t a_off = (uint32_t)__cvta_generic_to_shared(s_off);
-    const uint32_t a_r = (uint32_t)__cvta_generic_to_shared(s_r) + rsh;
+    const uint32_t a_or = (uint32_t)__cvta_generic_to_shared(s_or);
     const uint32_t a_c = (uint32_t)__cvta_generic_to_shared(s_c) + csh;
     const uint32_t a_v = (uint32_t)__cvta_generic_to_shared(s_v) + vsh;
     const uint32_t a_pk = (uint32_t)__cvta_generic_to_shared(s_pk);
     const uint32_t a_sel = (uint32_t)__cvta_generic_to_shared(s_sel);
     const uint32_t a_lut4 = (uint32_t)__cvta_generic_to_shared(s_lut4);
     const uint32_t a_lut = (uint32_t)__cvta_generic_to_shared(s_lut);
-    auto word_at = [](uint32_t a) {  // 4 bytes at any shared byte address
-        const uint32_t w = a & ~3u;
-        return __funnelshift_r(lds_u32(w), lds_u32(w + 4), (a & 3) * 8);
-    };
 #pragma unroll 2
     for (uint32_t j = 0; j < PER; ++j) {
-        const uint32_t li = j * ROW_THREADS + threadIdx.x;
+        const uint32_t li = j * SMALL8_THREADS + threadIdx.x;
         if (li >= nrow) break;
-        const uint32_t off = lds_u16(a_off + 2 * li), r = lds_u8(a_r + li);
+        const uint32_t e = lds_u32(a_or + 4 * li);  // offset | r << 16
+        const uint32_t off = e & 0xFFFFu, r = e >> 16;
         const uint32_t cw = word_at(a_c + off);  // bytes past r are ignored
         const uint32_t vw = word_at(a_v + off);
         uint32_t mask, vs;
-        const uint32_t live = r >= 4 ? 0xFFFFFFFFu : ((1u << (8 * r)) - 1u);
+        const uint32_t live = __funnelshift_lc(0xFFFFFFFFu, 0u, 8 * r);  // low r bytes
         if constexpr (KK == 4) {
             // one table entry per row: the two low bits of the four column
             // bytes gathered by a multiply, (r, idx) -> selector, mask, valid;
@@ -640,7 +658,8 @@ __global__ void __launch_bounds__(ROW_THREADS, SUMS ? 6 : 1) k_rows_small8(RowPa
         float o[KK];
 #pragma unroll
         for (int col = 0; col < KK; ++col) {
-            const float val = __uint_as_float(lds_u32(a_lut + 4 * ((vs >> (8 * col)) & 0xFFu)));
+            const uint32_t sh = col == 0 ? (vs << 2) : (vs >> (8 * col - 2));
+            const float val = __uint_as_float(lds_u32(a_lut | (sh & 0x3FCu)));
             o[col] = (mask >> col) & 1u ? val : 0.0f;
         }
         float* orow = orow0 + (uint64_t)li * KK;

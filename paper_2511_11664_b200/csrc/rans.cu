@@ -164,6 +164,7 @@ struct DecParams {
     // u8 tensors with K in {1, 2, 4} into chunk_state (k_rows_small8 reads
     // the prefix instead of looking back)
     int chunk_sums;
+    float* dq_lut;  // optional [B][256]: dequantised value of every u8 symbol (k_rows_small8)
 };
 
 constexpr uint32_t LUT_SLICE = 2048;  // slots per k_dec_prepare slice CTA
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(256) k_dec_prepare(DecParams p) {
     __shared__ uint32_t s_scan[33];
     __shared__ int s_bad;
     if (threadIdx.x == 0) s_bad = 0;
+    if (p.dq_lut) build_dequant_lut(p.dq_lut + (uint64_t)b * 256, (double)in.zero_point, in.scale);
     if (p.chunk_state)
         for (uint32_t i = threadIdx.x; i < p.nchunk_cap; i += blockDim.x)
             p.chunk_state[(uint64_t)b * p.nchunk_cap + i] = 0ull;
