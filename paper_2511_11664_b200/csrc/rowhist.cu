@@ -101,7 +101,16 @@ __device__ void rowhist_swar(const uint32_t* bm, uint32_t w0, uint32_t w1, uint3
     uint32_t c[K + 1];
 #pragma unroll
     for (int v = 0; v <= K; ++v) c[v] = 0;
-    for (uint32_t w = w0 + threadIdx.x; w < w1; w += RH_THREADS) swar_counts<K>(__ldg(bm + w), c);
+    // four loads in flight per thread (the bitmap is L2-resident: latency-bound)
+    uint32_t w = w0 + threadIdx.x;
+    for (; w + 3 * RH_THREADS < w1; w += 4 * RH_THREADS) {
+        uint32_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(bm + w + u * RH_THREADS);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) swar_counts<K>(v[u], c);
+    }
+    for (; w < w1; w += RH_THREADS) swar_counts<K>(__ldg(bm + w), c);
     __shared__ uint32_t s_c[9];
     if (threadIdx.x <= K) s_c[threadIdx.x] = 0;
     __syncthreads();
@@ -144,7 +153,22 @@ __global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__
         const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         for (uint32_t v = 0; v <= K; ++v) s_h[warp][v][lane] = 0;
         const uint32_t kmask = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
-        for (uint32_t r = u0 + threadIdx.x; r < r1; r += RH_THREADS) {
+        uint32_t r = u0 + threadIdx.x;
+        if (K <= 32) {  // four rows (eight loads) in flight per thread
+            for (; r + 3 * RH_THREADS < r1; r += 4 * RH_THREADS) {
+                uint32_t lo[4], hi[4], sh[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t start = (r + u * RH_THREADS) * K;  // < 2^32: T < 2^31
+                    sh[u] = start & 31;
+                    lo[u] = __ldg(bm + (start >> 5));
+                    hi[u] = __ldg(bm + (start >> 5) + 1);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) s_h[warp][__popc(__funnelshift_r(lo[u], hi[u], sh[u]) & kmask)][lane] += 1;
+            }
+        }
+        for (; r < r1; r += RH_THREADS) {
             const uint64_t start = (uint64_t)r * K;
             const uint32_t w = (uint32_t)(start >> 5), s = (uint32_t)(start & 31);
             uint32_t v;
