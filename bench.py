@@ -235,7 +235,10 @@ class ClockSampler:
         loaded = [m for m, _, u in self.samples if u > 0] or [m for m, _, _ in self.samples]
         return dict(sm_mhz=statistics.median(loaded), sm_max_mhz=self.max_mhz, reasons=sorted(reasons),
                     samples=len(self.samples), samples_under_load=sum(1 for s in self.samples if s[2] > 0),
-                    source="NVML, polled every ~2 ms during the timed region")
+                    source="NVML, polled every ~2 ms during the timed region",
+                    note="samples_under_load counts NVML utilization > 0, a trailing average over >= 1/6 s: "
+                         "a timed region of ~0.1 s after an idle phase can read 0 while every sample "
+                         "was taken with the GPU busy")
 
 
 def gpu_local_cpus(torch, device):

@@ -280,9 +280,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // Programmatic dependent launch: pipeline kernels are launched with the
-// PDL attribute so their launch overlaps the predecessor's tail; each one
-// waits here, before touching memory, until the predecessor grid has
-// completed and flushed (a no-op when launched without the attribute).
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// PDL attribute; each one waits here, before touching memory, until the
+// predecessor grid has completed and flushed, then at once allows its own
+// dependent grid to launch (it becomes resident and parks in its own wait,
+// so its launch latency hides behind this kernel instead of following it).
+// Every PDL kernel calls this first, before any early return, so completion
+// is transitive along the chain.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 
 }  // namespace scz
