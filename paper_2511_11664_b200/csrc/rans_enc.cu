@@ -237,14 +237,18 @@ __device__ __forceinline__ EncTab enc_tab_fast(const EncTab& e, int n) {
     }
     return f;
 }
-__device__ __forceinline__ void enc_apply_ring(EncLane& L, const EncTab& t, bool live, uint32_t gtm, uint8_t* ob) {
+// obs: the warp's ring as a 32-bit shared address (plus the masked position;
+// not OR'd: static shared offsets start after the reserved 1 KB, so the
+// ring base is not ENC_RB-aligned in the address space).
+__device__ __forceinline__ void enc_apply_ring(EncLane& L, const EncTab& t, bool live, uint32_t gtm, uint32_t obs) {
     const bool e1 = live && L.x >= t.freq;
-    const bool e2 = live && (L.x >> 8) >= t.freq;
+    const bool e2 = live && (L.x >> 8) >= t.freq;  // implies e1
     const uint32_t b1 = __ballot_sync(0xffffffffu, e1);
     const uint32_t b2 = __ballot_sync(0xffffffffu, e2);
-    const uint32_t pos = L.emitted + __popc(b1 & gtm) + __popc(b2 & gtm) + 1;
-    if (e1) ob[(0u - pos) & (ENC_RB - 1)] = (uint8_t)L.x;
-    if (e2) ob[(0u - pos - 1) & (ENC_RB - 1)] = (uint8_t)(L.x >> 8);
+    // bytes before this lane's first: ring positions -(n + 1), -(n + 2)
+    const uint32_t n = L.emitted + __popc(b1 & gtm) + __popc(b2 & gtm);
+    sts_u8_if(obs + (~n & (ENC_RB - 1)), L.x, e1);
+    sts_u8_if(obs + (~(n + 1) & (ENC_RB - 1)), L.x >> 8, e2);
     L.emitted += __popc(b1) + __popc(b2);
     const uint32_t x = e2 ? (L.x >> 16) : (e1 ? (L.x >> 8) : L.x);
     const uint32_t q = __funnelshift_r(__umulhi(x, t.rcp), 0u, t.shift);
@@ -299,6 +303,7 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
         __shared__ __align__(16) uint8_t s_ring[ENC2_WPB][2][1024];
         __shared__ __align__(16) uint8_t s_ob[ENC2_WPB][ENC_RB];
         uint8_t* ob = s_ob[warp];
+        const uint32_t obs = (uint32_t)__cvta_generic_to_shared(ob);
         uint32_t flushed = 0;  // bytes already in the slot (multiple of 16)
         auto flush = [&]() {   // every complete 16-byte chunk since the last flush
             const uint32_t upto = E.emitted & ~15u;
@@ -334,23 +339,25 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
                     if (s == s_top) {  // the highest step may be partial
                         const bool act = (uint32_t)s * 32 + lane < len;
                         t = s_tab[act ? rs[(s & 31) * 32] : 0];
-                        enc_apply_ring(E, t, act, gtm, ob);
+                        enc_apply_ring(E, t, act, gtm, obs);
                         --s;
                     }
                     // groups of four steps: the four table entries are loaded
                     // up front (symbols do not depend on the state)
 #pragma unroll 1
                     for (; s - 3 >= lo; s -= 4) {
-                        const EncTab t0 = s_tab[rs[(s & 31) * 32]];
-                        const EncTab t1 = s_tab[rs[((s - 1) & 31) * 32]];
-                        const EncTab t2 = s_tab[rs[((s - 2) & 31) * 32]];
-                        const EncTab t3 = s_tab[rs[((s - 3) & 31) * 32]];
-                        enc_apply_ring(E, t0, true, gtm, ob);
-                        enc_apply_ring(E, t1, true, gtm, ob);
-                        enc_apply_ring(E, t2, true, gtm, ob);
-                        enc_apply_ring(E, t3, true, gtm, ob);
+                        // s - 3 .. s lie in one half-chunk: no wrap, one base
+                        const uint8_t* rp = rs + (s & 31) * 32;
+                        const EncTab t0 = s_tab[rp[0]];
+                        const EncTab t1 = s_tab[rp[-32]];
+                        const EncTab t2 = s_tab[rp[-64]];
+                        const EncTab t3 = s_tab[rp[-96]];
+                        enc_apply_ring(E, t0, true, gtm, obs);
+                        enc_apply_ring(E, t1, true, gtm, obs);
+                        enc_apply_ring(E, t2, true, gtm, obs);
+                        enc_apply_ring(E, t3, true, gtm, obs);
                     }
-                    for (; s >= lo; --s) enc_apply_ring(E, s_tab[rs[(s & 31) * 32]], true, gtm, ob);
+                    for (; s >= lo; --s) enc_apply_ring(E, s_tab[rs[(s & 31) * 32]], true, gtm, obs);
                     __syncwarp();
                     flush();
                 }
