@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
         const uint32_t wa = ring_s + (a & (DRING - 4));
         const uint32_t w0 = lds_u32(wa);
         const uint32_t w1 = lds_u32(wa + 4);
-        const uint32_t v = __funnelshift_r(w0, w1, (a & 3) * 8);
+        const uint32_t v = __funnelshift_r(w0, w1, a * 8);  // the shift is taken mod 32
         const uint32_t sel = p2 ? 0x1045u : (p1 ? 0x2104u : 0x3210u);
         x = __byte_perm(x, v, sel);
         cur += __popc(b1) + __popc(b2);
