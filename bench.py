@@ -63,7 +63,7 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--format", type=int, default=2, choices=[1, 2])
     ap.add_argument("--block-syms", type=int, default=8192)
-    ap.add_argument("--contexts", type=int, default=int(os.environ.get("SCZ_BENCH_CONTEXTS", "3")),
+    ap.add_argument("--contexts", type=int, default=int(os.environ.get("SCZ_BENCH_CONTEXTS", "6")),
                     help="library contexts the device-resident steps rotate over (>= 2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="bounded CPU-baseline sample (rank 0, N=1)")
@@ -341,7 +341,7 @@ def run_ours(args):
         return float(t.item())
 
     # ---- device-resident timed region -------------------------------------
-    # Library contexts (own stream + scratch each; --contexts, default 3)
+    # Library contexts (own stream + scratch each; --contexts, default 6)
     # rotate between steps: step i + 2's encode is queued before the host
     # reads step i's headers (scz_batch_sync) and queues its decode, so the
     # GPU never idles on the host round trip.  Every step still compresses and decompresses
