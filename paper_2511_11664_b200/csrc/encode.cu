@@ -284,16 +284,17 @@ __device__ __noinline__ uint32_t quant_exact(float x, double scale, double zf, d
     return (uint32_t)r;
 }
 
-// fp32 estimate y = x * fl32(1/s) + z has |error| < 2^-14.4; any
-// y within 2^-12 of a rounding boundary k + 1/2 is recomputed exactly.
+// fp32 estimate y = x * fl32(1/s) + z has |error| < 2^-15.4; any
+// y within QGUARD = 2^-13 of a rounding boundary k + 1/2 is recomputed exactly.
+constexpr float QGUARD = 0x1p-13f;
 __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, int qmax,
                                                double scale, double zf, bool fast) {
     if (fast) {
-        // d = y - rint(y) is exact; y lies within 2^-12 of a half-integer
-        // iff |d| >= 1/2 - 2^-12, and only those take the exact path
+        // d = y - rint(y) is exact; y lies within QGUARD of a half-integer
+        // iff |d| >= 1/2 - QGUARD, and only those take the exact path
         const float y = fmaf(x, r32, zf32);
         const float rq = rintf(y);
-        if (fabsf(y - rq) < 0.5f - 0x1p-12f) {
+        if (fabsf(y - rq) < 0.5f - QGUARD) {
             const int q = (int)rq;
             return (uint32_t)min(max(q, 0), qmax);
         }
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 5) k_quantize(QuantParams p) {
     // every element and a store predicated on its bitmap bit.  In the fast
     // path the estimate's rint lies in [0, qmax] (y >= -1/2 and y <= qmax + 1/2
     // up to rounding, since lo <= x <= hi and z = round(-lo / s), and elements
-    // within 2^-12 of a half-integer are excluded), so the symbol is the low
+    // within QGUARD of a half-integer are excluded), so the symbol is the low
     // byte of y + 1.5 * 2^23 and needs no clamp.  A bit per group of four
     // collects "an element is near a rounding boundary (or the scale is out of
     // the fp32 range)"; such groups are redone afterwards, the elements near a
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 5) k_quantize(QuantParams p) {
             const float y = fmaf(e[j], r32, zf32);
             const float t = __fadd_rn(y, 0x1.8p23f);
             const float rq = __fsub_rn(t, 0x1.8p23f);
-            sl |= !(fabsf(__fsub_rn(y, rq)) < 0.5f - 0x1p-12f);
+            sl |= !(fabsf(__fsub_rn(y, rq)) < 0.5f - QGUARD);
             if constexpr (SYM_OUT) {
                 // caller-supplied parameters: x may lie outside the range
                 const uint32_t q = (uint32_t)min(max(__float_as_int(t) - 0x4B400000, 0), qmax);
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 5) k_quantize(QuantParams p) {
             const float x = xb[tile_base + off];
             const float y = fmaf(x, r32, zf32);
             const float rq = __fsub_rn(__fadd_rn(y, 0x1.8p23f), 0x1.8p23f);
-            if (fast && fabsf(__fsub_rn(y, rq)) < 0.5f - 0x1p-12f) continue;
+            if (fast && fabsf(__fsub_rn(y, rq)) < 0.5f - QGUARD) continue;
             const int bit = 4 * (lane & 7) + j;
             const uint32_t q = quant_exact(x, scale, zf, (double)qmax);
             if ((wbits >> bit) & 1u) s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;

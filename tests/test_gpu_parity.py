@@ -164,6 +164,33 @@ def test_quantize_matches_oracle_random():
         assert np.array_equal(out.data.view(np.uint32), orc.dequantize(qo, mo, s, z).view(np.uint32))
 
 
+def test_pipeline_guard_band_planted_boundaries():
+    """The batch pipeline's quantiser (unclamped magic-constant symbols, 2^-13
+    guard band, deferred fp64 path) against the oracle on tensors whose
+    values sit on and one ulp around rounding boundaries: v1 containers
+    byte-identical, v2 containers identical to the oracle's."""
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        q_bits = (8, 4, 2, 6, 8, 3)[trial]
+        n = 96 * 1024
+        x = (rng.laplace(0, 1, n) * (1e-2, 1.0, 300.0)[trial % 3]).astype(np.float32)
+        if trial % 2 == 0:
+            x = np.abs(x)  # post-ReLU: z = 0
+        x[rng.random(n) < 0.4] = 0.0
+        s, z = orc.params_for(x, q_bits)
+        k = rng.integers(0, (1 << q_bits) - 1, 20000)
+        planted = ((k + 0.5 - z) * s).astype(np.float32)
+        lo, hi = x.min(), x.max()
+        planted = np.clip(planted, lo, hi)  # keep the tensor's range (and params)
+        idx = rng.integers(0, n, planted.size)
+        x[idx] = np.nextafter(planted, planted + rng.choice([-1, 0, 1], planted.size).astype(np.float32))
+        t = sz.FeatureTensor((n,), x)
+        for fmt in (1, 2):
+            c = sz.compress(t, q_bits, format=fmt)
+            ref = orc.compress(x, (n,), q_bits, None if fmt == 1 else c.n_rows, fmt=fmt)
+            assert container.to_bytes(c) == orc.to_bytes(ref), (trial, fmt)
+
+
 def test_csr_kat_and_corruption():
     # test_sparse.py:38-101
     q = sz.QuantizedMatrix(2, 3, [0, 5, 0, 3, 0, 2], [True, False, True, False, True, False])
