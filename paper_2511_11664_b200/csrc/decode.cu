@@ -20,7 +20,7 @@ namespace scz {
 constexpr int ROW_CHUNK = 1024;     // max rows per chunk
 constexpr int OUT_ELEMS = 4096;     // dense fp32 elements staged per chunk
 constexpr int ROW_THREADS = 256;
-constexpr int SMALL8_THREADS = 128;  // k_rows_small8: SMALL_ROWS / 8 rows per thread
+constexpr int SMALL8_THREADS = 256;  // k_rows_small8: SMALL_ROWS / 8 rows per thread
 
 __host__ __device__ inline uint32_t rows_per_chunk(uint32_t K) {
     const uint32_t r = K ? (uint32_t)OUT_ELEMS / K : (uint32_t)ROW_CHUNK;
@@ -466,7 +466,7 @@ __global__ void k_init_row_lut() {
 // output row is KK * 4-byte aligned (host-checked), so rows leave with one
 // vector store and no alignment test.
 template <int KK, bool SUMS, bool VEC = false>
-__global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 12 : 1) k_rows_small8(RowParams p) {
+__global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(RowParams p) {
     static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;

@@ -12,7 +12,7 @@
 
 namespace scz {
 
-constexpr uint32_t SMALL_ROWS_DEC = 1024;  // == SMALL_ROWS (decode.cu)
+constexpr uint32_t SMALL_ROWS_DEC = 2048;  // == SMALL_ROWS (decode.cu)
 constexpr int DEC2_WPB = 16;         // warps (= blocks) per CTA, throughput mode
 constexpr int DEC2_WPB_SMALL = 4;    // latency mode (grid would not fill the GPU)
 constexpr int DCHUNK = 256;          // bytes per cp.async chunk (8 per lane)
