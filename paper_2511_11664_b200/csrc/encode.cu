@@ -620,10 +620,19 @@ __device__ __forceinline__ void materialize_body(const MatParams& p, uint8_t* s_
         if (rr >= K) rr -= K;
         const uint32_t m = (uint32_t)rr;
         if ((K & (K - 1)) == 0 && K <= 32) {  // K | 32: m == 0, c = bit mod K
-            while (w) {
-                const int bit = __ffs(w) - 1;
-                w &= w - 1;
-                s_c[lrank++] = (S)(bit & (K - 1));
+            if constexpr (sizeof(S) == 1) {
+                // all 32 bit positions, predicated (no per-lane trip count,
+                // no bit scans): c = j mod K lands at the next rank slot
+                uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_c) + lrank;
+                const uint32_t km = K - 1;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sts_u8_bump(sa, (uint32_t)j & km, w, 1u << j);
+            } else {
+                while (w) {
+                    const int bit = __ffs(w) - 1;
+                    w &= w - 1;
+                    s_c[lrank++] = (S)(bit & (K - 1));
+                }
             }
         } else {
             while (w) {
@@ -643,10 +652,21 @@ __device__ __forceinline__ void materialize_body(const MatParams& p, uint8_t* s_
         uint8_t* s_rc = s_buf + TILE + 32;  // (u8 columns use the first TILE + 32 bytes)
         const uint32_t kmask = K == 32 ? 0xffffffffu : ((1u << K) - 1u);
         const uint32_t nr = (uint32_t)(i1 - i0);
-        for (uint32_t j = threadIdx.x; j < nr; j += TILE_THREADS) {
-            const uint32_t start = (uint32_t)((i0 + j) * K - ts);  // < TILE
-            const uint32_t wi = start >> 5, sh = start & 31;
-            s_rc[j] = (uint8_t)__popc(__funnelshift_r(s_w[wi], s_w[wi + 1], sh) & kmask);
+        if (K == 4) {
+            // K = 4 divides the tile: thread t's bitmap word holds rows
+            // 8t .. 8t + 7 as nibbles; SWAR nibble popcounts, spread to bytes
+            static_assert(TILE % 4 == 0 && TILE_WORDS == TILE_THREADS, "one word per thread");
+            const uint32_t ww = s_w[threadIdx.x];
+            uint32_t x = ww - ((ww >> 1) & 0x55555555u);
+            x = (x & 0x33333333u) + ((x >> 2) & 0x33333333u);
+            const uint32_t lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;
+            reinterpret_cast<uint2*>(s_rc)[threadIdx.x] = make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
+        } else {
+            for (uint32_t j = threadIdx.x; j < nr; j += TILE_THREADS) {
+                const uint32_t start = (uint32_t)((i0 + j) * K - ts);  // < TILE
+                const uint32_t wi = start >> 5, sh = start & 31;
+                s_rc[j] = (uint8_t)__popc(__funnelshift_r(s_w[wi], s_w[wi + 1], sh) & kmask);
+            }
         }
         __syncthreads();
         block_copy_s2g<TILE_THREADS>(reinterpret_cast<uint8_t*>(cr + base_rank),
