@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import gc
 import json
 import math
 import os
@@ -403,6 +404,8 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(NC)]
     clocks = ClockSampler(local)
+    gc.collect()
+    gc.disable()  # no collector pause while the host feeds the queue
     with clocks:
         barrier()
         ev0.record(streams[0])
@@ -412,6 +415,7 @@ def run_ours(args):
         for k in range(NC):
             ev_end[k].record(streams[k])
         barrier()
+    gc.enable()
     launches = sum(c.launches for c in ctxs) - l0
     # per-step completion gaps on the device (decode-end to decode-end)
     done = [ev0.elapsed_time(e) for e in step_ev]
