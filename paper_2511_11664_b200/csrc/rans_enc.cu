@@ -250,7 +250,9 @@ __device__ __forceinline__ void enc_apply_ring(EncLane& L, const EncTab& t, bool
     sts_u8_if(obs + (~n & (ENC_RB - 1)), L.x, e1);
     sts_u8_if(obs + (~(n + 1) & (ENC_RB - 1)), L.x >> 8, e2);
     L.emitted += __popc(b1) + __popc(b2);
-    const uint32_t x = e2 ? (L.x >> 16) : (e1 ? (L.x >> 8) : L.x);
+    uint32_t x = L.x;
+    if (e1) x >>= 8;  // two predicated shifts (e2 implies e1)
+    if (e2) x >>= 8;
     const uint32_t q = __funnelshift_r(__umulhi(x, t.rcp), 0u, t.shift);
     const uint32_t xn = x + t.cum + q * (t.shift >> 16);
     if (live) L.x = xn;
