@@ -64,6 +64,8 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--format", type=int, default=2, choices=[1, 2])
     ap.add_argument("--block-syms", type=int, default=8192)
+    ap.add_argument("--serialize", type=int, default=int(os.environ.get("SCZ_BENCH_SERIALIZE", "1")),
+                    help="1: the rotating contexts' batch calls run in queue order (event chain)")
     ap.add_argument("--contexts", type=int, default=int(os.environ.get("SCZ_BENCH_CONTEXTS", "6")),
                     help="library contexts the device-resident steps rotate over (>= 2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -359,18 +361,39 @@ def run_ours(args):
     infos = [(_native.Info * B)() for _ in range(NC)]
     outs = [out_dev] + [torch.empty_like(x_dev) for _ in range(NC - 1)]
 
+    # --serialize (default): every queued batch call waits for the one
+    # queued before it (an event chain across the context streams), so the
+    # device runs the steps' kernels in queue order instead of interleaving
+    # kernels of several contexts; the header read-back of a step still waits
+    # only for that step's encode.
+    chain_ev = [None]
+
+    def chain(k):
+        if args.serialize and chain_ev[0] is not None:
+            streams[k].wait_event(chain_ev[0])
+
+    def mark(k):
+        if args.serialize:
+            e = torch.cuda.Event()
+            e.record(streams[k])
+            chain_ev[0] = e
+
     def enc(k):
         c = ctxs[k]
+        chain(k)
         c.check(lib.scz_encode_batch(c.h, ctypes.c_void_p(x_dev.data_ptr()), T, B, wl["q"], -1, 14,
                                      args.format, 32, args.block_syms, ctypes.byref(batches[k])))
+        mark(k)
 
     def dec(k):
         c = ctxs[k]
         c.check(lib.scz_batch_sync(c.h, ctypes.byref(batches[k]), infos[k]))
+        chain(k)
         c.check(lib.scz_decode_batch_async(c.h, infos[k], B, ctypes.c_void_p(batches[k].d_freqs),
                                            ctypes.c_void_p(batches[k].d_block_bytes),
                                            ctypes.c_void_p(batches[k].d_payload),
                                            ctypes.c_void_p(outs[k].data_ptr())))
+        mark(k)
 
     host_ms = []  # host time spent queueing each step (diagnostic)
     step_ev = []  # (stream, event) after each step's decode (diagnostic)
