@@ -457,7 +457,8 @@ __global__ void __launch_bounds__(128) k_colhist(ColHistParams p) {
     pdl_wait();
     const uint32_t q = blockIdx.x * 128 + threadIdx.x;
     const uint32_t b = blockIdx.z;
-    if (q >= p.period_words) return;
+    const bool single = gridDim.y == 1;  // this CTA alone covers its columns
+    if (q >= p.period_words && !single) return;
     const uint32_t r0 = blockIdx.y * p.rows_per_cta;
     const uint32_t r1 = min(p.n_rows, r0 + p.rows_per_cta);
     const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad;
@@ -494,6 +495,18 @@ __global__ void __launch_bounds__(128) k_colhist(ColHistParams p) {
         if (pending > 11) flush();
     }
     flush();
+    if (single) {
+        // the only contribution to these counters: plain stores, transposed
+        // through shared memory so each warp writes 128 contiguous bytes
+        __shared__ uint32_t s_cnt[128 * 33];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s_cnt[threadIdx.x * 33 + i] = cnt[i];
+        __syncthreads();
+        uint32_t* hp = p.hp + (uint64_t)b * p.hp_stride + (uint64_t)blockIdx.x * 128 * 32;
+        const uint32_t nw = min(128u, p.period_words - blockIdx.x * 128) * 32;
+        for (uint32_t w = threadIdx.x; w < nw; w += 128) hp[w] = s_cnt[(w >> 5) * 33 + (w & 31)];
+        return;
+    }
     uint32_t* hp = p.hp + (uint64_t)b * p.hp_stride + q * 32;
 #pragma unroll
     for (int i = 0; i < 32; ++i)
