@@ -68,7 +68,7 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--format", type=int, default=2, choices=[1, 2])
     ap.add_argument("--block-syms", type=int, default=8192)
-    ap.add_argument("--serialize", type=int, default=int(os.environ.get("SCZ_BENCH_SERIALIZE", "1")),
+    ap.add_argument("--serialize", type=int, default=int(os.environ.get("SCZ_BENCH_SERIALIZE", "0")),
                     help="1: the rotating contexts' batch calls run in queue order (event chain)")
     ap.add_argument("--contexts", type=int, default=int(os.environ.get("SCZ_BENCH_CONTEXTS", "6")),
                     help="library contexts the device-resident steps rotate over (>= 2)")
@@ -365,7 +365,7 @@ def run_ours(args):
     infos = [(_native.Info * B)() for _ in range(NC)]
     outs = [out_dev] + [torch.empty_like(x_dev) for _ in range(NC - 1)]
 
-    # --serialize (default): every queued batch call waits for the one
+    # --serialize 1: every queued batch call waits for the one
     # queued before it (an event chain across the context streams), so the
     # device runs the steps' kernels in queue order instead of interleaving
     # kernels of several contexts; the header read-back of a step still waits
