@@ -178,6 +178,11 @@ int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch,
                          int32_t* h_status);
 
 /* ---- instrumentation ---------------------------------------------------- */
+/* Device time (CUDA events) of the last host-buffer call on ctx
+ * (scz_compress, scz_decompress, scz_compress_batch, scz_decompress_batch):
+ * from its first host->device copy to its last device->host copy.  Replaces
+ * the wall clock of bench._time_ms (bench.py:88-98) for enc_ms / dec_ms. */
+int scz_last_call_ms(scz_ctx* ctx, float* ms);
 /* Per-kernel CUDA-event timing on the context stream (off by default). */
 int scz_ctx_set_timing(scz_ctx* ctx, int enable);
 /* "name total_ms launches\n" lines accumulated since the last read. */

@@ -79,7 +79,7 @@ EXPORTS = (
     "scz_decode_batch", "scz_decode_batch_async", "scz_decode_status", "scz_decode_batch_device", "scz_quantize",
     "scz_quantize_params", "scz_dequantize", "scz_csr_encode", "scz_csr_decode", "scz_build_counts",
     "scz_normalize", "scz_rans_encode", "scz_rans_decode", "scz_search", "scz_compress_batch",
-    "scz_decompress_batch", "scz_ctx_set_timing", "scz_ctx_read_timing",
+    "scz_decompress_batch", "scz_ctx_set_timing", "scz_ctx_read_timing", "scz_last_call_ms",
 )
 
 _lib = None
@@ -127,6 +127,7 @@ def load_library():
             "scz_decompress_batch": (I32, [P, P, U32, P, U64, P, U64, P, U64, P, P]),
             "scz_ctx_set_timing": (I32, [P, I32]),
             "scz_ctx_read_timing": (I32, [P, ctypes.c_char_p, U64]),
+            "scz_last_call_ms": (I32, [P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -176,6 +177,12 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self.lib.scz_launch_count(self.h))
+
+    def last_call_ms(self) -> float:
+        """CUDA-event device time of the last host-buffer call (scz_last_call_ms)."""
+        ms = ctypes.c_float()
+        self.check(self.lib.scz_last_call_ms(self.h, ctypes.byref(ms)))
+        return float(ms.value)
 
     def set_timing(self, enable: bool) -> None:
         self.check(self.lib.scz_ctx_set_timing(self.h, 1 if enable else 0))

@@ -286,6 +286,23 @@ struct scz_ctx {
         last_ev = nullptr;
     }
 
+    // Device span of the last host-buffer call (scz_compress / scz_decompress
+    // and their _batch forms): events around its first H2D copy and its last
+    // D2H copy, read by scz_last_call_ms (bench.measure's enc_ms / dec_ms).
+    cudaEvent_t call_ev[2] = {nullptr, nullptr};
+    bool call_done = false;
+    int call_begin(cudaStream_t s) {
+        call_done = false;
+        for (cudaEvent_t& e : call_ev)
+            if (!e && cudaEventCreate(&e) != cudaSuccess) return cuda(cudaGetLastError(), "cudaEventCreate");
+        return cuda(cudaEventRecord(call_ev[0], s), "cudaEventRecord");
+    }
+    int call_end(cudaStream_t s) {
+        int st = cuda(cudaEventRecord(call_ev[1], s), "cudaEventRecord");
+        call_done = st == SCZ_OK;
+        return st;
+    }
+
     int fail(int code, const char* fmt, ...) {
         char buf[512];
         va_list ap;
@@ -1265,6 +1282,8 @@ void scz_ctx_destroy(scz_ctx* ctx) {
         cudaStreamDestroy(ctx->xfer_out);
     }
     for (cudaEvent_t e : ctx->xev) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->call_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->sync_ev) cudaEventDestroy(ctx->sync_ev);
     for (auto& g : ctx->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -1402,6 +1421,7 @@ int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64
     int st = plan_encode_cached(ctx, total, 1, q_bits, n_rows, precision, format, lanes, block_syms, &pl);
     if (st) return st;
     CK(ctx->x_in.ensure(total * 4));
+    if ((st = ctx->call_begin(ctx->stream)) != SCZ_OK) return st;
     CK(cudaMemcpyAsync(ctx->x_in.p, x, total * 4, cudaMemcpyHostToDevice, ctx->stream));
     const std::string key = key_of("enc", {(uint64_t)(uintptr_t)ctx->x_in.p, total, 1, (uint64_t)q_bits,
                                            (uint64_t)n_rows, (uint64_t)precision, (uint64_t)format,
@@ -1427,6 +1447,7 @@ int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_blocks.p, ctx->block_len.as<uint32_t>() + info->blocks_off,
                        (size_t)info->n_blocks * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((st = ctx->call_end(ctx->stream)) != SCZ_OK) return st;
     CK(cudaStreamSynchronize(ctx->stream));
     if (freqs) *freqs = ctx->h_freqs.as<uint32_t>();
     if (block_bytes) *block_bytes = ctx->h_blocks.as<uint32_t>();
@@ -1461,6 +1482,7 @@ int scz_decompress(scz_ctx* ctx, const scz_info* info_in, const uint32_t* freqs,
     CK(ctx->dfreqs.ensure((size_t)in.alphabet * 4));
     CK(ctx->dblocks.ensure((size_t)in.n_blocks * 4));
     CK(ctx->dout.ensure(in.total * 4));
+    if ((st = ctx->call_begin(ctx->stream)) != SCZ_OK) return st;
     CK(cudaMemcpyAsync(ctx->dpayload.p, payload, in.payload_len, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->dfreqs.p, freqs, (size_t)in.alphabet * 4, cudaMemcpyHostToDevice, ctx->stream));
     if (in.version == 2)
@@ -1474,6 +1496,7 @@ int scz_decompress(scz_ctx* ctx, const scz_info* info_in, const uint32_t* freqs,
     CK(cudaStreamSynchronize(ctx->stream));
     if (dst != SCZ_OK) return ctx->fail(dst, "corrupt stream (device check failed)");
     CK(cudaMemcpyAsync(out, ctx->dout.p, in.total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((st = ctx->call_end(ctx->stream)) != SCZ_OK) return st;
     CK(cudaStreamSynchronize(ctx->stream));
     return SCZ_OK;
 }
@@ -1963,6 +1986,7 @@ int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t 
     CK(ctx->hb_freqs.ensure(ftot * 4));
     CK(ctx->hb_blocks.ensure(btot * 4));
     scz_info* hi = ctx->hb_info.as<scz_info>();
+    if ((st = ctx->call_begin(ctx->xfer)) != SCZ_OK) return st;
     // every chunk's features go up on the copy stream right away
     for (uint32_t c = 0; c < nch; ++c) {
         const uint32_t b0 = c * per, nb = b0 < batch ? std::min(per, batch - b0) : 0;
@@ -2025,6 +2049,7 @@ int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t 
         }
         ptot += cpt;
     }
+    if ((st = ctx->call_end(s)) != SCZ_OK) return st;
     CK(cudaStreamSynchronize(s));
     *infos = hi;
     if (payload) *payload = ctx->hb_payload.as<uint8_t>();
@@ -2061,6 +2086,7 @@ int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, c
     CK(ctx->dfreqs.ensure(freqs_count * 4 + 4));
     CK(ctx->dblocks.ensure(blocks_count * 4 + 4));
     CK(ctx->dout.ensure(out_total * 4));
+    if ((st = ctx->call_begin(ctx->xfer)) != SCZ_OK) return st;
     // copy stream: tables, then each chunk's payload range; compute stream:
     // decode chunk c; second copy stream: chunk c's features back to the
     // host while chunk c + 1 decodes
@@ -2101,8 +2127,20 @@ int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, c
                            cudaMemcpyDeviceToHost, ctx->xfer_out));
         out_base += n_out;
     }
+    CK(cudaEventRecord(ctx->xev[15], s));
+    CK(cudaStreamWaitEvent(ctx->xfer_out, ctx->xev[15], 0));
+    if ((st = ctx->call_end(ctx->xfer_out)) != SCZ_OK) return st;
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(ctx->xfer_out));
+    return SCZ_OK;
+}
+
+int scz_last_call_ms(scz_ctx* ctx, float* ms) {
+    if (!ctx || !ms) return SCZ_INVALID_INPUT;
+    if (!ctx->call_done) return ctx->fail(SCZ_INVALID_INPUT, "no completed host-buffer call on this context");
+    cudaSetDevice(ctx->device);
+    CK(cudaEventSynchronize(ctx->call_ev[1]));
+    CK(cudaEventElapsedTime(ms, ctx->call_ev[0], ctx->call_ev[1]));
     return SCZ_OK;
 }
 
