@@ -180,6 +180,10 @@ struct scz_ctx {
     int32_t* dstatus_cur = nullptr;  // statuses of the last run_decode (inside dinfo)
     // host staging
     HostBuf h_info, h_payload, h_freqs, h_blocks, h_status, h_misc;
+    static constexpr uint32_t NSTAGE = 4;  // pinned header staging slots of run_decode
+    HostBuf h_stage[NSTAGE];
+    cudaEvent_t stage_ev[NSTAGE] = {};
+    uint32_t stage_next = 0;
     int32_t* h_status_async = nullptr;
     uint32_t last_batch = 0;
     HostBuf hb_info, hb_payload, hb_freqs, hb_blocks;
@@ -219,6 +223,7 @@ struct scz_ctx {
         for (HostBuf* b : {&h_info, &h_payload, &h_freqs, &h_blocks, &h_status, &h_misc, &hb_info, &hb_payload,
                            &hb_freqs, &hb_blocks})
             f(b);
+        for (HostBuf& b : h_stage) f(&b);
     }
     // CUDA-graph cache: a launch sequence seen twice with the same key and
     // allocation generation is captured once and replayed afterwards.
@@ -629,6 +634,7 @@ int plan_encode_cached(scz_ctx* ctx, uint64_t T, uint32_t B, int q_bits, int64_t
 // The encode pipeline over a device batch.  cand_out (device) optional.
 int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_out,
                uint32_t* dump = nullptr) {
+    ctx->have_last_plan = false;  // the encode buffers no longer hold scz_encode_batch's batch
     const uint32_t B = pl.B;
     const uint64_t T = pl.T;
     cudaStream_t s = ctx->stream;
@@ -952,6 +958,12 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     return SCZ_OK;
 }
 
+// Stage entry points reuse the encode scratch: the batch a previous
+// scz_encode_batch left for scz_decode_batch_device is gone afterwards.
+inline void ctx_forget_batch(scz_ctx* ctx) {
+    if (ctx) ctx->have_last_plan = false;
+}
+
 // ---------------------------------------------------------------- decode
 void dec_class(const scz_info& in, uint8_t* width) {
     // symbol width + lookup flavour: 1 = u8 LUT, 2 = u16 LUT, 4 = binary search
@@ -1031,14 +1043,22 @@ struct DecCaps {
 
 int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* d_freqs, const uint32_t* d_blocks,
                     const uint8_t* d_payload, float* d_out, bool stage, uint32_t* q_out, uint8_t* mask_out,
-                    const scz_info* h_hdr, const scz_info* d_enc_info, const std::string& key);
+                    const scz_info* h_hdr, const scz_info* d_enc_info, const std::string& key,
+                    cudaEvent_t staged = nullptr);
 
 int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t* d_freqs,
                const uint32_t* d_blocks, const uint8_t* d_payload, float* d_out, bool stage,
                uint32_t* q_out, uint8_t* mask_out) {
     cudaStream_t s = ctx->stream;
-    CK(ctx->h_misc.ensure((size_t)B * (sizeof(scz_info) + 8 + 4)));
-    scz_info* hi = ctx->h_misc.as<scz_info>();
+    // Headers, output offsets and statuses are staged in a pinned slot that
+    // one async H2D copy reads.  Slots rotate and each is reused only after
+    // its previous copy completed (its event), so back-to-back async decodes
+    // on one context never overwrite headers a queued copy has yet to read.
+    const uint32_t slot = ctx->stage_next++ % scz_ctx::NSTAGE;
+    if (ctx->stage_ev[slot]) CK(cudaEventSynchronize(ctx->stage_ev[slot]));
+    else CK(cudaEventCreateWithFlags(&ctx->stage_ev[slot], cudaEventDisableTiming));
+    CK(ctx->h_stage[slot].ensure((size_t)B * (sizeof(scz_info) + 8 + 4)));
+    scz_info* hi = ctx->h_stage[slot].as<scz_info>();
     uint64_t* hoff = reinterpret_cast<uint64_t*>(hi + B);
     int32_t* hst = reinterpret_cast<int32_t*>(hoff + B);
     uint32_t acap = 1, nblk_cap = 1, nchunk_cap = 1, widths = 0, maxK = 1, kmask = 0;
@@ -1085,14 +1105,15 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
                 (uint64_t)any_v1 | ((uint64_t)any_v2 << 1) | ((uint64_t)stage << 2) |
                     ((uint64_t)c.total_mult4 << 3),
                 (uint64_t)(uintptr_t)d_freqs, (uint64_t)(uintptr_t)d_blocks, (uint64_t)(uintptr_t)d_payload,
-                (uint64_t)(uintptr_t)d_out, (uint64_t)(uintptr_t)q_out, (uint64_t)(uintptr_t)mask_out,
-                (uint64_t)(uintptr_t)hi});
-    return decode_launches(ctx, B, c, d_freqs, d_blocks, d_payload, d_out, stage, q_out, mask_out, hi, nullptr, key);
+                (uint64_t)(uintptr_t)d_out, (uint64_t)(uintptr_t)q_out, (uint64_t)(uintptr_t)mask_out});
+    return decode_launches(ctx, B, c, d_freqs, d_blocks, d_payload, d_out, stage, q_out, mask_out, hi, nullptr, key,
+                           ctx->stage_ev[slot]);
 }
 
 int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* d_freqs, const uint32_t* d_blocks,
                     const uint8_t* d_payload, float* d_out, bool stage, uint32_t* q_out, uint8_t* mask_out,
-                    const scz_info* h_hdr, const scz_info* d_enc_info, const std::string& key) {
+                    const scz_info* h_hdr, const scz_info* d_enc_info, const std::string& key,
+                    cudaEvent_t staged) {
     cudaStream_t s = ctx->stream;
     const uint32_t acap = c.acap, nblk_cap = c.nblk_cap, nchunk_cap = c.nchunk_cap, widths = c.widths,
                    maxK = c.maxK, kmask = c.kmask;
@@ -1115,10 +1136,12 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
     const uint64_t lut_stride = ((6ull << lut_n) + 15) & ~15ull;
     CK(ctx->dlut.ensure((size_t)B * lut_stride + 64));
     const uint32_t lut_slices = lut_n ? std::max<uint32_t>(1, (1u << lut_n) / LUT_SLICE) : 0;
-    return graph_run(ctx, key, [&]() -> int {
-    if (h_hdr) {
+    if (h_hdr) {  // the staged headers go up ahead of the (possibly replayed) launch sequence
         CK(cudaMemcpyAsync(ctx->dinfo.p, h_hdr, hdr_bytes, cudaMemcpyHostToDevice, s));
-    } else {
+        if (staged) CK(cudaEventRecord(staged, s));
+    }
+    return graph_run(ctx, key, [&]() -> int {
+    if (!h_hdr) {
         CK(launch_pdl(k_dec_headers, dim3(ceil_div_u32(B, 256)), 256, 0, s, d_enc_info, B, d_hi, d_off, d_st));
         LAUNCHED("k_dec_headers");
     }
@@ -1284,6 +1307,8 @@ void scz_ctx_destroy(scz_ctx* ctx) {
     for (cudaEvent_t e : ctx->xev) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->call_ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->sync_ev) cudaEventDestroy(ctx->sync_ev);
     for (auto& g : ctx->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -1432,6 +1457,10 @@ int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64
     CK(cudaMemcpyAsync(ctx->h_info.p, ctx->info.p, sizeof(scz_info), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     *info = *ctx->h_info.as<scz_info>();
+    // test hook: report every searched tensor as a near tie, so callers' host
+    // re-decision paths (container.compress, the INTEGRATION.md binding) run
+    static const bool force_tie = getenv("SCZ_FORCE_NEAR_TIE") != nullptr;
+    if (force_tie && (info->search_flags & SCZ_SEARCH_USED)) info->search_flags |= SCZ_SEARCH_NEAR_TIE;
     if (info->status != SCZ_OK) {
         const char* what[] = {"ok", "tensor contains NaN or Inf", "", "", "", "", "symbol exceeds alphabet",
                               "cannot normalize all-zero counts", "more distinct symbols than slots",
@@ -1516,6 +1545,7 @@ __global__ void k_set_params(TensorState* st, double scale, int64_t z) {
 int quantize_impl(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, bool given, double g_scale,
                   int64_t g_z, double* scale, int64_t* zero_point, float* minmax, uint32_t* q,
                   uint8_t* mask) {
+    ctx_forget_batch(ctx);
     if (n < 1 || n >= (1ull << 31)) return ctx->fail(SCZ_UNSUPPORTED, "size");
     cudaStream_t s = ctx->stream;
     uint32_t ntiles = ceil_div_u32(n, TILE), wp = ntiles * TILE_WORDS;
@@ -1576,6 +1606,7 @@ int scz_quantize(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, float* mi
 
 int scz_dequantize(scz_ctx* ctx, const uint32_t* q, const uint8_t* mask, uint64_t n, int q_bits, double scale,
                    int64_t zero_point, float* out) {
+    ctx_forget_batch(ctx);
     if (!ctx || !q || !mask || !out) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     (void)q_bits;
@@ -1595,6 +1626,7 @@ int scz_dequantize(scz_ctx* ctx, const uint32_t* q, const uint8_t* mask, uint64_
 
 int scz_csr_encode(scz_ctx* ctx, const uint32_t* q, const uint8_t* mask, uint64_t n_rows, uint64_t n_cols,
                    uint32_t* d, uint64_t* nnz_out) {
+    ctx_forget_batch(ctx);
     if (!ctx || !q || !mask || !d) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     const uint64_t n = n_rows * n_cols;
@@ -1637,6 +1669,7 @@ int scz_csr_encode(scz_ctx* ctx, const uint32_t* q, const uint8_t* mask, uint64_
 
 int scz_csr_decode(scz_ctx* ctx, const uint32_t* d, uint64_t nnz, uint64_t n_rows, uint64_t n_cols, uint32_t* q,
                    uint8_t* mask) {
+    ctx_forget_batch(ctx);
     if (!ctx || !d || !q || !mask) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     const uint64_t L = 2 * nnz + n_rows, n = n_rows * n_cols;
@@ -1677,6 +1710,7 @@ int scz_csr_decode(scz_ctx* ctx, const uint32_t* d, uint64_t nnz, uint64_t n_row
 }
 
 int scz_build_counts(scz_ctx* ctx, const uint32_t* d, uint64_t n, uint64_t alphabet, int64_t* counts) {
+    ctx_forget_batch(ctx);
     if (!ctx || !counts) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     if (alphabet < 1) return ctx->fail(SCZ_INVALID_INPUT, "alphabet_size must be >= 1");
@@ -1702,6 +1736,7 @@ int scz_build_counts(scz_ctx* ctx, const uint32_t* d, uint64_t n, uint64_t alpha
 }
 
 int scz_normalize(scz_ctx* ctx, const int64_t* counts, uint64_t alphabet, int precision, uint32_t* freqs) {
+    ctx_forget_batch(ctx);
     if (!ctx || !counts || !freqs) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     if (alphabet < 1 || alphabet >= (1ull << 31)) return ctx->fail(SCZ_INVALID_INPUT, "alphabet");
@@ -1731,6 +1766,7 @@ int scz_normalize(scz_ctx* ctx, const int64_t* counts, uint64_t alphabet, int pr
 int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t* freqs, uint64_t alphabet,
                     int precision, uint32_t lanes, uint32_t block_syms, uint8_t* out, uint64_t* out_len,
                     uint32_t* block_bytes) {
+    ctx_forget_batch(ctx);
     if (!ctx || !freqs || !out || !out_len) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     if (precision < 1 || precision > 16) return ctx->fail(SCZ_INVALID_INPUT, "precision");
@@ -1796,6 +1832,7 @@ int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t*
 int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint32_t* freqs, uint64_t alphabet,
                     int precision, uint32_t lanes, uint32_t block_syms, uint64_t n_blocks,
                     const uint32_t* block_bytes, uint64_t count, uint32_t* out) {
+    ctx_forget_batch(ctx);
     if (!ctx || !freqs || !out) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     scz_info in;
@@ -2114,7 +2151,6 @@ int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, c
         if (!nb) break;
         uint64_t n_out = 0;
         for (uint32_t i = b0; i < b0 + nb; ++i) n_out += h_info[i].total;
-        if (c) CK(cudaStreamSynchronize(s));  // run_decode restages its pinned header copy
         CK(cudaStreamWaitEvent(s, ctx->xev[1 + c], 0));
         if ((st = run_decode(ctx, h_info + b0, nb, ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
                              ctx->dpayload.as<uint8_t>(), ctx->dout.as<float>() + out_base, false, nullptr,

@@ -23,7 +23,7 @@ constexpr int TILE = 8192;             // elements per stats/quantize tile
 constexpr int TILE_THREADS = 256;      // 32 elements per thread
 constexpr int TILE_WORDS = TILE / 32;  // bitmap words per tile
 constexpr uint32_t STATE_LOW = 1u << 23;  // rans.py:26
-constexpr int MAX_CAND = 64;           // feasible reshape candidates per launch
+constexpr int MAX_CAND = 256;          // feasible reshape candidates per launch (K <= 2^Q <= 256 bounds their count)
 
 // Per-tensor device state written by the encode kernels (internal, not ABI).
 struct TensorState {

@@ -243,3 +243,23 @@ def test_oracle_self_round_trip_random():
             assert np.all(out[~nz] == 0)
             if nz.any():
                 assert np.abs(out[nz] - x[nz]).max() <= s + 1e-6
+
+
+def test_oracle_general_alphabet_pinned_to_reference():
+    """K > 65535 and alphabets past 4096 / 8192 (tests/inputs.py GENERAL_ALPHABET):
+    the oracle's v1 containers and reconstructions equal the unmodified
+    reference's (tests/golden/general_alphabet.json, make_golden_general.py)."""
+    import hashlib
+    import json
+
+    from inputs import GENERAL_ALPHABET, sparse_columns
+
+    pins = {r["label"]: r for r in json.load(open(os.path.join(GOLDEN, "general_alphabet.json")))}
+    for label, T, n_rows, stride, q, prec in GENERAL_ALPHABET:
+        x = sparse_columns(T, T // n_rows, stride, seed=T % 997)
+        pin = pins[label]
+        assert hashlib.sha256(x.tobytes()).hexdigest() == pin["input_sha"], label
+        c = orc.compress(x, (T,), q, n_rows, prec)
+        raw = orc.to_bytes(c)
+        assert hashlib.sha256(raw).hexdigest() == pin["container_sha"], label
+        assert hashlib.sha256(orc.decompress(c).tobytes()).hexdigest() == pin["output_sha"], label
