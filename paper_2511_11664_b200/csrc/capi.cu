@@ -19,6 +19,7 @@
 #include "rans.cu"
 #include "rans_enc.cu"
 #include "rans_dec.cu"
+#include "rans_v1.cu"
 #include "rowhist.cu"
 #include "decode.cu"
 
@@ -910,7 +911,12 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
                 pk.write_failed = 0;  // the first launch wrote the failed tensors' headers
                 LAUNCHED(wname<S>("k_rans_enc_v2"));
             } else {
-                CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
+                if constexpr (std::is_same<Src, Contig8Src>::value) {
+                    if (pl.L_max < (1ull << 30)) CK(launch_pdl(k_rans_enc_v1_fast, B, 32, 0, s, ep, src));
+                    else CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
+                } else {
+                    CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
+                }
                 LAUNCHED(wname<S>("k_rans_enc_v1"));
             }
             return SCZ_OK;
@@ -1088,7 +1094,7 @@ int run_decode(scz_ctx* ctx, const scz_info* h_info, uint32_t B, const uint32_t*
     // v2 decode tables: (4 + 2) bytes per slot covers both LUT classes
     int lut_n = 0;  // largest precision among v2 tensors of the LUT classes
     for (uint32_t b = 0; b < B; ++b)
-        if (hi[b].version == 2 && hi[b].sym_bytes < 4) lut_n = std::max(lut_n, (int)hi[b].precision);
+        if (hi[b].sym_bytes < 4) lut_n = std::max(lut_n, (int)hi[b].precision);  // v2 and v1 (fast) LUT classes
     bool any_v1 = false, any_v2 = false;
     for (uint32_t b = 0; b < B; ++b) (hi[b].version == 2 ? any_v2 : any_v1) = true;
     (void)s;
@@ -1172,10 +1178,20 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
             LAUNCHED(wname<S>("k_rans_dec_v2"));
         }
         if (any_v1) {
-            size_t smem = RING + tab + lut;
-            CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-            CK(launch_pdl(k_rans_dec_v1<S, L>, B, 32, smem, s, dp));
+            bool fast = Lmax < (1ull << 30);  // 32-bit stream offsets in the fast kernel
+            if constexpr (sizeof(L) == 4) fast = false;
+            if (fast) {  // u8 / u16 classes: the latency-optimised serial decoder
+                const size_t smem = dec_v1_smem(maxn, sizeof(L));
+                if constexpr (sizeof(L) < 4)
+                    CK(cudaFuncSetAttribute(k_rans_dec_v1_fast<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+                if constexpr (sizeof(L) < 4) CK(launch_pdl(k_rans_dec_v1_fast<S, L>, B, 32, smem, s, dp));
+            } else {
+                size_t smem = RING + tab + lut;
+                CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+                CK(launch_pdl(k_rans_dec_v1<S, L>, B, 32, smem, s, dp));
+            }
             LAUNCHED(wname<S>("k_rans_dec_v1"));
         }
         return SCZ_OK;
@@ -1394,7 +1410,7 @@ int scz_decode_batch_device(scz_ctx* ctx, float* d_out) {
     c.nblk_cap = pl.format == 2 ? pl.nblk_cap : 1;
     c.Lmax = (pl.L_max + 15) & ~15ull;
     c.maxn = pl.precision;
-    c.lut_n = pl.format == 2 ? pl.precision : 0;
+    c.lut_n = pl.precision;
     c.any_v1 = pl.format == 1;
     c.any_v2 = pl.format == 2;
     c.total_mult4 = pl.T % 4 == 0;

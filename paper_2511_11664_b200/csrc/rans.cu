@@ -200,6 +200,11 @@ __device__ void build_lut_slice(const DecParams& p, const scz_info& in, uint32_t
     uint8_t* base = p.lut + (uint64_t)b * p.lut_stride;
     uint32_t* step = reinterpret_cast<uint32_t*>(base);
     L* sym = reinterpret_cast<L*>(base + lut_sym_off(n));
+    // v1 (k_rans_dec_v1_fast): f and slot - cum as separate u16 arrays, so
+    // the serial decoder's state update is one IMAD on two 16-bit loads
+    const bool split = in.version == 1;
+    uint16_t* f16 = reinterpret_cast<uint16_t*>(base);
+    uint16_t* b16 = f16 + ((size_t)1 << n);
     const uint32_t slot0 = s0 + 8 * threadIdx.x;
     if (slot0 >= (1u << n)) return;
     uint32_t lo = 0, hi = A;  // last symbol with cum <= slot0
@@ -217,9 +222,20 @@ __device__ void build_lut_slice(const DecParams& p, const scz_info& in, uint32_t
         e[k] = ((s_cum[lo + 1] - s_cum[lo]) << 16) | (sl - s_cum[lo]);
         sy[k] = (L)lo;
     }
-    uint4* d4 = reinterpret_cast<uint4*>(step + slot0);
-    d4[0] = make_uint4(e[0], e[1], e[2], e[3]);
-    d4[1] = make_uint4(e[4], e[5], e[6], e[7]);
+    if (split) {
+        uint32_t fw[4], bw[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            fw[k] = (e[2 * k] >> 16) | (e[2 * k + 1] & 0xFFFF0000u);
+            bw[k] = (e[2 * k] & 0xFFFFu) | (e[2 * k + 1] << 16);
+        }
+        *reinterpret_cast<uint4*>(f16 + slot0) = make_uint4(fw[0], fw[1], fw[2], fw[3]);
+        *reinterpret_cast<uint4*>(b16 + slot0) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+    } else {
+        uint4* d4 = reinterpret_cast<uint4*>(step + slot0);
+        d4[0] = make_uint4(e[0], e[1], e[2], e[3]);
+        d4[1] = make_uint4(e[4], e[5], e[6], e[7]);
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) sym[slot0 + k] = sy[k];
 }
@@ -229,7 +245,7 @@ __global__ void __launch_bounds__(256) k_dec_prepare(DecParams p) {
     const uint32_t b = blockIdx.y;
     const scz_info& in = p.info[b];
     if (blockIdx.x > 0) {
-        if (p.status[b] != SCZ_OK || in.version != 2) return;
+        if (p.status[b] != SCZ_OK || (in.version != 2 && in.version != 1)) return;
         if (in.sym_bytes == 1) build_lut_slice<uint8_t>(p, in, b, blockIdx.x - 1);
         else if (in.sym_bytes == 2) build_lut_slice<uint16_t>(p, in, b, blockIdx.x - 1);
         return;
