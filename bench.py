@@ -65,7 +65,10 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=256, help="tensors per rank (weak scaling)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling: this many tensors in total, shard.partition over the ranks "
+                         "(config C3: 4096)")
     ap.add_argument("--format", type=int, default=2, choices=[1, 2])
     ap.add_argument("--block-syms", type=int, default=8192)
     ap.add_argument("--serialize", type=int, default=int(os.environ.get("SCZ_BENCH_SERIALIZE", "0")),
@@ -77,6 +80,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip v1 / latency side measurements")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer round trip (profiling runs)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-BASELINE-config sub-records")
     return ap.parse_args()
 
 
@@ -293,14 +297,26 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SCZ_BENCH_DEVICE pins every rank to one GPU (a multi-rank dry run of the
+    # torchrun path on a one-GPU box); NCCL refuses two ranks on one device,
+    # so that mode uses gloo for the barrier and the reductions
+    dev_override = os.environ.get("SCZ_BENCH_DEVICE")
+    if dev_override is not None:
+        local = int(dev_override)
     torch.cuda.set_device(local)
     dist = None
+    backend = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SCZ_BENCH_DIST_BACKEND", "gloo" if dev_override is not None else "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    red_dev = torch.device("cuda", local) if backend == "nccl" else None
 
-    from paper_2511_11664_b200 import _native
+    from paper_2511_11664_b200 import _native, shard
 
     # Host threads (and the pinned buffers they touch first) on the GPU's own
     # NUMA node: the e2e path is PCIe-bound, and DMA to far-socket memory
@@ -312,13 +328,24 @@ def run_ours(args):
 
     wl = WORKLOADS[args.workload]
     T = int(np.prod(wl["dims"]))
-    B = args.batch
+    # the tensors this rank codes: its own `batch` seeds (weak scaling,
+    # shard.weak_seeds) or its contiguous slice of --global-batch (strong
+    # scaling, shard.partition); tensors are independent, no data collective
+    if args.global_batch:
+        lo, hi = shard.partition(args.global_batch, world, rank)
+        seeds = range(lo, hi)
+        scaling = "strong"
+    else:
+        seeds = shard.weak_seeds(args.batch, rank)
+        scaling = "weak"
+    B = len(seeds)
+    total_units = args.global_batch if args.global_batch else args.batch * world
     ctx = _native.context(local)
     lib = ctx.lib
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
     host = torch.empty((B, T), dtype=torch.float32).pin_memory()
-    host.numpy()[:] = make_batch(wl, B, rank * B)
+    host.numpy()[:] = make_batch(wl, B, seeds.start)
     x_dev = host.cuda(local)
     out_dev = torch.empty_like(x_dev)
     torch.cuda.synchronize()
@@ -341,11 +368,7 @@ def run_ours(args):
             dist.barrier()
 
     def max_over_ranks(v):
-        if not dist:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return shard.reduce_max(v, dist, red_dev)
 
     # ---- device-resident timed region -------------------------------------
     # Library contexts (own stream + scratch each; --contexts, default 6)
@@ -451,7 +474,7 @@ def run_ours(args):
                      step_gap_ms_p50=statistics.median(gaps), step_gap_ms_max=gaps[-1])
     ms = max(ev0.elapsed_time(e) for e in ev_end) / args.steps
     ms = max_over_ranks(ms)
-    value = 4.0 * T * B * world / (ms * 1e-3) / 1e9
+    value = 4.0 * T * total_units / (ms * 1e-3) / 1e9
 
     statuses = (ctypes.c_int32 * B)()
     for k in range(NC):
@@ -528,7 +551,7 @@ def run_ours(args):
     if not args.no_e2e:
         e2e_ms, io, h_out, e2e_status = run_e2e(args, torch, _native, lib, local, host, T, B, wl)
         e2e_ms = max_over_ranks(e2e_ms)
-        e2e_value = 4.0 * T * B * world / (e2e_ms * 1e-3) / 1e9
+        e2e_value = 4.0 * T * total_units / (e2e_ms * 1e-3) / 1e9
         assert all(s == 0 for s in e2e_status)
         assert torch.equal(h_out, out_dev.cpu()), "host-path reconstruction differs from device path"
         e2e = dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=io["h2d"],
@@ -550,13 +573,15 @@ def run_ours(args):
     if rank == 0:
         line = dict(
             metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
-            warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling="weak",
+            warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling=scaling,
             vs_baseline=None, dtype="u8/u32 (fp32 in/out, fp64 quant params)", data="synthetic",
-            config=dict(workload=wl["name"], global_batch=B * world, per_gpu_batch=B, q_bits=wl["q"],
+            config=dict(workload=wl["name"], global_batch=total_units, per_gpu_batch=B, q_bits=wl["q"],
                         precision=14, format=f"v{args.format}", lanes=32,
                         block_syms=args.block_syms, reshape="Algorithm 1 on device",
                         parallelism=f"dp{world} (independent tensors, no collective)",
-                        l2="inputs 822 MB per rank > 126 MB L2 (no flush needed)"),
+                        l2=f"inputs {4 * T * B / 1e6:.0f} MB per rank "
+                           + ("> 126 MB L2 (no flush needed)" if 4 * T * B > 126e6 else
+                              "< 126 MB L2: NOT flushed between steps")),
             bytes_per_element=bpe,
             e2e=e2e,
             roofline=roofline, pipeline_roofline=pipeline_roofline, kernel_share=kernel_share,
@@ -724,7 +749,201 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
     res["v1_reference_format"] = dict(value=4.0 * T * B / (v1_ms * 1e-3) / 1e9, unit=UNIT,
                                       ms_per_step=v1_ms, batch=B,
                                       note="bit-exact reference wire format; serial stream per tensor")
+    if not args.no_configs:
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        peak = float(json.load(open(peaks_path))["hbm_gbs"]) if os.path.exists(peaks_path) else 6650.0
+        t0 = time.perf_counter()
+        res["configs"] = config_records(args, torch, _native, x_dev.device.index or 0, peak)
+        res["configs"]["wall_s"] = round(time.perf_counter() - t0, 1)
     return res
+
+
+# ------------------------------------------------ every BASELINE config
+CONTAINER_FIXED = 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 4 + 8  # container.py:62 without dims / freqs
+
+
+def container_bytes(info, ndims):
+    """Total .scz bytes of one tensor (container.py:62; FORMAT.md v2 adds 12 + 4 n_blocks)."""
+    b = CONTAINER_FIXED + 4 * ndims + 2 * int(info.alphabet) + int(info.payload_len)
+    if int(info.version) == 2:
+        b += 12 + 4 * int(info.n_blocks)
+    return b
+
+
+class DeviceBatch:
+    """Encode / decode of one device-resident batch through the C ABI on one
+    library context, timed with CUDA events on the context's stream:
+    encode = scz_encode_batch, decode = scz_decode_batch_async (after the
+    host read the headers with scz_batch_sync).  Optionally writes a 256 MB
+    buffer on the same stream before every timed repetition (L2 flush) when
+    the batch is smaller than the 126 MB L2."""
+
+    def __init__(self, torch, _native, device):
+        self.torch = torch
+        self.ctx = _native.Context(device)
+        self.lib = self.ctx.lib
+        self.native = _native
+        self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=torch.device("cuda", device))
+        self.flush_buf = torch.empty(64 << 20, dtype=torch.float32, device=torch.device("cuda", device))
+        self.batch = _native.Batch()
+
+    def flush(self):
+        with self.torch.cuda.stream(self.stream):
+            self.flush_buf.fill_(1.0)
+
+    def run(self, x, out, B, T, q, fmt, bs, n_rows=-1, reps=5, warm=3, flush=False):
+        """[(encode ms, decode ms)] of `reps` timed repetitions + the infos."""
+        torch, lib, c = self.torch, self.lib, self.ctx
+        infos = (self.native.Info * B)()
+        st = (ctypes.c_int32 * B)()
+        res = []
+        for r in range(warm + reps):  # eager, graph capture, replay, then timed replays
+            if flush:
+                self.flush()
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            e0.record(self.stream)
+            c.check(lib.scz_encode_batch(c.h, ctypes.c_void_p(x.data_ptr()), T, B, q, n_rows, 14, fmt, 32, bs,
+                                         ctypes.byref(self.batch)))
+            e1.record(self.stream)
+            c.check(lib.scz_batch_sync(c.h, ctypes.byref(self.batch), infos))
+            e2.record(self.stream)
+            c.check(lib.scz_decode_batch_async(c.h, infos, B, ctypes.c_void_p(self.batch.d_freqs),
+                                               ctypes.c_void_p(self.batch.d_block_bytes),
+                                               ctypes.c_void_p(self.batch.d_payload),
+                                               ctypes.c_void_p(out.data_ptr())))
+            e3.record(self.stream)
+            c.check(lib.scz_decode_status(c.h, B, st))
+            assert all(v == 0 for v in st) and all(infos[i].status == 0 for i in range(B)), "device status"
+            if r >= warm:
+                res.append((e0.elapsed_time(e1), e2.elapsed_time(e3)))
+        return res, infos
+
+
+def config_records(args, torch, _native, device, peak):
+    """One record per BASELINE.json config on this GPU: device
+    encode / decode times (CUDA events), throughput, p50 latency, bytes per
+    element in both formats, encode / decode roofline fractions, and the
+    oracle port (the reference algorithm in C + numpy) timed beside it on one
+    host core for a bounded sample."""
+    from oracle import oracle as orc
+    from paper_2511_11664_b200.synth import make_input
+
+    dev = DeviceBatch(torch, _native, device)
+    recs = {}
+
+    def dev_tensor(specs):
+        xs = np.stack([make_input(sp) for sp in specs])
+        return torch.from_numpy(xs).to(torch.device("cuda", device))
+
+    def summarize(name, xs, dims, q, fmt, bs, reps, flush, n_rows=-1):
+        B, T = xs.shape
+        out = torch.empty_like(xs)
+        times, infos = dev.run(xs, out, B, T, q, fmt, bs, n_rows, reps=reps, flush=flush)
+        enc = statistics.median(t[0] for t in times)
+        dec = statistics.median(t[1] for t in times)
+        sbytes = sum(container_bytes(infos[i], len(dims)) for i in range(B))
+        err = (out - xs).abs().amax(dim=1)
+        scales = torch.tensor([infos[i].scale for i in range(B)], device=xs.device, dtype=torch.float32)
+        assert bool((err <= scales * 1.0001 + 1e-6).all()), name
+        r = dict(format=f"v{fmt}", batch=B, encode_ms=enc, decode_ms=dec, gbs=4.0 * T * B / ((enc + dec) * 1e-3) / 1e9,
+                 bytes_per_element=sbytes / (T * B),
+                 encode_roofline=(4.0 * T * B + sbytes) / (enc * 1e-3) / 1e9 / peak,
+                 decode_roofline=(4.0 * T * B + sbytes) / (dec * 1e-3) / 1e9 / peak,
+                 n_rows=int(infos[0].n_rows), n_cols=int(infos[0].n_cols))
+        if fmt == 2:
+            r["block_syms"] = bs
+        return r, infos
+
+    def cpu_p50(spec, q, n=3):
+        x = make_input(spec)
+        ts = []
+        for _ in range(n):
+            t0 = time.perf_counter()
+            c = orc.compress(x, spec["dims"], q, None, 14)
+            orc.decompress(c)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return dict(ms_p50=statistics.median(ts), cores=1, kind="port",
+                    sample=f"{n} x compress (Algorithm 1) + decompress of the same tensor, v1, one process")
+
+    # C1: one ResNet-50 layer2 tensor, sparsity 0.5 (primary) and 0.9 (the reference's test value)
+    for sp in (0.5, 0.9):
+        spec = dict(kind="relu-laplace", dims=(1, 512, 28, 28), sparsity=sp, seed=42)
+        x = dev_tensor([spec])
+        v2, _ = summarize("C1", x, spec["dims"], 8, 2, args.block_syms, 30, True)
+        v1, _ = summarize("C1v1", x, spec["dims"], 8, 1, args.block_syms, 3, True)
+        recs[f"C1-resnet50-layer2-relu{sp}"] = dict(
+            tensor="(1, 512, 28, 28)", v2=dict(v2, latency_us_p50=1e3 * (v2["encode_ms"] + v2["decode_ms"])),
+            v1=dict(v1, latency_us_p50=1e3 * (v1["encode_ms"] + v1["decode_ms"])),
+            cpu_baseline=cpu_p50(spec, 8), l2="single tensor: 256 MB L2 flush before every repetition")
+    # C2: VGG16 batch 256 (serial encode / decode rooflines; the headline is the pipelined value)
+    wl = WORKLOADS["vgg16"]
+    x = dev_tensor([dict(kind=wl["kind"], dims=wl["dims"], sparsity=wl["sparsity"], seed=i) for i in range(256)])
+    v2, _ = summarize("C2vgg", x, wl["dims"], 8, 2, args.block_syms, 3, False)
+    v1, _ = summarize("C2vgg1", x, wl["dims"], 8, 1, args.block_syms, 1, False)
+    recs["C2-vgg16-batch256"] = dict(v2=v2, v1=v1, note="one context, encode then decode (not pipelined)")
+    del x
+    # C2: MobileNetV2 features[10], signed (z = 131), batch 256: 12.8 MB < L2, flushed
+    spec = [dict(kind="signed", dims=(1, 64, 14, 14), seed=i) for i in range(256)]
+    x = dev_tensor(spec)
+    v2, _ = summarize("C2mnv2", x, (1, 64, 14, 14), 8, 2, args.block_syms, 5, True)
+    v1, _ = summarize("C2mnv2v1", x, (1, 64, 14, 14), 8, 1, args.block_syms, 3, True)
+    lat, _ = summarize("C2mnv2lat", x[:1].contiguous(), (1, 64, 14, 14), 8, 2, args.block_syms, 30, True)
+    recs["C2-mobilenetv2-batch256"] = dict(v2=v2, v1=v1, latency_us_p50=1e3 * (lat["encode_ms"] + lat["decode_ms"]),
+                                           cpu_baseline=cpu_p50(spec[0], 8, 5),
+                                           l2="batch 12.8 MB < L2: 256 MB flush before every repetition")
+    del x
+    # C3: ResNet-50 features, batch 4096 on this GPU (seeds 0..511, each tensor 8 times: host generation time)
+    spec = [dict(kind="relu-laplace", dims=(1, 512, 28, 28), sparsity=0.5, seed=i) for i in range(512)]
+    x1 = dev_tensor(spec)
+    x = x1.repeat(8, 1)
+    del x1
+    v2, _ = summarize("C3", x, (1, 512, 28, 28), 8, 2, args.block_syms, 2, False)
+    recs["C3-resnet50-batch4096"] = dict(v2=v2, note="N = 1; bench.py --workload resnet50 --global-batch 4096 "
+                                                     "under torchrun is the strong-scaling run")
+    del x
+    torch.cuda.empty_cache()
+    # C4: Llama2-7B hidden state 1x2048x4096, signed dense (25.2 M-symbol stream)
+    spec = dict(kind="signed", dims=(1, 2048, 4096), seed=42)
+    x = dev_tensor([spec])
+    v2, _ = summarize("C4", x, spec["dims"], 8, 2, args.block_syms, 5, True)
+    v1, _ = summarize("C4v1", x, spec["dims"], 8, 1, args.block_syms, 1, True)
+    recs["C4-llama2-7b-hidden"] = dict(tensor="(1, 2048, 4096)", v2=dict(v2, latency_ms=v2["encode_ms"] + v2["decode_ms"]),
+                                       v1=dict(v1, latency_ms=v1["encode_ms"] + v1["decode_ms"]),
+                                       cpu_baseline=cpu_p50(spec, 8, 1))
+    del x
+    # C5: reshape and bit-width sweep against the approximate model (entropy x l_D):
+    # every feasible N is coded (v1 bytes); the model's early-stopped choice
+    # and its exhaustive optimum are compared with the smallest actual container
+    from paper_2511_11664_b200 import optimizer
+    from paper_2511_11664_b200.tensor import FeatureTensor
+
+    sweep = {}
+    for name, spec in (("swint-stage2", dict(kind="signed", dims=(1, 28, 28, 192), seed=42)),
+                       ("densenet121-block2", dict(kind="relu-laplace", dims=(1, 512, 28, 28), sparsity=0.6, seed=42))):
+        x = dev_tensor([spec])
+        T = x.shape[1]
+        rows = []
+        ft = FeatureTensor(spec["dims"], x[0].cpu().numpy())
+        for q in (2, 4, 6, 8):
+            n_search, _ = optimizer.search(ft, q)  # Algorithm 1 (device histograms)
+            lat, _ = summarize("C5", x, spec["dims"], q, 2, args.block_syms, 5, True)
+            cands = optimizer.candidate_rows(T, q) or [T]
+            actual = {}
+            out = torch.empty_like(x)
+            for n_rows in cands:
+                _, infos = dev.run(x, out, 1, T, q, 1, args.block_syms, n_rows, reps=0, warm=1)
+                actual[n_rows] = container_bytes(infos[0], len(spec["dims"]))
+            n_model, _ = optimizer.exhaustive_search(ft, q)
+            n_best = min(actual, key=actual.get)
+            rows.append(dict(q=q, n_search=int(n_search), n_model_optimum=int(n_model), n_actual_best=int(n_best),
+                             device_n=lat["n_rows"], bytes_search=actual[n_search], bytes_actual_best=actual[n_best],
+                             search_over_best=actual[n_search] / actual[n_best], candidates=len(cands),
+                             bytes_per_element_v1=actual[n_search] / T, v2=lat,
+                             latency_us_p50=1e3 * (lat["encode_ms"] + lat["decode_ms"])))
+        sweep[name] = rows
+        del x
+    recs["C5-reshape-q-sweep"] = sweep
+    return recs
 
 
 def main():
