@@ -380,7 +380,9 @@ def run_ours(args):
     # without the headers it must launch every symbol-class / K variant the
     # plan allows; with the chosen variants known on the host this path is
     # faster for a full batch.)
-    NC = max(2, args.contexts)
+    # (each context holds a whole batch of scratch, about 6x the fp32 input:
+    # large per-rank batches rotate over fewer contexts)
+    NC = max(2, args.contexts if 4 * T * B <= (2 << 30) else min(args.contexts, 3))
     ctxs = [ctx] + [_native.Context(local) for _ in range(NC - 1)]
     streams = [stream] + [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local))
                           for c in ctxs[1:]]

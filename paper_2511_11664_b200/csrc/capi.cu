@@ -1134,7 +1134,8 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
     ctx->dstatus_cur = d_st;
     CK(ctx->cumtab.ensure((size_t)B * (acap + 1) * 4));
     CK(ctx->dblk_off.ensure((size_t)B * nblk_cap * 4));
-    CK(ctx->dsym.ensure((size_t)B * Lmax * 4));
+    // decoded symbols: row b at b * Lmax elements of the widest class present
+    CK(ctx->dsym.ensure((size_t)B * Lmax * ((widths & 4) ? 4 : ((widths & 2) ? 2 : 1)) + 64));
     // look-back words / chunk sums, then the [B][256] dequantisation tables
     const size_t dq_at = ((size_t)B * nchunk_cap * 8 + 15) & ~(size_t)15;  // 16-byte aligned tables
     CK(ctx->chunk_sum.ensure(dq_at + (size_t)B * 256 * 4));
@@ -1151,8 +1152,9 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
         CK(launch_pdl(k_dec_headers, dim3(ceil_div_u32(B, 256)), 256, 0, s, d_enc_info, B, d_hi, d_off, d_st));
         LAUNCHED("k_dec_headers");
     }
+    const uint64_t sym_row = Lmax * ((widths & 4) ? 4 : ((widths & 2) ? 2 : 1));  // bytes per tensor
     DecParams dp{ctx->dinfo.as<scz_info>(), d_freqs, d_blocks, d_payload, ctx->cumtab.as<uint32_t>(),
-                 ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, Lmax,
+                 ctx->dblk_off.as<uint32_t>(), acap, nblk_cap, ctx->dsym.p, sym_row,
                  d_st, ctx->dlut.as<uint8_t>(), lut_stride,
                  ctx->chunk_sum.as<unsigned long long>(), nchunk_cap, stage ? 0 : 1, d_dq};
     CK(launch_pdl(k_dec_prepare, dim3(1 + lut_slices, B), 256, 0, s, dp));
@@ -1160,7 +1162,7 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
     // rows of K <= 4 floats are vector-aligned when the output base is 16-byte
     // aligned and every tensor starts at a multiple of 4 floats
     const bool vec_rows = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && c.total_mult4;
-    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, Lmax, ctx->chunk_sum.as<unsigned long long>(), nchunk_cap,
+    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, sym_row, ctx->chunk_sum.as<unsigned long long>(), nchunk_cap,
                  d_st, d_out, d_off, q_out, mask_out, d_dq};
     auto run_width = [&](auto tag) -> int {
         using S = decltype(tag);
@@ -1711,7 +1713,7 @@ int scz_csr_decode(scz_ctx* ctx, const uint32_t* d, uint64_t nnz, uint64_t n_row
     CK(cudaMemsetAsync(ctx->dstatus.p, 0, 4, s));
     uint32_t* qd = ctx->dsym_in.as<uint32_t>();
     uint8_t* md = reinterpret_cast<uint8_t*>(qd + n);
-    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, L, ctx->chunk_sum.as<unsigned long long>(), nch,
+    RowParams rp{ctx->dinfo.as<scz_info>(), ctx->dsym.p, L * 4, ctx->chunk_sum.as<unsigned long long>(), nch,
                  ctx->dstatus.as<int32_t>(), nullptr, nullptr, qd, md};
     k_rows_out<uint32_t, true><<<dim3(nch, 1), ROW_THREADS, 0, s>>>(rp);
     LAUNCHED("k_rows_out");
@@ -1905,7 +1907,7 @@ int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint3
     CK(ctx->dlut.ensure(lut_stride + 64));
     DecParams dp{ctx->dinfo.as<scz_info>(), ctx->dfreqs.as<uint32_t>(), ctx->dblocks.as<uint32_t>(),
                  ctx->dpayload.as<uint8_t>(), ctx->cumtab.as<uint32_t>(), ctx->dblk_off.as<uint32_t>(),
-                 (uint32_t)alphabet, (uint32_t)std::max<uint64_t>(n_blocks, 1), ctx->dsym.p, count,
+                 (uint32_t)alphabet, (uint32_t)std::max<uint64_t>(n_blocks, 1), ctx->dsym.p, count * 4,
                  ctx->dstatus.as<int32_t>(), ctx->dlut.as<uint8_t>(), lut_stride};
     const uint32_t lut_slices = use_lut ? std::max<uint32_t>(1, (1u << precision) / LUT_SLICE) : 0;
     k_dec_prepare<<<dim3(1 + lut_slices, 1), 256, 0, s>>>(dp);

@@ -49,8 +49,8 @@ __device__ __forceinline__ float dequant(uint32_t v, const float* lut, double z,
 
 struct RowParams {
     const scz_info* info;   // [B]
-    const void* dsym;       // [B][dsym_stride] decoded D
-    uint64_t dsym_stride;
+    const void* dsym;       // decoded D: tensor b's row at byte b * dsym_stride
+    uint64_t dsym_stride;   // bytes (Lmax x the widest symbol class of the batch)
     unsigned long long* chunk_state;  // [B][nchunk_cap] look-back words, zeroed per launch
     uint32_t nchunk_cap;
     int32_t* status;        // [B]
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_out(RowParams p) {
     if (r0 >= N) return;
     if (chunk_dead(p, b, chunk)) return;
     const uint64_t nnz = in.nnz;
-    const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    const S* d = reinterpret_cast<const S*>(reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride);
     const S* vals = d;
     const S* cols = d + nnz;
     const S* rc = d + 2 * nnz;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_fast(RowParams p) {
     if (r0 >= N) return;
     if (chunk_dead(p, b, chunk)) return;
     const uint64_t nnz = in.nnz;
-    const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    const S* d = reinterpret_cast<const S*>(reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride);
     __shared__ uint32_t s_off[ROW_CHUNK];
     __shared__ __align__(16) float s_out[OUT_ELEMS];
     __shared__ S s_c[OUT_ELEMS], s_v[OUT_ELEMS];
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(ROW_THREADS) k_rows_small(RowParams p) {
     if (r0 >= N) return;
     if (chunk_dead(p, b, chunk)) return;
     const uint64_t nnz = in.nnz;
-    const S* d = reinterpret_cast<const S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    const S* d = reinterpret_cast<const S*>(reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride);
     __shared__ uint32_t s_off[ROW_CHUNK];
     __shared__ uint8_t s_r[ROW_CHUNK];
     __shared__ uint32_t s_scan[33];

@@ -150,8 +150,8 @@ struct DecParams {
     uint32_t* cumtab;            // scratch [B][acap + 1]
     uint32_t* blk_off;           // scratch [B][nblk_cap]
     uint32_t acap, nblk_cap;
-    void* dsym;                  // out [B][dsym_stride] symbols, width sym_w
-    uint64_t dsym_stride;
+    void* dsym;                  // out: tensor b's symbols at byte b * dsym_stride
+    uint64_t dsym_stride;        // bytes (one stride for every symbol class of a batch)
     int32_t* status;             // [B]
     // v2 LUT classes: per-tensor decode tables built once in global memory
     // (k_dec_prepare slices) and bulk-copied into each decoder CTA:
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(32) k_rans_dec_v1(DecParams p) {
                  (ring.byte(a0 + 3) << 24);
     uint64_t pos = 4;
     const uint32_t mask = nslots - 1;
-    S* out = reinterpret_cast<S*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    S* out = reinterpret_cast<S*>(reinterpret_cast<uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride);
     bool bad = false;
     for (uint64_t i = 0; i < Ls; ++i) {
         const uint32_t slot = x & mask;

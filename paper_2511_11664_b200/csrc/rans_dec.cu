@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(WPB * 32) k_rans_dec_v2(DecParams p) {
     const uint32_t mask = nslots - 1;
     const uint32_t ltm = lanemask_lt();
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-    S* out = reinterpret_cast<S*>(p.dsym) + (uint64_t)b * p.dsym_stride + base + lane;
+    S* out = reinterpret_cast<S*>(reinterpret_cast<uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride) + base + lane;
     const uint32_t steps = (len + 31) / 32;
     // One step: pop the lane's symbol (rans.py:147-152) and refill.  A
     // stream that runs past its block end keeps decoding ring garbage and is

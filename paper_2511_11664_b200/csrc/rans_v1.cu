@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(32) k_rans_dec_v1_fast(DecParams p) {
     const uint64_t gbase = a0 & ~15ull;
     const uint32_t off0 = (uint32_t)(a0 - gbase);
     const uint32_t end = off0 + (uint32_t)in.payload_len;
-    uint8_t* gout = reinterpret_cast<uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride * sizeof(S);  // 16-aligned
+    uint8_t* gout = reinterpret_cast<uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;  // 16-aligned
     constexpr uint32_t HS = V1_HALF / sizeof(S);  // symbols per output half
     uint32_t x = 0, pos = 0;
     if (lane == 0) {

@@ -241,3 +241,24 @@ def test_highly_composite_element_count_searches_all_candidates():
         n_dev, rep = sz.optimizer.exhaustive_search(t, 8)
         n_ref, seen = orc.exhaustive_search(x, 8)
         assert n_dev == n_ref and len(rep.candidates) == len(seen) > 64
+
+
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_mixed_symbol_classes_in_one_batch_decode(fmt):
+    """One batch decode whose tensors decode into different symbol classes
+    (u16 rows for K = 256, u8 rows for K = 4): every tensor's row of decoded
+    symbols has its own byte range (a u16 row used to overlap the u8 rows of
+    later tensors when rows were indexed in elements of each class)."""
+    dims = (1, 64, 28, 28)
+    T = int(np.prod(dims))
+    ts = [sz.FeatureTensor(dims, make_input(dict(kind="relu-laplace", dims=dims, sparsity=0.5, seed=300 + i)))
+          for i in range(6)]
+    cs = []
+    for i, t in enumerate(ts):
+        n_rows = T // 256 if i in (0, 1) else T // 4  # K = 256 -> u16 symbols; K = 4 -> u8
+        cs.append(sz.compress(t, 8, n_rows, format=fmt, block_syms=1024))
+    assert cs[0].n_cols == 256 and cs[2].n_cols == 4
+    outs = container.decompress_many(cs)
+    for c, o in zip(cs, outs):
+        want = sz.decompress(c)
+        assert np.array_equal(o.data.view(np.uint32), want.data.view(np.uint32))
