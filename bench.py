@@ -687,8 +687,20 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
     o0 = ctypes.c_void_p(out_dev[0].data_ptr())
     lat_enc, lat_dec = [], []
 
+    # L2 flush between repetitions: a 256 MB buffer (> 126 MB L2) is written
+    # once and READ before every repetition -- reading evicts the tensor's
+    # lines without leaving 256 MB of dirty lines whose write-back would then
+    # compete with the timed kernels
+    flush_buf = torch.ones(64 << 20, dtype=torch.float32, device=x_dev.device)
+    flush_sink = torch.empty(1, dtype=torch.float32, device=x_dev.device)
+
+    def flush():
+        with torch.cuda.stream(stream):
+            torch.sum(flush_buf, dim=0, out=flush_sink)
+
     def one(timed, bs=args.block_syms):
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        flush()  # the tensor (3.2 MB) would otherwise stay in L2 between repetitions
         a.record(stream)
         ctx.check(lib.scz_encode_batch(ctx.h, x0, T, 1, wl["q"], -1, 14, 2, 32, bs,
                                        ctypes.byref(batch)))
@@ -706,6 +718,23 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
     # latency: the production path (repeated shapes replay captured CUDA graphs)
     for it in range(50):
         one(it >= 10)
+    # the device round trip: decode straight from the encoder's on-device
+    # headers (scz_decode_batch_device), no host read of the headers between
+    lat_dev = []
+    for it in range(50):
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush()
+        a.record(stream)
+        ctx.check(lib.scz_encode_batch(ctx.h, x0, T, 1, wl["q"], -1, 14, 2, 32, args.block_syms,
+                                       ctypes.byref(batch)))
+        ctx.check(lib.scz_decode_batch_device(ctx.h, o0))
+        c.record(stream)
+        c.synchronize()
+        if it >= 10:
+            lat_dev.append(a.elapsed_time(c) * 1e3)
+    st1 = (ctypes.c_int32 * 1)()
+    ctx.check(lib.scz_decode_status(ctx.h, 1, st1))
+    assert st1[0] == 0
     # per-kernel breakdown: a separate pass with per-launch events (eager)
     ctx.set_timing(True)
     for it in range(15):
@@ -717,7 +746,11 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
     res["latency_us_p50"] = dict(
         encode=statistics.median(lat_enc), decode=statistics.median(lat_dec),
         encode_plus_decode=statistics.median([e + d for e, d in zip(lat_enc, lat_dec)]),
-        tensor=str(wl["dims"]), format="v2", note="device-resident, includes the info D2H sync; kernel_us from a separate per-launch-event pass",
+        device_round_trip=statistics.median(lat_dev),
+        tensor=str(wl["dims"]), format="v2",
+        note="device-resident, L2 flushed before every repetition; encode includes the header D2H sync "
+             "(scz_batch_sync); device_round_trip = scz_encode_batch + scz_decode_batch_device (headers stay "
+             "on the device); kernel_us from a separate per-launch-event pass",
         kernel_us={k: round(1e3 * ms / n, 2) for k, (ms, n) in sorted(kt.items(), key=lambda kv: -kv[1][0])})
     # the block-size trade-off: shorter v2 blocks shorten the serial rANS
     # chains (more blocks in flight for one tensor) at the cost of 128 state
@@ -776,7 +809,7 @@ class DeviceBatch:
     """Encode / decode of one device-resident batch through the C ABI on one
     library context, timed with CUDA events on the context's stream:
     encode = scz_encode_batch, decode = scz_decode_batch_async (after the
-    host read the headers with scz_batch_sync).  Optionally writes a 256 MB
+    host read the headers with scz_batch_sync).  Optionally reads a 256 MB
     buffer on the same stream before every timed repetition (L2 flush) when
     the batch is smaller than the 126 MB L2."""
 
@@ -786,12 +819,13 @@ class DeviceBatch:
         self.lib = self.ctx.lib
         self.native = _native
         self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=torch.device("cuda", device))
-        self.flush_buf = torch.empty(64 << 20, dtype=torch.float32, device=torch.device("cuda", device))
+        self.flush_buf = torch.ones(64 << 20, dtype=torch.float32, device=torch.device("cuda", device))
+        self.flush_sink = torch.empty(1, dtype=torch.float32, device=torch.device("cuda", device))
         self.batch = _native.Batch()
 
-    def flush(self):
+    def flush(self):  # read 256 MB (> L2): evicts the batch without leaving dirty lines
         with self.torch.cuda.stream(self.stream):
-            self.flush_buf.fill_(1.0)
+            self.torch.sum(self.flush_buf, dim=0, out=self.flush_sink)
 
     def run(self, x, out, B, T, q, fmt, bs, n_rows=-1, reps=5, warm=3, flush=False):
         """[(encode ms, decode ms)] of `reps` timed repetitions + the infos."""
