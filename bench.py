@@ -692,7 +692,7 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
     # lines without leaving 256 MB of dirty lines whose write-back would then
     # compete with the timed kernels
     flush_buf = torch.ones(64 << 20, dtype=torch.float32, device=x_dev.device)
-    flush_sink = torch.empty(1, dtype=torch.float32, device=x_dev.device)
+    flush_sink = torch.empty((), dtype=torch.float32, device=x_dev.device)
 
     def flush():
         with torch.cuda.stream(stream):
@@ -820,7 +820,7 @@ class DeviceBatch:
         self.native = _native
         self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=torch.device("cuda", device))
         self.flush_buf = torch.ones(64 << 20, dtype=torch.float32, device=torch.device("cuda", device))
-        self.flush_sink = torch.empty(1, dtype=torch.float32, device=torch.device("cuda", device))
+        self.flush_sink = torch.empty((), dtype=torch.float32, device=torch.device("cuda", device))
         self.batch = _native.Batch()
 
     def flush(self):  # read 256 MB (> L2): evicts the batch without leaving dirty lines
