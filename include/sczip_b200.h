@@ -11,6 +11,7 @@
  *   scz_compress        container.compress         container.py:73-106
  *   scz_decompress      container.decompress       container.py:109-121
  *   scz_encode_batch    compress over a device batch (SPEC.md:394 batch mode)
+ *   scz_encode_batch_ptrs  compress over a heterogeneous device batch
  *   scz_decode_batch    decompress over a device batch
  *   scz_quantize        tensor.params_for+quantize tensor.py:125-140
  *   scz_quantize_params tensor.quantize            tensor.py:130-140
@@ -137,6 +138,17 @@ int scz_decompress(scz_ctx* ctx, const scz_info* info, const uint32_t* freqs,
 int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t batch,
                      int q_bits, int64_t n_rows, int precision, int format,
                      uint32_t lanes, uint32_t block_syms, scz_batch* out);
+/* Heterogeneous batch: tensor i is numel[i] float32 at the
+ * DEVICE address d_x[i] (d_x and numel are host arrays).  Tensors of equal
+ * size are encoded together (gathered into one [B][T] array first unless they
+ * already are one) and every group's output is appended to one
+ * context-owned result: out describes all `batch` tensors in the caller's
+ * order, and scz_batch_sync / scz_decode_batch(_async) consume it like any
+ * batch (tensor i decodes to d_out + numel[0] + ... + numel[i-1]).  Returns
+ * after the device work (the staging tables are reused by the next call). */
+int scz_encode_batch_ptrs(scz_ctx* ctx, const float* const* d_x, const uint64_t* numel, uint32_t batch,
+                          int q_bits, int64_t n_rows, int precision, int format, uint32_t lanes,
+                          uint32_t block_syms, scz_batch* out);
 /* Wait for the batch, copy its infos to h_info[batch] and set payload_total. */
 int scz_batch_sync(scz_ctx* ctx, scz_batch* b, scz_info* h_info);
 /* Decode `batch` tensors described by h_info (host copy; its offsets index

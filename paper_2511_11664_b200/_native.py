@@ -80,6 +80,7 @@ EXPORTS = (
     "scz_quantize_params", "scz_dequantize", "scz_csr_encode", "scz_csr_decode", "scz_build_counts",
     "scz_normalize", "scz_rans_encode", "scz_rans_decode", "scz_search", "scz_compress_batch",
     "scz_decompress_batch", "scz_ctx_set_timing", "scz_ctx_read_timing", "scz_last_call_ms",
+    "scz_encode_batch_ptrs",
 )
 
 _lib = None
@@ -128,6 +129,7 @@ def load_library():
             "scz_ctx_set_timing": (I32, [P, I32]),
             "scz_ctx_read_timing": (I32, [P, ctypes.c_char_p, U64]),
             "scz_last_call_ms": (I32, [P, P]),
+            "scz_encode_batch_ptrs": (I32, [P, P, P, U32, I32, I64, I32, I32, U32, U32, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -207,6 +207,10 @@ struct scz_ctx {
         return SCZ_OK;
     }
     DevBuf candcnt, selbuf, dlut, probe, lbwords;
+    // heterogeneous batches (scz_encode_batch_ptrs): the combined result,
+    // the gathered inputs of a group, the group's pointer / order tables
+    DevBuf hx_info, hx_freqs, hx_blocks, hx_payload, hx_gather, hx_tab;
+    HostBuf hx_htab;
     // Allocation generation of THIS context's buffers: a cached graph holds
     // raw pointers into them, so it is stale once any of them reallocates
     // (other contexts' allocations do not invalidate it).
@@ -216,13 +220,14 @@ struct scz_ctx {
         for (DevBuf* b : {&x_in, &bitmap, &tile_stats, &tile_off, &state, &vhist, &v8, &cr, &hp, &rhist, &counts,
                           &terms, &freqs, &cum, &enctab, &slots, &block_len, &blk_off, &cand_out, &info, &payload,
                           &ticket, &selbuf, &dlut, &probe, &dsym_in, &dinfo, &dfreqs, &dblocks, &dpayload, &cumtab,
-                          &dblk_off, &dsym, &chunk_sum, &dstatus, &out_off, &dout, &candcnt, &lbwords})
+                          &dblk_off, &dsym, &chunk_sum, &dstatus, &out_off, &dout, &candcnt, &lbwords,
+                          &hx_info, &hx_freqs, &hx_blocks, &hx_payload, &hx_gather, &hx_tab})
             f(b);
     }
     template <class F>
     void for_each_host_buf(F f) {
         for (HostBuf* b : {&h_info, &h_payload, &h_freqs, &h_blocks, &h_status, &h_misc, &hb_info, &hb_payload,
-                           &hb_freqs, &hb_blocks})
+                           &hb_freqs, &hb_blocks, &hx_htab})
             f(b);
         for (HostBuf& b : h_stage) f(&b);
     }
@@ -544,6 +549,55 @@ __global__ void __launch_bounds__(256) k_pack(const scz_info* info, const uint8_
         d2[w] = sh ? __funnelshift_r(lo, sw[w + 1], sh) : lo;  // slots are padded: w+1 is readable
     }
     for (uint32_t i = head + 4 * nwords + threadIdx.x; i < len; i += 256) dst[i] = src[i];
+}
+
+// Heterogeneous batch (scz_encode_batch_ptrs): append the outputs of one
+// equal-size group (its own run_encode) to the combined result.  CTA b copies
+// tensor b's payload bytes (keeping their position relative to the group's
+// payload region) and writes its header, offsets rebased onto the combined
+// buffers, at its position in the caller's order.
+__global__ void __launch_bounds__(256) k_append_group(const scz_info* src_info, const uint32_t* order,
+                                                      scz_info* dst_info, const uint8_t* src_payload,
+                                                      uint8_t* dst_payload, uint64_t pbase, uint64_t fbase,
+                                                      uint64_t bbase) {
+    pdl_wait();
+    const uint32_t b = blockIdx.x;
+    const scz_info in = src_info[b];
+    if (in.status == SCZ_OK) {
+        const uint8_t* src = src_payload + in.payload_off;
+        uint8_t* dst = dst_payload + pbase + in.payload_off;
+        for (uint64_t i = threadIdx.x; i < in.payload_len; i += 256) dst[i] = src[i];
+    }
+    if (threadIdx.x == 0) {
+        scz_info o = in;
+        o.payload_off += pbase;
+        o.freqs_off += fbase;
+        o.blocks_off += bbase;
+        dst_info[order[b]] = o;
+    }
+}
+
+// Gather of equal-size tensors at arbitrary device addresses into one
+// contiguous [B][T] buffer: CTA (chunk, b) copies 16-byte aligned runs when
+// both ends allow it, else floats.
+__global__ void __launch_bounds__(256) k_gather(const float* const* src, uint64_t T, float* dst) {
+    pdl_wait();
+    const uint32_t b = blockIdx.y;
+    const float* s = src[b];
+    float* d = dst + (uint64_t)b * T;
+    const uint64_t per = ((T + gridDim.x - 1) / gridDim.x + 3) & ~3ull;
+    const uint64_t lo = (uint64_t)blockIdx.x * per, hi = min(T, lo + per);
+    if (lo >= hi) return;
+    const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0;
+    if (vec) {
+        const uint64_t n4 = (hi - lo) / 4;
+        const float4* s4 = reinterpret_cast<const float4*>(s + lo);
+        float4* d4 = reinterpret_cast<float4*>(d + lo);
+        for (uint64_t i = threadIdx.x; i < n4; i += 256) d4[i] = __ldg(s4 + i);
+        for (uint64_t i = lo + 4 * n4 + threadIdx.x; i < hi; i += 256) d[i] = s[i];
+    } else {
+        for (uint64_t i = lo + threadIdx.x; i < hi; i += 256) d[i] = s[i];
+    }
 }
 
 // Run `body` (stream-ordered launches only, no host syncs) through the graph
@@ -1362,6 +1416,106 @@ int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t ba
     out->freqs_total = (uint64_t)batch * pl.acap;
     out->blocks_total = (uint64_t)batch * pl.nblk_cap;
     ctx->last_batch = batch;
+    return SCZ_OK;
+}
+
+int scz_encode_batch_ptrs(scz_ctx* ctx, const float* const* d_x, const uint64_t* numel, uint32_t batch,
+                          int q_bits, int64_t n_rows, int precision, int format, uint32_t lanes,
+                          uint32_t block_syms, scz_batch* out) {
+    if (!ctx || !out || !d_x || !numel) return SCZ_INVALID_INPUT;
+    if (batch < 1) return ctx->fail(SCZ_INVALID_INPUT, "batch must be >= 1");
+    cudaSetDevice(ctx->device);
+    ctx->mark();
+    cudaStream_t s = ctx->stream;
+    // groups of equal element count, in first-appearance order
+    std::vector<uint64_t> sizes;
+    std::vector<std::vector<uint32_t>> groups;
+    for (uint32_t i = 0; i < batch; ++i) {
+        if (!d_x[i]) return ctx->fail(SCZ_INVALID_INPUT, "null tensor pointer %u", i);
+        size_t g = 0;
+        while (g < sizes.size() && sizes[g] != numel[i]) ++g;
+        if (g == sizes.size()) {
+            sizes.push_back(numel[i]);
+            groups.emplace_back();
+        }
+        groups[g].push_back(i);
+    }
+    std::vector<EncPlan> plans(groups.size());
+    uint64_t ptot = 0, ftot = 0, btot = 0, gmax = 0;
+    for (size_t g = 0; g < groups.size(); ++g) {
+        const uint32_t Bg = (uint32_t)groups[g].size();
+        int st = plan_encode(ctx, sizes[g], Bg, q_bits, n_rows, precision, format, lanes, block_syms, &plans[g]);
+        if (st) return st;
+        ptot += (uint64_t)Bg * plans[g].payload_cap;
+        ftot += (uint64_t)Bg * plans[g].acap;
+        btot += (uint64_t)Bg * plans[g].nblk_cap;
+        gmax = std::max<uint64_t>(gmax, (uint64_t)Bg * sizes[g]);
+    }
+    CK(ctx->hx_info.ensure((size_t)batch * sizeof(scz_info)));
+    CK(ctx->hx_freqs.ensure(ftot * 4 + 16));
+    CK(ctx->hx_blocks.ensure(btot * 4 + 16));
+    CK(ctx->hx_payload.ensure(ptot + 4096));
+    CK(ctx->hx_tab.ensure((size_t)batch * 16 + 64));
+    CK(ctx->hx_htab.ensure((size_t)batch * 16 + 64));
+    // host staging of the per-group pointer and order tables: every group's
+    // slice is written before the single upload, and the stream has finished
+    // with the previous call's tables (the call ends with a synchronisation)
+    const float** h_ptr = ctx->hx_htab.as<const float*>();
+    uint32_t* h_ord = reinterpret_cast<uint32_t*>(h_ptr + batch);
+    {
+        uint32_t k = 0;
+        for (auto& grp : groups)
+            for (uint32_t i : grp) {
+                h_ptr[k] = d_x[i];
+                h_ord[k] = i;
+                ++k;
+            }
+    }
+    CK(cudaMemcpyAsync(ctx->hx_tab.p, ctx->hx_htab.p, (size_t)batch * 12, cudaMemcpyHostToDevice, s));
+    const float** d_ptr = ctx->hx_tab.as<const float*>();
+    const uint32_t* d_ord = reinterpret_cast<const uint32_t*>(d_ptr + batch);
+    uint64_t pbase = 0, fbase = 0, bbase = 0;
+    uint32_t k0 = 0;
+    for (size_t g = 0; g < groups.size(); ++g) {
+        const EncPlan& pl = plans[g];
+        const uint32_t Bg = pl.B;
+        const uint64_t T = pl.T;
+        // inputs: used in place when the group is already one [Bg][T] array
+        bool contiguous = true;
+        for (uint32_t k = 1; k < Bg && contiguous; ++k)
+            contiguous = d_x[groups[g][k]] == d_x[groups[g][0]] + (uint64_t)k * T;
+        const float* dx = d_x[groups[g][0]];
+        if (!contiguous) {
+            CK(ctx->hx_gather.ensure((size_t)gmax * 4 + 16));
+            const uint32_t chunks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(64, T / 8192));
+            CK(launch_pdl(k_gather, dim3(chunks, Bg), 256, 0, s, d_ptr + k0, T, ctx->hx_gather.as<float>()));
+            LAUNCHED("k_gather");
+            dx = ctx->hx_gather.as<float>();
+        }
+        int st = run_encode(ctx, dx, pl, nullptr);
+        if (st) return st;
+        CK(launch_pdl(k_append_group, dim3(Bg), 256, 0, s, ctx->info.as<scz_info>(), d_ord + k0,
+                      ctx->hx_info.as<scz_info>(), ctx->payload.as<uint8_t>(), ctx->hx_payload.as<uint8_t>(), pbase,
+                      fbase, bbase));
+        LAUNCHED("k_append_group");
+        CK(cudaMemcpyAsync(ctx->hx_freqs.as<uint32_t>() + fbase, ctx->freqs.p, (size_t)Bg * pl.acap * 4,
+                           cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->hx_blocks.as<uint32_t>() + bbase, ctx->block_len.p, (size_t)Bg * pl.nblk_cap * 4,
+                           cudaMemcpyDeviceToDevice, s));
+        pbase += (uint64_t)Bg * pl.payload_cap;
+        fbase += (uint64_t)Bg * pl.acap;
+        bbase += (uint64_t)Bg * pl.nblk_cap;
+        k0 += Bg;
+    }
+    CK(cudaStreamSynchronize(s));  // the group buffers are reused by the next group / call
+    out->batch = batch;
+    out->d_info = ctx->hx_info.as<scz_info>();
+    out->d_freqs = ctx->hx_freqs.as<uint32_t>();
+    out->d_block_bytes = ctx->hx_blocks.as<uint32_t>();
+    out->d_payload = ctx->hx_payload.as<uint8_t>();
+    out->payload_total = 0;
+    out->freqs_total = ftot;
+    out->blocks_total = btot;
     return SCZ_OK;
 }
 

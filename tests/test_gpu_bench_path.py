@@ -262,3 +262,79 @@ def test_mixed_symbol_classes_in_one_batch_decode(fmt):
     for c, o in zip(cs, outs):
         want = sz.decompress(c)
         assert np.array_equal(o.data.view(np.uint32), want.data.view(np.uint32))
+
+
+@pytest.mark.parametrize("fmt", [2, 1])
+def test_heterogeneous_device_batch_encode(fmt):
+    """scz_encode_batch_ptrs: tensors of several sizes at
+    arbitrary device addresses, interleaved, one of them non-finite; every
+    container equals the oracle's, the failed tensor reports InvalidInput, and
+    one batch decode reconstructs the rest in the caller's order."""
+    import torch
+
+    shapes = [(1, 64, 28, 28), (3, 5, 7), (1, 32, 14, 14), (1, 64, 28, 28), (601,), (1, 32, 14, 14),
+              (1, 64, 28, 28)]
+    specs = [dict(kind="relu-laplace" if i % 2 == 0 else "signed", dims=d, sparsity=0.5, seed=400 + i)
+             for i, d in enumerate(shapes)]
+    xs = [make_input(sp).astype(np.float32) for sp in specs]
+    xs[5][7] = np.inf
+    # tensors 0 and 3 share one [2][T] device array in order (a group used in place
+    # needs consecutive addresses; here they are not consecutive in the batch, so the
+    # group {0, 3, 6} is gathered), the others are separate allocations
+    pair = torch.from_numpy(np.stack([xs[0], xs[3]])).cuda()
+    dev = [pair[0], torch.from_numpy(xs[1]).cuda(), torch.from_numpy(xs[2]).cuda(), pair[1],
+           torch.from_numpy(xs[4]).cuda(), torch.from_numpy(xs[5]).cuda(), torch.from_numpy(xs[6]).cuda()]
+    B = len(dev)
+    ptrs = (ctypes.c_void_p * B)(*[t.data_ptr() for t in dev])
+    numel = (ctypes.c_uint64 * B)(*[t.numel() for t in dev])
+    ctx = _native.Context(0)
+    lib = ctx.lib
+    batch = _native.Batch()
+    infos = (_native.Info * B)()
+    for rep in range(2):
+        ctx.check(lib.scz_encode_batch_ptrs(ctx.h, ptrs, numel, B, 8, -1, 14, fmt, 32, 1024, ctypes.byref(batch)))
+        ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), infos))
+        assert [infos[i].status for i in range(B)] == [0, 0, 0, 0, 0, 1, 0]
+        ok = [i for i in range(B) if infos[i].status == 0]
+        pay = d2h(batch.d_payload, int(batch.payload_total))
+        fr = d2h(batch.d_freqs, 4 * int(batch.freqs_total)).view(np.uint32)
+        bl = d2h(batch.d_block_bytes, 4 * int(batch.blocks_total)).view(np.uint32)
+        for i in ok:
+            inf = infos[i]
+            freqs = fr[inf.freqs_off: inf.freqs_off + inf.alphabet].astype(np.int64)
+            blocks = bl[inf.blocks_off: inf.blocks_off + inf.n_blocks].copy() if fmt == 2 else None
+            c = container._container_from_info(inf, shapes[i], freqs, blocks,
+                                               pay[inf.payload_off: inf.payload_off + inf.payload_len].tobytes())
+            ref = orc.compress(xs[i], shapes[i], 8, None, 14, fmt=fmt, lanes=32, block_syms=1024)
+            assert container.to_bytes(c) == orc.to_bytes(ref), (i, rep)
+        # one batch decode of the good tensors (their infos index the combined buffers)
+        sub = (_native.Info * len(ok))(*[infos[i] for i in ok])
+        tot = sum(dev[i].numel() for i in ok)
+        out = torch.full((tot,), -1.0, device="cuda")
+        ctx.check(lib.scz_decode_batch_async(ctx.h, sub, len(ok), ctypes.c_void_p(batch.d_freqs),
+                                             ctypes.c_void_p(batch.d_block_bytes), ctypes.c_void_p(batch.d_payload),
+                                             ctypes.c_void_p(out.data_ptr())))
+        st = (ctypes.c_int32 * len(ok))()
+        ctx.check(lib.scz_decode_status(ctx.h, len(ok), st))
+        assert list(st) == [0] * len(ok)
+        got = out.cpu().numpy()
+        pos = 0
+        for i in ok:
+            want = orc.decompress(orc.compress(xs[i], shapes[i], 8, None, 14, fmt=fmt, lanes=32, block_syms=1024))
+            assert np.array_equal(got[pos: pos + xs[i].size].view(np.uint32), want.view(np.uint32)), (i, rep)
+            pos += xs[i].size
+
+
+def test_compress_many_mixed_shapes():
+    """container.compress_many groups mixed shapes and keeps the input order."""
+    shapes = [(1, 32, 14, 14), (3, 5, 7), (1, 32, 14, 14), (601,)]
+    ts = [sz.FeatureTensor(d, make_input(dict(kind="relu-laplace", dims=d, sparsity=0.4, seed=i)))
+          for i, d in enumerate(shapes)]
+    for fmt in (1, 2):
+        many = container.compress_many(ts, 6, format=fmt, block_syms=512)
+        for t, c in zip(ts, many):
+            assert c.dims == t.dims
+            assert container.to_bytes(c) == container.to_bytes(sz.compress(t, 6, format=fmt, block_syms=512))
+        outs = container.decompress_many(many)
+        for c, o in zip(many, outs):
+            assert np.array_equal(o.data.view(np.uint32), sz.decompress(c).data.view(np.uint32))
