@@ -788,7 +788,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         cp.hp = ctx->hp.as<uint32_t>();
         cp.hp_stride = (uint32_t)pl.period;
         dim3 g(ceil_div_u32(cp.period_words, 128), ceil_div_u32(cp.n_rows, cp.rows_per_cta), B);
-        CK(launch_pdl(k_colhist, g, 128, 0, s, cp));
+        CK(launch_pdl(k_colhist, g, 128, g.y == 1 ? (size_t)128 * 33 * 4 : 0, s, cp));
         LAUNCHED("k_colhist");
 
     }

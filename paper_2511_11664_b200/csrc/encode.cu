@@ -460,7 +460,9 @@ __global__ void __launch_bounds__(128) k_colhist(ColHistParams p) {
     const bool single = gridDim.y == 1;  // this CTA alone covers its columns
     if (q >= p.period_words && !single) return;
     const uint32_t r0 = blockIdx.y * p.rows_per_cta;
-    const uint32_t r1 = min(p.n_rows, r0 + p.rows_per_cta);
+    // (in the single-CTA form, threads past the last column only take part
+    // in the transposed store's barrier)
+    const uint32_t r1 = q < p.period_words ? min(p.n_rows, r0 + p.rows_per_cta) : r0;
     const uint32_t* bm = p.bitmap + (uint64_t)b * p.words_pad;
     // nib[j] holds eight 4-bit counters: bit positions j, j + 4, ..., j + 28
     // of the word column, flushed into cnt[] every 15 rows (SWAR: 3
@@ -498,7 +500,8 @@ __global__ void __launch_bounds__(128) k_colhist(ColHistParams p) {
     if (single) {
         // the only contribution to these counters: plain stores, transposed
         // through shared memory so each warp writes 128 contiguous bytes
-        __shared__ uint32_t s_cnt[128 * 33];
+        // (dynamic shared memory: launches of the atomic form carry none)
+        extern __shared__ uint32_t s_cnt[];  // [128 * 33]
 #pragma unroll
         for (int i = 0; i < 32; ++i) s_cnt[threadIdx.x * 33 + i] = cnt[i];
         __syncthreads();

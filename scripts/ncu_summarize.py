@@ -15,7 +15,9 @@ METRICS = [
     "gpu__time_duration.sum",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
-    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__inst_executed.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
@@ -91,11 +93,13 @@ def main():
             f"## {k}  ({len(vs)} launches)",
             f"    duration            {dur / 1e3:10.2f} us",
             f"    dram read + write   {dram / 1e6:10.2f} MB   ({dram / dur:.0f} GB/s achieved)" if dur == dur and dur else "",
-            f"    dram throughput     {mean.get('dram__throughput.avg.pct_of_peak_sustained_elapsed', 0):10.1f} % of peak",
+            f"    dram throughput     {mean.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 0):10.1f} % of peak",
             f"    SM throughput       {mean.get('sm__throughput.avg.pct_of_peak_sustained_elapsed', 0):10.1f} %",
             f"    issue active        {mean.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):10.1f} %",
             f"    warps active        {mean.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):10.1f} % of max",
             f"    L2 hit rate         {mean.get('lts__t_sector_hit_rate.pct', 0):10.1f} %",
+            f"    warp instructions   {mean.get('smsp__inst_executed.sum', 0):10.3g}",
+            f"    smem bank conflicts {mean.get('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 0):10.3g}",
             f"    registers / thread  {mean.get('launch__registers_per_thread', 0):10.0f}",
             f"    grid x block        {mean.get('launch__grid_size', 0):10.0f} x {mean.get('launch__block_size', 0):.0f}",
             "",
