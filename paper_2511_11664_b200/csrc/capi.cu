@@ -444,7 +444,7 @@ int plan_encode(scz_ctx* ctx, uint64_t T, uint32_t B, int q_bits, int64_t n_rows
         pl->nblk_cap = 1;
         pl->slot_cap = 4 + 2 * pl->L_max;
     }
-    pl->slot_cap = (pl->slot_cap + 15) & ~15ull;
+    pl->slot_cap = (pl->slot_cap + 127) & ~127ull;  // 128-byte lines (the encoder discards a slot's lines)
     pl->payload_cap = (uint64_t)pl->nblk_cap * pl->slot_cap;
     return SCZ_OK;
 }

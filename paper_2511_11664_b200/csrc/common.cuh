@@ -253,6 +253,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // mbarrier + bulk (TMA 1-D) copies: one thread moves a whole table into
 // shared memory; the CTA waits on the barrier's transaction count.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// A value the compiler must keep in a register (it cannot rematerialise the
+// output of a volatile asm): used for 32-bit shared addresses in hot loops.
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");

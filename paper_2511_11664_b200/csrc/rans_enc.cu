@@ -220,9 +220,7 @@ __device__ __forceinline__ void enc_apply(EncLane& L, const EncTab& t, bool live
 // with cmpl = 2^n - f; f = 1 as rcp = 2^32 - 1, shift 0, bias = cum + 2^n - 1),
 // so x' = x + bias + q * cmpl with q = umulhi(x, rcp) >> shift equals
 // (x / f << n) + cum + x % f (rans.py:143-144) for every f >= 1 -- three
-// dependent operations on the state.  Bytes go to a per-warp shared ring
-// (ob, RB bytes, same backwards order as the slot), flushed in 16-byte chunks.
-constexpr uint32_t ENC_RB = 2048;
+// dependent operations on the state.
 __device__ __forceinline__ EncTab enc_tab_fast(const EncTab& e, int n) {
     EncTab f;
     f.freq = e.freq << (31 - n);
@@ -237,25 +235,178 @@ __device__ __forceinline__ EncTab enc_tab_fast(const EncTab& e, int n) {
     }
     return f;
 }
-// obs: the warp's ring as a 32-bit shared address (plus the masked position;
-// not OR'd: static shared offsets start after the reserved 1 KB, so the
-// ring base is not ENC_RB-aligned in the address space).
-__device__ __forceinline__ void enc_apply_ring(EncLane& L, const EncTab& t, bool live, uint32_t gtm, uint32_t obs) {
-    const bool e1 = live && L.x >= t.freq;
-    const bool e2 = live && (L.x >> 8) >= t.freq;  // implies e1
+// The u8 pipeline path (RING): symbols staged per warp in shared memory by
+// cp.async, three 1 KB chunks (32 steps each) in flight ahead of the coder;
+// table entries of the next four steps loaded while the current four are
+// coded; emitted bytes go DOWN a per-warp 2 KB shared window from its top
+// (the byte of warp-order position k of a step lands at base - 1 - k, so the
+// window holds the bytes already in decoder order) and leave in 16-byte
+// chunks every 16 steps, after which the < 16 leftover bytes move back to the
+// top.  No address masking in the step: position = base - (bytes of the
+// higher lanes), one IADD3; the second byte's store has an immediate offset.
+constexpr uint32_t ENC_OB = 2048;    // output window per warp (16 steps emit <= 1024 bytes)
+constexpr uint32_t ENC_SCH = 1024;   // symbol chunk: 32 steps x 32 lanes
+constexpr int ENC_NSCH = 3;          // symbol chunks per warp (two in flight ahead)
+
+template <bool PRED>
+__device__ __forceinline__ void enc_step_lin(uint32_t& x, uint32_t& base, const EncTab& t, uint32_t gtm,
+                                             bool live) {
+    const uint32_t x8 = x >> 8;
+    const bool e1 = (!PRED || live) && x >= t.freq;   // t.freq holds the bound f << (31 - n)
+    const bool e2 = (!PRED || live) && x8 >= t.freq;  // implies e1
     const uint32_t b1 = __ballot_sync(0xffffffffu, e1);
     const uint32_t b2 = __ballot_sync(0xffffffffu, e2);
-    // bytes before this lane's first: ring positions -(n + 1), -(n + 2)
-    const uint32_t n = L.emitted + __popc(b1 & gtm) + __popc(b2 & gtm);
-    sts_u8_if(obs + (~n & (ENC_RB - 1)), L.x, e1);
-    sts_u8_if(obs + (~(n + 1) & (ENC_RB - 1)), L.x >> 8, e2);
-    L.emitted += __popc(b1) + __popc(b2);
-    uint32_t x = L.x;
-    if (e1) x >>= 8;  // two predicated shifts (e2 implies e1)
-    if (e2) x >>= 8;
-    const uint32_t q = __funnelshift_r(__umulhi(x, t.rcp), 0u, t.shift);
-    const uint32_t xn = x + t.cum + q * (t.shift >> 16);
-    if (live) L.x = xn;
+    const uint32_t pos = base - __popc(b1 & gtm) - __popc(b2 & gtm);
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.u8 [%0+-1], %1;\n}\n" ::"r"(pos), "r"(x),
+                 "r"((uint32_t)e1)
+                 : "memory");
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.u8 [%0+-2], %1;\n}\n" ::"r"(pos), "r"(x8),
+                 "r"((uint32_t)e2)
+                 : "memory");
+    base -= __popc(b1) + __popc(b2);
+    uint32_t xs = e1 ? x8 : x;
+    if (e2) xs >>= 8;
+    const uint32_t q = __funnelshift_r(__umulhi(xs, t.rcp), 0u, t.shift);
+    const uint32_t xn = q * (t.shift >> 16) + (xs + t.cum);
+    x = (!PRED || live) ? xn : x;
+}
+
+__device__ __forceinline__ EncTab lds_tab16(uint32_t saddr) {
+    EncTab t;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(t.freq), "=r"(t.cum), "=r"(t.rcp), "=r"(t.shift)
+                 : "r"(saddr));
+    return t;
+}
+
+__device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uint32_t len, int steps,
+                                            const EncTab* s_tab, uint8_t* slot_end, uint32_t warp, uint32_t lane,
+                                            uint32_t gtm) {
+    __shared__ __align__(16) uint8_t s_sym[ENC2_WPB][ENC_NSCH][ENC_SCH];
+    __shared__ __align__(16) uint8_t s_ob[ENC2_WPB][ENC_OB];
+    // shared addresses pinned in registers (opaque copies: otherwise the
+    // compiler re-derives the shared window base, S2R included, per load)
+    const uint32_t tab_s = opaque_u32(smem_u32(s_tab));
+    const uint32_t ob_s = opaque_u32(smem_u32(s_ob[warp]));
+    const uint32_t top = ob_s + ENC_OB;
+    const uint32_t sym_s = opaque_u32(smem_u32(s_sym[warp][0]) + lane);
+    uint32_t base = top;   // window bytes [base, rtop) are pending
+    uint32_t rtop = top;   // [rtop, top) already went to the slot
+    uint32_t flushed = 0;  // bytes already in the slot (multiple of 16)
+    uint32_t x = E.x;
+    // window byte at address a goes to slot_end - flushed - (rtop - a): the
+    // complete 16-byte chunks below rtop leave; when less than one flush
+    // interval (16 steps, <= 1024 bytes) of room is left below base, the
+    // < 16 leftover bytes move up to the top
+    auto flush = [&]() {
+        __syncwarp();
+        const uint32_t nfl = (rtop - base) & ~15u;
+        for (uint32_t c = 16 * lane; c < nfl; c += 512) {
+            uint4 v;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(rtop - c - 16)
+                         : "memory");
+            *reinterpret_cast<uint4*>(slot_end - flushed - c - 16) = v;
+        }
+        flushed += nfl;
+        rtop -= nfl;
+        if (base < ob_s + 1024) {
+            const uint32_t rem = rtop - base;
+            const uint32_t v = lane < rem ? lds_u8(base + lane) : 0u;
+            __syncwarp();
+            if (lane < rem) sts_u8_if(top - rem + lane, v, true);
+            rtop = top;
+            base = top - rem;
+        }
+        __syncwarp();
+    };
+    auto fetch = [&](int g) {
+        if (g >= 0) {
+            uint8_t* dst = s_sym[warp][g % ENC_NSCH] + 16 * lane;
+            const uint8_t* src = gsym + (size_t)g * ENC_SCH + 16 * lane;
+            cp_async16(dst, src);
+            cp_async16(dst + 512, src + 512);
+        }
+        cp_async_commit();
+    };
+    if (steps > 0) {
+        int cg = (steps - 1) >> 5;  // chunk being read (landed)
+        fetch(cg);
+        fetch(cg - 1);
+        fetch(cg - 2);
+        cp_async_wait<2>();
+        __syncwarp();
+        uint32_t symc = sym_s + (uint32_t)(cg % ENC_NSCH) * ENC_SCH;
+        // chunk of step s: leaving chunk cg frees its slot for chunk cg - 3
+        auto ensure = [&](int s) {
+            if ((s >> 5) != cg) {
+                __syncwarp();
+                fetch(cg - 3);
+                --cg;
+                cp_async_wait<2>();
+                __syncwarp();
+                symc = sym_s + (uint32_t)(cg % ENC_NSCH) * ENC_SCH;
+            }
+        };
+        auto sym_at = [&](int s) -> uint32_t { return symc + (uint32_t)(s & 31) * 32; };
+        int s = steps - 1;
+        if (len & 31u) {  // the highest step of the tensor's last block is partial
+            const bool act = (uint32_t)s * 32 + lane < len;
+            const EncTab t = lds_tab16(tab_s + 16 * (act ? lds_u8(sym_at(s)) : 0u));
+            enc_step_lin<true>(x, base, t, gtm, act);
+            if ((s & 15) == 0) flush();
+            --s;
+        }
+        for (; s >= 0 && (s & 3) != 3; --s) {  // align the rest to groups of four steps
+            ensure(s);
+            enc_step_lin<false>(x, base, lds_tab16(tab_s + 16 * lds_u8(sym_at(s))), gtm, true);
+            if ((s & 15) == 0) flush();
+        }
+        // groups of four steps (never across a chunk or a flush boundary).
+        // Entry k of the next group loads right after step k of this one
+        // used its registers, four steps ahead of its use; the next group's
+        // symbols load at the start of this one.
+        if (s >= 3) {
+            ensure(s);
+            const uint32_t a = sym_at(s);
+            uint32_t y0 = lds_u8(a), y1 = lds_u8(a - 32), y2 = lds_u8(a - 64), y3 = lds_u8(a - 96);
+            EncTab t0 = lds_tab16(tab_s + 16 * y0), t1 = lds_tab16(tab_s + 16 * y1);
+            EncTab t2 = lds_tab16(tab_s + 16 * y2), t3 = lds_tab16(tab_s + 16 * y3);
+#pragma unroll 1
+            for (;;) {
+                const int sn = s - 4;
+                const bool more = sn >= 3;
+                if (more) {
+                    ensure(sn);
+                    const uint32_t an = sym_at(sn);
+                    y0 = lds_u8(an);
+                    y1 = lds_u8(an - 32);
+                    y2 = lds_u8(an - 64);
+                    y3 = lds_u8(an - 96);
+                }
+                // unconditional: after the last group these reload entries
+                // of the last symbols (harmless, unused)
+                enc_step_lin<false>(x, base, t0, gtm, true);
+                t0 = lds_tab16(tab_s + 16 * y0);
+                enc_step_lin<false>(x, base, t1, gtm, true);
+                t1 = lds_tab16(tab_s + 16 * y1);
+                enc_step_lin<false>(x, base, t2, gtm, true);
+                t2 = lds_tab16(tab_s + 16 * y2);
+                enc_step_lin<false>(x, base, t3, gtm, true);
+                t3 = lds_tab16(tab_s + 16 * y3);
+                if (((s - 3) & 15) == 0) flush();
+                s = sn;
+                if (!more) break;
+            }
+        }
+    }
+    cp_async_wait<0>();
+    // the last (< 16) bytes, then the emitted count
+    const uint32_t pend = rtop - base;
+    if (lane < pend) slot_end[-(int32_t)(flushed + pend) + (int32_t)lane] = (uint8_t)lds_u8(base + lane);
+    E.emitted = flushed + pend;
+    E.x = x;
 }
 
 template <class Src, bool SMEM, bool CHECK>
@@ -297,80 +448,7 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
     uint8_t* slot_end = p.slots + ((uint64_t)b * p.slots_per_tensor + blk + 1) * p.slot_cap;
     EncLane E{STATE_LOW, 0u, 0u};
     if constexpr (RING) {
-        // u8 symbols staged through a per-warp 2 x 1 KB shared ring (chunk g =
-        // steps [32g, 32g + 32) = block bytes [1024g, 1024g + 1024)), fetched
-        // one chunk ahead with cp.async; the table entry of the next step is
-        // loaded while the current one is coded.  Output bytes collect in a
-        // per-warp shared ring and leave in 16-byte chunks every 16 steps.
-        __shared__ __align__(16) uint8_t s_ring[ENC2_WPB][2][1024];
-        __shared__ __align__(16) uint8_t s_ob[ENC2_WPB][ENC_RB];
-        uint8_t* ob = s_ob[warp];
-        const uint32_t obs = (uint32_t)__cvta_generic_to_shared(ob);
-        uint32_t flushed = 0;  // bytes already in the slot (multiple of 16)
-        auto flush = [&]() {   // every complete 16-byte chunk since the last flush
-            const uint32_t upto = E.emitted & ~15u;
-            for (uint32_t c = flushed + 16 * lane; c < upto; c += 512)
-                *reinterpret_cast<uint4*>(slot_end - c - 16) =
-                    *reinterpret_cast<const uint4*>(ob + ((0u - c - 16) & (ENC_RB - 1)));
-            flushed = upto;
-        };
-        const uint8_t* gsym = cur.d;
-        auto fetch = [&](int g) {
-            if (g >= 0) {
-                uint8_t* dst = s_ring[warp][g & 1] + 16 * lane;
-                const uint8_t* src = gsym + (size_t)g * 1024 + 16 * lane;
-                cp_async16(dst, src);
-                cp_async16(dst + 512, src + 512);
-            }
-            cp_async_commit();
-        };
-        if (steps > 0) {
-            const int s_top = steps - 1, g_top = s_top >> 5;
-            fetch(g_top);
-            fetch(g_top - 1);
-            for (int g = g_top; g >= 0; --g) {
-                cp_async_wait<1>();
-                __syncwarp();
-                const uint8_t* rs = s_ring[warp][g & 1] + lane;
-#pragma unroll 1
-                for (int h = 1; h >= 0; --h) {  // half-chunks of 16 steps
-                    const int lo = g * 32 + 16 * h;
-                    int s = min(lo + 15, s_top);
-                    if (s < lo) continue;
-                    EncTab t;
-                    if (s == s_top) {  // the highest step may be partial
-                        const bool act = (uint32_t)s * 32 + lane < len;
-                        t = s_tab[act ? rs[(s & 31) * 32] : 0];
-                        enc_apply_ring(E, t, act, gtm, obs);
-                        --s;
-                    }
-                    // groups of four steps: the four table entries are loaded
-                    // up front (symbols do not depend on the state)
-#pragma unroll 1
-                    for (; s - 3 >= lo; s -= 4) {
-                        // s - 3 .. s lie in one half-chunk: no wrap, one base
-                        const uint8_t* rp = rs + (s & 31) * 32;
-                        const EncTab t0 = s_tab[rp[0]];
-                        const EncTab t1 = s_tab[rp[-32]];
-                        const EncTab t2 = s_tab[rp[-64]];
-                        const EncTab t3 = s_tab[rp[-96]];
-                        enc_apply_ring(E, t0, true, gtm, obs);
-                        enc_apply_ring(E, t1, true, gtm, obs);
-                        enc_apply_ring(E, t2, true, gtm, obs);
-                        enc_apply_ring(E, t3, true, gtm, obs);
-                    }
-                    for (; s >= lo; --s) enc_apply_ring(E, s_tab[rs[(s & 31) * 32]], true, gtm, obs);
-                    __syncwarp();
-                    flush();
-                }
-                __syncwarp();
-                fetch(g - 2);
-            }
-        }
-        cp_async_wait<0>();
-        // the last partial chunk, byte by byte
-        const uint32_t k = flushed + lane;
-        if (k < E.emitted) slot_end[-(int32_t)k - 1] = ob[(0u - k - 1) & (ENC_RB - 1)];
+        enc_v2_ring(E, cur.d, len, steps, s_tab, slot_end, warp, lane, gtm);
     } else if (steps > 0) {
         // the highest step may be partial: peel it
         const int s_top = steps - 1;
@@ -415,6 +493,13 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
         __syncwarp();     // the slot bytes of every lane are visible to the warp
         const uint32_t excl = chunk_prefix(pk.lb + (uint64_t)b * p.slots_per_tensor, blk, blen);
         warp_copy_bytes(pk.payload + (uint64_t)b * pk.pcap + excl, start, blen, lane);
+        // the slot is dead now: drop its L2 lines without a write-back to HBM
+        // (slots are 128-byte aligned; the lines below `start` hold only this
+        // slot's unused head)
+        __syncwarp();
+        for (uintptr_t a = (reinterpret_cast<uintptr_t>(start) & ~(uintptr_t)127) + 128 * lane;
+             a < reinterpret_cast<uintptr_t>(slot_end); a += 128 * 32)
+            asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(a) : "memory");
         if (blk == nblk - 1 && lane == 0) {
             __threadfence();  // every block published: their error bits are visible
             const uint32_t eb = *(volatile uint32_t*)&st.errbits;
@@ -434,7 +519,7 @@ __global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src 
 // class is known only after k_select), so no launch is spent on an empty
 // class.  u32 tensors (K > 65535) go to k_rans_enc_v2<SplitSrc<uint32_t>>.
 template <bool SMEM>
-__global__ void __launch_bounds__(ENC2_WPB * 32, 10)
+__global__ void __launch_bounds__(ENC2_WPB * 32, 8)
     k_rans_enc_v2_u8u16(EncParams p, Contig8Src s8, SplitSrc<uint16_t> s16, PackParams pk) {
     pdl_wait();
     const TensorState& st = p.state[blockIdx.x];
