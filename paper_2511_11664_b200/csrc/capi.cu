@@ -877,21 +877,29 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     }
     sel.dump = dump;
     sel.groups = 1;
-    if (pl.searching && pl.acap <= SEL_WARP_ACAP) {
-        // small batches: spread the candidates over several CTAs per tensor
+    // small batches: one 1024-thread CTA per tensor and pass (the decision
+    // runs once per tensor; its fp64 terms and the normalise spread over 32
+    // warps of one SM); batches: 256 threads, candidates over several CTAs
+    // per tensor while the grid would not fill the GPU
+    const bool sel_wide = B <= (uint32_t)ctx->num_sms / 8;
+    const int sel_nt = sel_wide ? SEL_THREADS_WIDE : SEL_THREADS;
+    if (pl.searching && pl.acap <= SEL_WARP_ACAP && !sel_wide) {
         const uint32_t per_cta = SEL_THREADS / 32;
         const uint32_t want = ceil_div_u32(n_first, per_cta);
         const uint32_t room = std::max<uint32_t>(1, (uint32_t)(2 * ctx->num_sms) / B);
         sel.groups = std::max<uint32_t>(1, std::min(want, room));
     }
+    // cost-pass slots per round: as many as the warps, within ~96 KB
+    sel.nb = (uint32_t)std::max<size_t>(2, std::min<size_t>(sel_nt / 32, (96u << 10) / ((size_t)pl.acap * 16)));
     {   // (the tickets were zeroed by k_stats)
         sel.gcost = ctx->selbuf.as<double>();
         sel.gacnt = reinterpret_cast<uint32_t*>(sel.gcost + (size_t)B * MAX_CAND * 2);
         sel.ticket = sel_ticket;
     }
-    const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)rh_total) : 0;
+    const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)rh_total, sel.nb) : 0;
+    auto k_sel = sel_wide ? k_select<SEL_THREADS_WIDE> : k_select<SEL_THREADS>;
     if (sel_smem > 0)  // static BlockScratch + dynamic may pass 48 KB: always opt in
-        CK(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
+        CK(cudaFuncSetAttribute(k_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
     const bool probe = getenv("SCZ_SELECT_PROBE") && !ctx->timing && B <= 64;
     if (probe) {  // debug timeline of k_select phases (synchronous; graphs off)
         CK(ctx->probe.ensure((size_t)B * sel.groups * 16 * 8));
@@ -901,7 +909,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     sel.pass = split ? 1 : 0;
     sel.c_begin = 0;
     sel.c_end = n_first;
-    CK(launch_pdl(k_select, dim3(sel.groups, B), SEL_THREADS, sel_smem, s, sel));
+    CK(launch_pdl(k_sel, dim3(sel.groups, B), sel_nt, sel_smem, s, sel));
     LAUNCHED("k_select");
     if (split) {  // the rest of the candidates, pending tensors only
         if ((rst = rowhist_pass(n_first, ncand, true)) != SCZ_OK) return rst;
@@ -910,8 +918,9 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         sel2.c_begin = n_first;
         sel2.c_end = ncand;
         const uint32_t room = std::max<uint32_t>(1, (uint32_t)(2 * ctx->num_sms) / B);
-        sel2.groups = std::max<uint32_t>(1, std::min(ceil_div_u32(ncand - n_first, SEL_THREADS / 32), room));
-        CK(launch_pdl(k_select, dim3(sel2.groups, B), SEL_THREADS, sel_smem, s, sel2));
+        sel2.groups = sel_wide ? 1
+                               : std::max<uint32_t>(1, std::min(ceil_div_u32(ncand - n_first, SEL_THREADS / 32), room));
+        CK(launch_pdl(k_sel, dim3(sel2.groups, B), sel_nt, sel_smem, s, sel2));
         LAUNCHED("k_select/2");
     }
     if (probe) {
@@ -921,7 +930,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         for (uint32_t i = 0; i < B * sel.groups; ++i) {
             const unsigned long long t0 = h[(size_t)(i - i % sel.groups) * 16];
             fprintf(stderr, "k_select b=%u g=%u ns:", i / sel.groups, i % sel.groups);
-            for (int k = 1; k < 7; ++k)
+            for (int k = 1; k < 14; ++k)
                 fprintf(stderr, " %lld", h[(size_t)i * 16 + k] ? (long long)(h[(size_t)i * 16 + k] - t0) : -1ll);
             fprintf(stderr, "\n");
         }
