@@ -343,7 +343,9 @@ __global__ void __launch_bounds__(TILE_THREADS, 5) k_quantize(QuantParams p) {
     s_wbits[threadIdx.x] = myword;
     uint32_t tot;
     s_wpre[threadIdx.x] = block_exclusive_scan<TILE_THREADS>(__popc(myword), s_scan, &tot);
-    // (block_exclusive_scan ends with __syncthreads)
+    // a warp reads only its own 32 words of s_wpre (written by its lanes after
+    // the scan's closing barrier): a warp barrier orders them (racecheck)
+    __syncwarp();
     const uint32_t base_rank = p.tile_off[(uint64_t)b * p.n_tiles + tile];
     const double scale = st.scale;
     const double zf = (double)st.zero_point;

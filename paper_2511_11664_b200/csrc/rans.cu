@@ -340,6 +340,7 @@ struct Ring {
     uint8_t* buf;
     uint64_t filled;  // absolute (payload-buffer) address up to which bytes are loaded
     __device__ __forceinline__ void fill_to(const uint8_t* payload, uint64_t want, uint32_t lane) {
+        __syncwarp();  // every lane's earlier reads of the slots about to be refilled (racecheck)
         while (filled < want) {  // warp-uniform
             uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(payload + filled) + lane);
             *reinterpret_cast<uint32_t*>(buf + ((filled + 4 * lane) & (RING - 1))) = w;
