@@ -974,12 +974,9 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
                 pk.write_failed = 0;  // the first launch wrote the failed tensors' headers
                 LAUNCHED(wname<S>("k_rans_enc_v2"));
             } else {
-                if constexpr (std::is_same<Src, Contig8Src>::value) {
-                    if (pl.L_max < (1ull << 30)) CK(launch_pdl(k_rans_enc_v1_fast, B, 32, 0, s, ep, src));
-                    else CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
-                } else {
-                    CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
-                }
+                // role-split serial coder (rans_v1.cu); 32-bit stream offsets
+                if (pl.L_max < (1ull << 30)) CK(launch_pdl(k_rans_enc_v1p<Src>, B, V1_THREADS, 0, s, ep, src));
+                else CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
                 LAUNCHED(wname<S>("k_rans_enc_v1"));
             }
             return SCZ_OK;
@@ -1245,12 +1242,12 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
         if (any_v1) {
             bool fast = Lmax < (1ull << 30);  // 32-bit stream offsets in the fast kernel
             if constexpr (sizeof(L) == 4) fast = false;
-            if (fast) {  // u8 / u16 classes: the latency-optimised serial decoder
-                const size_t smem = dec_v1_smem(maxn, sizeof(L));
+            if (fast) {  // u8 / u16 classes: the role-split serial decoder (rans_v1.cu)
+                const size_t smem = dec_v1p_smem(maxn, sizeof(L));
                 if constexpr (sizeof(L) < 4)
-                    CK(cudaFuncSetAttribute(k_rans_dec_v1_fast<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    CK(cudaFuncSetAttribute(k_rans_dec_v1p<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem));
-                if constexpr (sizeof(L) < 4) CK(launch_pdl(k_rans_dec_v1_fast<S, L>, B, 32, smem, s, dp));
+                if constexpr (sizeof(L) < 4) CK(launch_pdl(k_rans_dec_v1p<S, L>, B, V1_THREADS, smem, s, dp));
             } else {
                 size_t smem = RING + tab + lut;
                 CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -200,9 +200,9 @@ __device__ void build_lut_slice(const DecParams& p, const scz_info& in, uint32_t
     uint8_t* base = p.lut + (uint64_t)b * p.lut_stride;
     uint32_t* step = reinterpret_cast<uint32_t*>(base);
     L* sym = reinterpret_cast<L*>(base + lut_sym_off(n));
-    // v1 (k_rans_dec_v1_fast): f and slot - cum as separate u16 arrays, so
-    // the serial decoder's state update is one IMAD on two 16-bit loads
-    const bool split = in.version == 1;
+    // one layout for v1 and v2 (k_rans_dec_v1p reads f and slot - cum as the
+    // two 16-bit halves of the entry)
+    const bool split = false;
     uint16_t* f16 = reinterpret_cast<uint16_t*>(base);
     uint16_t* b16 = f16 + ((size_t)1 << n);
     const uint32_t slot0 = s0 + 8 * threadIdx.x;
