@@ -784,6 +784,19 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
     res["v1_reference_format"] = dict(value=4.0 * T * B / (v1_ms * 1e-3) / 1e9, unit=UNIT,
                                       ms_per_step=v1_ms, batch=B,
                                       note="bit-exact reference wire format; serial stream per tensor")
+    # v1 end to end (like-for-like with the reference arm's format): the same
+    # pipelined host-buffer round trip as `e2e`, format 1
+    if not args.no_e2e:
+        import copy
+        a1 = copy.copy(args)
+        a1.format, a1.steps, a1.warmup = 1, 5, 0
+        host = x_dev.cpu().pin_memory()
+        e_ms, io, h_out, st1 = run_e2e(a1, torch, _native, lib, x_dev.device.index or 0, host, T, B, wl)
+        assert all(v == 0 for v in st1)
+        res["v1_reference_format"]["e2e"] = dict(
+            value=4.0 * T * B / (e_ms * 1e-3) / 1e9, unit=UNIT, ms_per_step=e_ms, steps=a1.steps,
+            h2d_bytes_per_step=io["h2d"], d2h_bytes_per_step=io["d2h"],
+            path="scz_compress_batch + scz_decompress_batch (format 1), pinned host buffers")
     if not args.no_configs:
         peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
         peak = float(json.load(open(peaks_path))["hbm_gbs"]) if os.path.exists(peaks_path) else 6650.0

@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     tmp = OUT + ".tmp"
-    cmd = [NVCC, *FLAGS, "-o", tmp, os.path.join(CSRC, "capi.cu")]
+    extra = os.environ.get("SCZ_NVCC_EXTRA", "").split()  # experiments: -D overrides
+    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, os.path.join(CSRC, "capi.cu")]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)

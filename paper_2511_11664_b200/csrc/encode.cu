@@ -83,7 +83,16 @@ __device__ void device_compute_params(float fmin, float fmax, int q_bits, double
     *z = zz;
 }
 
-__global__ void __launch_bounds__(TILE_THREADS, 5) k_stats(StatsParams p) {
+#ifndef SCZ_STATS_MINB
+#define SCZ_STATS_MINB 5
+#endif
+#ifndef SCZ_QUANT_MINB
+#define SCZ_QUANT_MINB 5
+#endif
+#ifndef SCZ_MAT_MINB
+#define SCZ_MAT_MINB 7
+#endif
+__global__ void __launch_bounds__(TILE_THREADS, SCZ_STATS_MINB) k_stats(StatsParams p) {
     pdl_wait();
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -303,7 +312,7 @@ __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, i
 }
 
 template <bool SYM_OUT>  // SYM_OUT: also write every element's symbol (stage API)
-__global__ void __launch_bounds__(TILE_THREADS, 5) k_quantize(QuantParams p) {
+__global__ void __launch_bounds__(TILE_THREADS, SCZ_QUANT_MINB) k_quantize(QuantParams p) {
     pdl_wait();
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -716,7 +725,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_materialize(MatParams p) {
 }
 
 // The pipeline's launch: u8 and u16 classes in one grid (see k_rans_enc_v2_u8u16).
-__global__ void __launch_bounds__(TILE_THREADS, 7) k_materialize_u8u16(MatParams p8, MatParams p16) {
+__global__ void __launch_bounds__(TILE_THREADS, SCZ_MAT_MINB) k_materialize_u8u16(MatParams p8, MatParams p16) {
     pdl_wait();
     __shared__ __align__(16) uint8_t s_buf[TILE * 2 + 64];
     const uint32_t w = p8.state[blockIdx.y].sym_bytes;

@@ -519,7 +519,10 @@ __global__ void __launch_bounds__(ENC2_WPB * 32) k_rans_enc_v2(EncParams p, Src 
 // class is known only after k_select), so no launch is spent on an empty
 // class.  u32 tensors (K > 65535) go to k_rans_enc_v2<SplitSrc<uint32_t>>.
 template <bool SMEM>
-__global__ void __launch_bounds__(ENC2_WPB * 32, 8)
+#ifndef SCZ_ENC2_MINB
+#define SCZ_ENC2_MINB 8
+#endif
+__global__ void __launch_bounds__(ENC2_WPB * 32, SCZ_ENC2_MINB)
     k_rans_enc_v2_u8u16(EncParams p, Contig8Src s8, SplitSrc<uint16_t> s16, PackParams pk) {
     pdl_wait();
     const TensorState& st = p.state[blockIdx.x];

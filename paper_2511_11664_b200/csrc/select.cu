@@ -151,8 +151,10 @@ __device__ unsigned long long block_sum64(unsigned long long v, BlockScratch<NT>
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) s.red64[warp] = v;
     __syncthreads();
-    unsigned long long t = 0;
-    for (int w = 0; w < NT / 32; ++w) t += s.red64[w];
+    // every warp folds the per-warp sums with shuffles (one load per lane,
+    // not NT / 32 dependent loads per thread)
+    unsigned long long t = lane < NT / 32 ? s.red64[lane] : 0ull;
+    t = warp_sum(t);
     __syncthreads();
     return t;
 }
@@ -164,8 +166,9 @@ __device__ uint32_t block_max32(uint32_t v, BlockScratch<NT>& s) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) s.red32[warp] = v;
     __syncthreads();
-    uint32_t t = 0;
-    for (int w = 0; w < NT / 32; ++w) t = max(t, s.red32[w]);
+    uint32_t t = lane < NT / 32 ? s.red32[lane] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = max(t, __shfl_xor_sync(0xffffffffu, t, o));
     __syncthreads();
     return t;
 }
@@ -233,8 +236,14 @@ __device__ __noinline__ int block_normalize(const uint32_t* counts, uint32_t A, 
         total += counts[i];
         npresent += counts[i] > 0;
     }
-    total = block_sum64(total, s);
-    npresent = block_sum64(npresent, s);
+    if (A < (1u << 12)) {  // one reduction: counts < 2^32, so total < 2^44 and npresent < 2^12
+        const unsigned long long both = block_sum64((total << 20) | npresent, s);
+        total = both >> 20;
+        npresent = both & ((1ull << 20) - 1);
+    } else {
+        total = block_sum64(total, s);
+        npresent = block_sum64(npresent, s);
+    }
     if (total == 0) return SCZ_NORMALIZE_ERROR;
     if (precision < 1 || precision > 16) return SCZ_INVALID_INPUT;
     const unsigned long long target = 1ull << precision;
