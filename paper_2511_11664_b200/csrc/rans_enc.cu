@@ -293,6 +293,9 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
     uint32_t base = top;   // window bytes [base, rtop) are pending
     uint32_t rtop = top;   // [rtop, top) already went to the slot
     uint32_t flushed = 0;  // bytes already in the slot (multiple of 16)
+    // the window is flushed (at a 16-step boundary) only once less than one
+    // interval's worst case (16 steps x 32 lanes x 2 bytes) is left below base
+    const uint32_t low = ob_s + 1024;
     uint32_t x = E.x;
     // window byte at address a goes to slot_end - flushed - (rtop - a): the
     // complete 16-byte chunks below rtop leave; when less than one flush
@@ -355,13 +358,13 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
             const bool act = (uint32_t)s * 32 + lane < len;
             const EncTab t = lds_tab16(tab_s + 16 * (act ? lds_u8(sym_at(s)) : 0u));
             enc_step_lin<true>(x, base, t, gtm, act);
-            if ((s & 15) == 0) flush();
+            if ((s & 15) == 0 && base < low) flush();
             --s;
         }
         for (; s >= 0 && (s & 3) != 3; --s) {  // align the rest to groups of four steps
             ensure(s);
             enc_step_lin<false>(x, base, lds_tab16(tab_s + 16 * lds_u8(sym_at(s))), gtm, true);
-            if ((s & 15) == 0) flush();
+            if ((s & 15) == 0 && base < low) flush();
         }
         // groups of four steps (never across a chunk or a flush boundary).
         // Entry k of the next group loads right after step k of this one
@@ -395,13 +398,14 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
                 t2 = lds_tab16(tab_s + 16 * y2);
                 enc_step_lin<false>(x, base, t3, gtm, true);
                 t3 = lds_tab16(tab_s + 16 * y3);
-                if (((s - 3) & 15) == 0) flush();
+                if (((s - 3) & 15) == 0 && base < low) flush();
                 s = sn;
                 if (!more) break;
             }
         }
     }
     cp_async_wait<0>();
+    flush();  // every complete 16-byte chunk
     // the last (< 16) bytes, then the emitted count
     const uint32_t pend = rtop - base;
     if (lane < pend) slot_end[-(int32_t)(flushed + pend) + (int32_t)lane] = (uint8_t)lds_u8(base + lane);
