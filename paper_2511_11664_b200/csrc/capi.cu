@@ -371,8 +371,25 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool no_pdl = getenv("SCZ_NO_PDL") != nullptr;  // diagnostics
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = no_pdl ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+// Plain stream-ordered launch for the v1 serial coders: under PDL their CTAs
+// become resident while the predecessor still holds warp slots, and two
+// chain threads can then land on one SM sub-partition (measured: the v1
+// encoder at B = 296 takes 33 ms with PDL, 22 ms without; their launch
+// latency is nothing against a 20-30 ms kernel).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_plain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                         Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.numAttrs = 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -795,8 +812,15 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     // Lazy search: the first pass prices the NA_FIRST candidates with the
     // smallest K (the scan usually stops among them); the rest are priced
     // only for tensors whose scan did not stop (sel_pending).
+    // Small batches (latency mode) price every candidate in one pass: the
+    // GPU is mostly idle there, and the second pass would add two dependent
+    // launches to the chain.
     constexpr uint32_t NA_FIRST = 5;
-    const bool split = pl.searching && !cand_out && pl.acap <= SEL_WARP_ACAP && ncand > NA_FIRST && !getenv("SCZ_NO_LAZY");
+#ifndef SCZ_LAZY_MIN_B
+#define SCZ_LAZY_MIN_B 1
+#endif
+    const bool split = pl.searching && !cand_out && pl.acap <= SEL_WARP_ACAP && ncand > NA_FIRST &&
+                       B >= SCZ_LAZY_MIN_B && !getenv("SCZ_NO_LAZY");
     const uint32_t n_first = split ? NA_FIRST : ncand;
     // row-count histograms (+ column folds) of candidates [c0, c1)
     auto rowhist_pass = [&](uint32_t c0, uint32_t c1, bool pending_only) -> int {
@@ -975,7 +999,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
                 LAUNCHED(wname<S>("k_rans_enc_v2"));
             } else {
                 // role-split serial coder (rans_v1.cu); 32-bit stream offsets
-                if (pl.L_max < (1ull << 30)) CK(launch_pdl(k_rans_enc_v1p<Src>, B, V1_THREADS, 0, s, ep, src));
+                if (pl.L_max < (1ull << 30)) CK(launch_plain(k_rans_enc_v1p<Src>, B, V1_THREADS, 0, s, ep, src));
                 else CK(launch_pdl(k_rans_enc_v1<Src>, B, 32, 0, s, ep, src));
                 LAUNCHED(wname<S>("k_rans_enc_v1"));
             }
@@ -1247,7 +1271,7 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
                 if constexpr (sizeof(L) < 4)
                     CK(cudaFuncSetAttribute(k_rans_dec_v1p<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem));
-                if constexpr (sizeof(L) < 4) CK(launch_pdl(k_rans_dec_v1p<S, L>, B, V1_THREADS, smem, s, dp));
+                if constexpr (sizeof(L) < 4) CK(launch_plain(k_rans_dec_v1p<S, L>, B, V1_THREADS, smem, s, dp));
             } else {
                 size_t smem = RING + tab + lut;
                 CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -34,10 +34,8 @@
 //     warp 2  emitter  slot -> symbol through the table's symbol column,
 //                      symbols into an output ring, TMA stores of halves.
 //
-// Roles hand chunks over through release/acquire counters in shared memory
-// (a consumer polls the producer's count; helpers back off with nanosleep,
-// the chain spins and only re-reads a count when its cached copy is
-// exhausted).  Byte-identical to rans.encode / rans.decode
+// Roles hand chunks over through mbarriers, one per queue slot and
+// direction (full / free), as TMA pipelines do.  Byte-identical to rans.encode / rans.decode
 // (tests/test_gpu_parity.py, tests/test_gpu_bench_path.py).
 #include "common.cuh"
 
@@ -66,25 +64,12 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
-// CTA-scope hand-over counters in shared memory
-__device__ __forceinline__ uint32_t ld_acquire_s(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_s(uint32_t a, uint32_t v) {
-    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
-}
-// chain thread: spin until the count at a reaches v (seen caches the last read)
-__device__ __forceinline__ void spin_ge(uint32_t a, uint32_t v, uint32_t& seen) {
-    while (seen < v) seen = ld_acquire_s(a);
-}
-// helper warps: poll with back-off (they run ahead of the chain)
-__device__ __forceinline__ void poll_ge(uint32_t a, uint32_t v, uint32_t& seen) {
-    while (seen < v) {
-        seen = ld_acquire_s(a);
-        if (seen < v) __nanosleep(100);
-    }
+// Role hand-over: one mbarrier per queue slot and direction ("full" /
+// "free"), phase parity = lap of the slot.  Producers arrive after their
+// writes (release), consumers try_wait.parity (acquire); an mbarrier phase
+// cannot run ahead of its consumer, so parities never alias.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Input ring owned by one warp (lane 0 issues, every lane waits): chunk c =
@@ -123,7 +108,10 @@ struct ChunkRing {
 // [bytes in decoder order] ends at the slot's end.
 template <class Src>
 __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src src) {
-    pdl_wait();
+    // launched without PDL (capi.cu launch_plain) and no early trigger: the
+    // next kernel launches when this one completes, so nothing parks on the
+    // SMs while the chains run
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const uint32_t b = blockIdx.x;
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) return;
@@ -132,14 +120,18 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src sr
     __shared__ __align__(8) uint2 s_cm[V1_NQ][V1_C];    // cmpl = 2^n - f, bound << 8 (saturated)
     __shared__ uint32_t s_xs[V1_NQ][V1_C];              // state before the symbol
     __shared__ __align__(128) uint8_t s_out[V1_OUT];
-    __shared__ uint32_t s_cnt[4];                       // fed, chained, freed, final state
+    __shared__ uint32_t s_final;                        // the final state
+    __shared__ __align__(8) uint64_t b_fed[V1_NQ], b_chn[V1_NQ], b_free[V1_NQ];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t L = (uint32_t)st.stream_len;
     const uint32_t nch = (L + V1_C - 1) / V1_C;
     const int n = p.precision;
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < V1_NQ) {
+        mbar_init(&b_fed[threadIdx.x], 32);  // the feeder's lanes
+        mbar_init(&b_chn[threadIdx.x], 1);   // the chain thread
+        mbar_init(&b_free[threadIdx.x], 32); // the emitter's lanes
+    }
     __syncthreads();
-    const uint32_t c_fed = smem_u32(&s_cnt[0]), c_chn = smem_u32(&s_cnt[1]), c_free = smem_u32(&s_cnt[2]);
     uint8_t* slot_end = p.slots + ((uint64_t)b * p.slots_per_tensor + 1) * p.slot_cap;  // 16-aligned
     uint32_t E = 0;  // emitter: bytes emitted so far
     if (warp == 1) {
@@ -147,10 +139,9 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src sr
         const EncTab* gt = p.enctab + (uint64_t)b * p.acap;
         const uint64_t nnz = st.nnz;
         const uint32_t one = 1u << n;
-        uint32_t seen = 0;
         for (uint32_t g0 = 0; g0 < nch; g0 += V1_G) {
             const uint32_t g1 = min(g0 + V1_G, nch);
-            if (g1 > V1_NQ) poll_ge(c_free, g1 - V1_NQ, seen);
+            for (uint32_t c = max(g0, V1_NQ); c < g1; ++c) mbar_wait(&b_free[c % V1_NQ], ((c / V1_NQ) - 1) & 1u);
             uint32_t sym[2 * V1_G];
 #pragma unroll
             for (uint32_t j = 0; j < 2 * V1_G; ++j) {
@@ -182,16 +173,15 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src sr
                     s_cm[c % V1_NQ][i] = cm;
                 }
             }
-            __syncwarp();
-            if (lane == 0) st_release_s(c_fed, g1);
+            for (uint32_t c = g0; c < g1; ++c) mbar_arrive(&b_fed[c % V1_NQ]);
         }
     } else if (warp == 0) {
         // ---- chain: the state recurrence (rans.py:139-144), one thread
         if (lane == 0) {
-            uint32_t x = STATE_LOW, seen_fed = 0;
+            uint32_t x = STATE_LOW;
             for (uint32_t c = 0; c < nch; ++c) {
-                spin_ge(c_fed, c + 1, seen_fed);
                 const uint32_t s = c % V1_NQ;
+                mbar_wait(&b_fed[s], (c / V1_NQ) & 1u);
                 // entries are loaded V1_D steps ahead of their use (explicit
                 // shared addresses, volatile: the issue order is as written)
                 const uint32_t ent_s = smem_u32(s_ent[s]), cm_s = smem_u32(s_cm[s]), xs_s = smem_u32(s_xs[s]);
@@ -251,18 +241,17 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src sr
                 } else {
                     for (uint32_t k = 0; k < m; ++k) code(lds128(ent_s + 16 * k), lds64(cm_s + 8 * k), k);
                 }
-                st_release_s(c_chn, c + 1);
+                mbar_arrive(&b_chn[s]);
             }
-            s_cnt[3] = x;
+            s_final = x;
         }
     } else {
         // ---- emitter: renormalisation bytes of 32 symbols per ballot scan
         const uint32_t ltm = lanemask_lt();
         const uint32_t out_s = smem_u32(s_out);
-        uint32_t seen = 0;
         for (uint32_t c = 0; c < nch; ++c) {
-            poll_ge(c_chn, c + 1, seen);
             const uint32_t s = c % V1_NQ;
+            mbar_wait(&b_chn[s], (c / V1_NQ) & 1u);
 #pragma unroll
             for (uint32_t h = 0; h < 2; ++h) {
                 const uint32_t k = h * 32 + lane;
@@ -293,13 +282,12 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src sr
                 }
                 E = En;
             }
-            __syncwarp();
-            if (lane == 0) st_release_s(c_free, c + 1);
+            mbar_arrive(&b_free[s]);
         }
     }
     __syncthreads();
     if (warp == 2) {
-        const uint32_t x = s_cnt[3];
+        const uint32_t x = s_final;
         // bytes of the last, partial half, then the 4 little-endian state bytes
         const uint32_t j0 = E & ~(V1_HALF - 1);
         for (uint32_t j = j0 + lane; j < E; j += 32) slot_end[-(int64_t)j - 1] = s_out[~j & (V1_OUT - 1)];
@@ -338,13 +326,14 @@ inline size_t dec_v1p_smem(int n, size_t lwidth) {
 
 template <typename S, typename L>
 __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
-    pdl_wait();
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // see k_rans_enc_v1p
     const uint32_t b = blockIdx.x;
     const scz_info& in = p.info[b];
     if (p.status[b] != SCZ_OK || in.version != 1 || in.sym_bytes != sizeof(S)) return;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[V1D_NR + 1];
-    __shared__ uint32_t s_cnt[8];  // pfull, pfree, schained, sfree, final x, final pos
+    __shared__ uint32_t s_fin[2];  // final state, final position
+    __shared__ __align__(8) uint64_t b_pfull[V1D_NP], b_pfree[V1D_NP], b_schn[V1_NQ], b_sfree[V1_NQ];
     const int n = in.precision;
     const uint32_t nslots = 1u << n;
     const uint32_t lut_bytes = (uint32_t)dec_v1p_lut_bytes(n, sizeof(L));
@@ -358,15 +347,20 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
     const uint32_t plen = (uint32_t)in.payload_len;  // >= 4 (host check)
     const uint32_t nch = (Ls + V1_C - 1) / V1_C;
     const uint32_t npch = (plen + V1D_PCH - 1) / V1D_PCH;
-    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < V1D_NP) {
+        mbar_init(&b_pfull[threadIdx.x], 32);  // the feeder's lanes
+        mbar_init(&b_pfree[threadIdx.x], 1);   // the chain thread
+    }
+    if (threadIdx.x < V1_NQ) {
+        mbar_init(&b_schn[threadIdx.x], 1);    // the chain thread
+        mbar_init(&b_sfree[threadIdx.x], 32);  // the emitter's lanes
+    }
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i <= V1D_NR; ++i) mbar_init(&bars[i], 1);
         mbar_expect_tx(&bars[V1D_NR], lut_bytes);
         bulk_g2s(lut, p.lut + (uint64_t)b * p.lut_stride, lut_bytes, &bars[V1D_NR]);
     }
     __syncthreads();
-    const uint32_t c_pfull = smem_u32(&s_cnt[0]), c_pfree = smem_u32(&s_cnt[1]);
-    const uint32_t c_chn = smem_u32(&s_cnt[2]), c_sfree = smem_u32(&s_cnt[3]);
     const uint32_t HS = V1_HALF / sizeof(S);  // symbols per output half
     uint8_t* gout = reinterpret_cast<uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;  // 16-aligned
     if (warp == 1) {
@@ -381,10 +375,9 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
             rg.issue(1);
         }
         int rw = 0;  // next raw chunk to wait for
-        uint32_t seen = 0;
         const uint32_t raw_s = smem_u32(raw);
         for (uint32_t g = 0; g < npch; ++g) {
-            if (g >= V1D_NP) poll_ge(c_pfree, g - V1D_NP + 1, seen);
+            if (g >= V1D_NP) mbar_wait(&b_pfree[g % V1D_NP], ((g / V1D_NP) - 1) & 1u);
             // raw bytes [off0 + 256 g, off0 + 256 g + 259) (clamped to the payload)
             const int hi = (int)(min(off0 + g * V1D_PCH + V1D_PCH + 2, rend - 1) / V1D_RCH);
             while (rw <= hi) {
@@ -407,8 +400,7 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
                 P[pi + u] = w;
                 if (pi + u < V1D_PMIR) P[V1D_PRING + pi + u] = w;
             }
-            __syncwarp();
-            if (lane == 0) st_release_s(c_pfull, g + 1);
+            mbar_arrive(&b_pfull[g % V1D_NP]);
         }
     } else if (warp == 0) {
         // ---- chain: the state recurrence (rans.py:199-210), one thread
@@ -416,8 +408,8 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
             const uint32_t mask = nslots - 1;
             const uint32_t lut_s = smem_u32(lut), P_s = smem_u32(P);
             const uint32_t slots_s = smem_u32(slots);
-            uint32_t seen_full = 0, seen_free = 0, released = 0;
-            spin_ge(c_pfull, 1, seen_full);
+            uint32_t waited = 1, released = 0;  // P chunks waited for / handed back
+            mbar_wait(&b_pfull[0], 0);
             const uint32_t x0 = lds_u32(P_s);
             const uint32_t x = __byte_perm(x0, 0u, 0x0123u);  // 4-byte little-endian initial state (rans.py:193)
             uint32_t ea = lut_s + 4 * (x & mask), xs = x >> n;  // entry address of x's slot, x >> n
@@ -425,14 +417,11 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
             mbar_wait(&bars[V1D_NR], 0);  // the table
             for (uint32_t c = 0; c < nch; ++c) {
                 const uint32_t s = c % V1_NQ;
-                if (c >= V1_NQ) spin_ge(c_sfree, c - V1_NQ + 1, seen_free);
+                if (c >= V1_NQ) mbar_wait(&b_sfree[s], ((c / V1_NQ) - 1) & 1u);
                 // this chunk refills at most 2 V1_C bytes: windows up to pos + 2 V1_C
                 const uint32_t need = min((pos + 2 * V1_C) / V1D_PCH, npch - 1) + 1;
-                spin_ge(c_pfull, need, seen_full);
-                if (pos / V1D_PCH > released) {
-                    released = pos / V1D_PCH;
-                    st_release_s(c_pfree, released);
-                }
+                for (; waited < need; ++waited) mbar_wait(&b_pfull[waited % V1D_NP], (waited / V1D_NP) & 1u);
+                for (; released < pos / V1D_PCH; ++released) mbar_arrive(&b_pfree[released % V1D_NP]);
                 const uint32_t pa0 = P_s + 4 * (pos % V1D_PRING);
                 uint32_t pa = pa0;
                 uint32_t v = lds_u32(pa);
@@ -469,28 +458,26 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
                     for (uint32_t k = 0; k < m; ++k) step(k);
                 }
                 pos += (pa - pa0) >> 2;
-                st_release_s(c_chn, c + 1);
+                mbar_arrive(&b_schn[s]);
             }
-            s_cnt[4] = (xs << n) | ((ea - lut_s) >> 2);  // the final state
-            s_cnt[5] = pos;
+            s_fin[0] = (xs << n) | ((ea - lut_s) >> 2);  // the final state
+            s_fin[1] = pos;
         }
     } else {
         // ---- emitter: slot -> symbol, output ring, TMA stores of halves
         mbar_wait(&bars[V1D_NR], 0);
         const L* lsym = reinterpret_cast<const L*>(lut + lut_sym_off(n));
         S* ob = reinterpret_cast<S*>(oring);
-        uint32_t seen = 0;
         for (uint32_t c = 0; c < nch; ++c) {
-            poll_ge(c_chn, c + 1, seen);
             const uint32_t s = c % V1_NQ;
+            mbar_wait(&b_schn[s], (c / V1_NQ) & 1u);
 #pragma unroll
             for (uint32_t h = 0; h < 2; ++h) {
                 const uint32_t k = h * 32 + lane;
                 const uint32_t i = c * V1_C + k;
                 if (i < Ls) ob[i % (2 * HS)] = (S)lsym[slots[s * V1_C + k]];
             }
-            __syncwarp();
-            if (lane == 0) st_release_s(c_sfree, c + 1);
+            mbar_arrive(&b_sfree[s]);
             const uint32_t iend = (c + 1) * V1_C;
             if (iend % HS == 0 && iend <= Ls) {  // a half is complete: TMA store it
                 fence_proxy_async_smem();
@@ -515,7 +502,7 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
         for (uint32_t i = lane; i < rem; i += 32) dst[i] = srcp[i];
         // rans.py:211-212: the final state is L and every byte was consumed
         if (lane == 0) {
-            if (s_cnt[4] != STATE_LOW || s_cnt[5] != plen) p.status[b] = SCZ_CORRUPT_STREAM;
+            if (s_fin[0] != STATE_LOW || s_fin[1] != plen) p.status[b] = SCZ_CORRUPT_STREAM;
             bulk_wait_all();
         }
     }

@@ -43,6 +43,20 @@ for _ in range(3):
 c.record(st)
 c.synchronize()
 ms = a.elapsed_time(c) / 3
+# one step split at its calls: device time of the encode, host gap, decode
+e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+e[0].record(st)
+ctx.check(lib.scz_encode_batch(ctx.h, ctypes.c_void_p(x.data_ptr()), T, B, wl["q"], -1, 14, 1, 32, 8192,
+                               ctypes.byref(batch)))
+e[1].record(st)
+ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), info))
+e[2].record(st)
+ctx.check(lib.scz_decode_batch_async(ctx.h, info, B, ctypes.c_void_p(batch.d_freqs),
+                                     ctypes.c_void_p(batch.d_block_bytes), ctypes.c_void_p(batch.d_payload),
+                                     ctypes.c_void_p(out.data_ptr())))
+e[3].record(st)
+e[3].synchronize()
+split_ms = dict(encode=e[0].elapsed_time(e[1]), sync_gap=e[1].elapsed_time(e[2]), decode=e[2].elapsed_time(e[3]))
 ctx.set_timing(True)
 ctx.read_timing()
 step()
@@ -50,7 +64,7 @@ torch.cuda.synchronize()
 kt = ctx.read_timing()
 ctx.set_timing(False)
 L = max(2 * info[i].nnz + info[i].n_rows for i in range(B))
-res = dict(workload=wl["name"], batch=B, ms_per_step=ms, gbs=4.0 * T * B / (ms * 1e-3) / 1e9, stream_len=L,
+res = dict(workload=wl["name"], batch=B, ms_per_step=ms, split_ms=split_ms, gbs=4.0 * T * B / (ms * 1e-3) / 1e9, stream_len=L,
            kernel_ms={k: round(v[0] / v[1], 3) for k, v in kt.items()},
            ns_per_symbol={k: round(v[0] / v[1] * 1e6 / L, 2) for k, v in kt.items() if "_v1" in k})
 st_ = (ctypes.c_int32 * B)()
