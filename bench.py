@@ -803,6 +803,13 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
         t0 = time.perf_counter()
         res["configs"] = config_records(args, torch, _native, x_dev.device.index or 0, peak)
         res["configs"]["wall_s"] = round(time.perf_counter() - t0, 1)
+        c2 = res["configs"].get("C2-vgg16-batch256", {}).get("v2")
+        if c2:  # SURVEY 8d's encode-side target, surfaced from the C2 record
+            res["encode_decode_roofline"] = dict(
+                encode=c2["encode_roofline"], decode=c2["decode_roofline"], encode_ms=c2["encode_ms"],
+                decode_ms=c2["decode_ms"], peak_gbs=peak,
+                note="encode-only / decode-only device time of the 256-tensor VGG16 batch (CUDA events, one "
+                     "context, not pipelined); algorithmic bytes 4T + S per tensor")
     return res
 
 
