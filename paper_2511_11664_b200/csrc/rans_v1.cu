@@ -43,9 +43,12 @@ namespace scz {
 
 constexpr uint32_t V1_OUT = 8192;                // output ring (two 4 KB halves)
 constexpr uint32_t V1_HALF = V1_OUT / 2;
-constexpr uint32_t V1_C = 64;                    // symbols per chunk
-constexpr uint32_t V1_NQ = 16;                   // chunks in the queue
-constexpr uint32_t V1_G = 8;                     // chunks per encoder feeder group
+#ifndef SCZ_V1_C
+#define SCZ_V1_C 64
+#endif
+constexpr uint32_t V1_C = SCZ_V1_C;              // symbols per chunk
+constexpr uint32_t V1_NQ = 1024 / V1_C;          // chunks in the queue
+constexpr uint32_t V1_G = 512 / V1_C;            // chunks per encoder feeder group (16 loads per lane)
 constexpr int V1_THREADS = 96;                   // chain, feeder, emitter warps
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -142,14 +145,15 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src sr
         for (uint32_t g0 = 0; g0 < nch; g0 += V1_G) {
             const uint32_t g1 = min(g0 + V1_G, nch);
             for (uint32_t c = max(g0, V1_NQ); c < g1; ++c) mbar_wait(&b_free[c % V1_NQ], ((c / V1_NQ) - 1) & 1u);
-            uint32_t sym[2 * V1_G];
+            constexpr uint32_t NL = V1_G * V1_C / 32;  // symbols per lane per group
+            uint32_t sym[NL];
 #pragma unroll
-            for (uint32_t j = 0; j < 2 * V1_G; ++j) {
+            for (uint32_t j = 0; j < NL; ++j) {
                 const uint32_t k = g0 * V1_C + j * 32 + lane;
                 sym[j] = k < L ? src.at(b, L - 1 - k, nnz) : 0u;
             }
 #pragma unroll
-            for (uint32_t j = 0; j < 2 * V1_G; ++j) {
+            for (uint32_t j = 0; j < NL; ++j) {
                 const uint32_t k = g0 * V1_C + j * 32 + lane;
                 if (k < L) {
                     const uint4 e = __ldg(reinterpret_cast<const uint4*>(gt) + sym[j]);  // freq, cum, rcp, shift
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_enc_v1p(EncParams p, Src sr
             const uint32_t s = c % V1_NQ;
             mbar_wait(&b_chn[s], (c / V1_NQ) & 1u);
 #pragma unroll
-            for (uint32_t h = 0; h < 2; ++h) {
+            for (uint32_t h = 0; h < V1_C / 32; ++h) {
                 const uint32_t k = h * 32 + lane;
                 const bool valid = c * V1_C + k < L;
                 const uint32_t x = s_xs[s][k], bnd = s_ent[s][k].x;
@@ -315,7 +319,7 @@ template __global__ void k_rans_enc_v1p<SplitSrc<uint32_t>>(EncParams, SplitSrc<
 constexpr uint32_t V1D_PCH = 256;                 // positions per P chunk
 constexpr uint32_t V1D_NP = 8;                    // P chunks in the ring
 constexpr uint32_t V1D_PRING = V1D_PCH * V1D_NP;  // positions in the ring
-constexpr uint32_t V1D_PMIR = 160;                // > 2 V1_C: one chunk's refills
+constexpr uint32_t V1D_PMIR = 2 * V1_C + 32;      // > 2 V1_C: one chunk's refills
 constexpr uint32_t V1D_RCH = 2048;                // raw TMA chunk (bytes)
 constexpr uint32_t V1D_NR = 4;
 
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(V1_THREADS) k_rans_dec_v1p(DecParams p) {
             const uint32_t s = c % V1_NQ;
             mbar_wait(&b_schn[s], (c / V1_NQ) & 1u);
 #pragma unroll
-            for (uint32_t h = 0; h < 2; ++h) {
+            for (uint32_t h = 0; h < V1_C / 32; ++h) {
                 const uint32_t k = h * 32 + lane;
                 const uint32_t i = c * V1_C + k;
                 if (i < Ls) ob[i % (2 * HS)] = (S)lsym[slots[s * V1_C + k]];
