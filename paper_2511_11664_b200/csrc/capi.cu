@@ -865,7 +865,9 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         rp.period = (uint32_t)pl.period;
         rp.n_fold = c1 - c0;  // one column-fold CTA per candidate, ahead of the row chunks
         size_t smem = std::max<size_t>(RH_PRIV_SMEM, (size_t)std::min<uint32_t>(maxbins, 4096) * 4);
-        CK(launch_pdl(k_rowhist2, dim3(chunks + (c1 - c0), B), RH_THREADS, smem, s, rp));
+        rp.n_tensors = B;
+        const uint32_t gy = pending_only ? std::min<uint32_t>(B, 32) : B;
+        CK(launch_pdl(k_rowhist2, dim3(chunks + (c1 - c0), gy), RH_THREADS, smem, s, rp));
         LAUNCHED("k_rowhist");
         return SCZ_OK;
     };

@@ -41,6 +41,7 @@ struct RowHist2Params {
                                        // grid: they are the longest CTAs and start right away)
     const TensorState* state;          // pending_only: skip tensors whose search already stopped
     int pending_only;
+    uint32_t n_tensors;                // pending_only: tensor b = blockIdx.y, + gridDim.y, ...
 };
 
 __device__ void fold_columns(const RowHist2Params& p, uint32_t b, uint32_t c) {
@@ -123,10 +124,7 @@ __device__ void rowhist_swar(const uint32_t* bm, uint32_t w0, uint32_t w1, uint3
     if (threadIdx.x >= 1 && threadIdx.x <= K && s_c[threadIdx.x]) atomicAdd(gh + threadIdx.x, s_c[threadIdx.x]);
 }
 
-__global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__ RowHist2Params p) {
-    pdl_wait();
-    const uint32_t b = blockIdx.y;
-    if (p.pending_only && !p.state[b].sel_pending) return;
+__device__ __forceinline__ void rowhist2_tensor(const RowHist2Params& p, uint32_t b) {
     if (blockIdx.x < p.n_fold) {
         fold_columns(p, b, blockIdx.x);
         return;
@@ -224,6 +222,22 @@ __global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__
     if (use_smem)
         for (uint32_t i = 1 + threadIdx.x; i <= K; i += RH_THREADS)
             if (s_big[i]) atomicAdd(gh + i, s_big[i]);
+}
+
+// First pass: one tensor per blockIdx.y.  Lazy second pass (pending tensors
+// only, usually none): a short grid striding over the batch, so a batch
+// whose scans all stopped costs a wave of CTAs that exit, not B x chunks.
+__global__ void __launch_bounds__(RH_THREADS) k_rowhist2(const __grid_constant__ RowHist2Params p) {
+    pdl_wait();
+    if (!p.pending_only) {
+        rowhist2_tensor(p, blockIdx.y);
+        return;
+    }
+    for (uint32_t b = blockIdx.y; b < p.n_tensors; b += gridDim.y) {
+        if (!p.state[b].sel_pending) continue;  // uniform per CTA
+        rowhist2_tensor(p, b);
+        __syncthreads();  // shared scratch reused by the next tensor
+    }
 }
 
 }  // namespace scz
