@@ -311,13 +311,15 @@ __device__ __forceinline__ uint32_t quant_fast(float x, float r32, float zf32, i
     return quant_exact(x, scale, zf, (double)qmax);
 }
 
-template <bool SYM_OUT>  // SYM_OUT: also write every element's symbol (stage API)
-__global__ void __launch_bounds__(TILE_THREADS, SCZ_QUANT_MINB) k_quantize(QuantParams p) {
-    pdl_wait();
-    const uint32_t tile = blockIdx.x, b = blockIdx.y;
+// One 8192-element tile of tensor b.  `staged`: the tile's fp32 data was
+// prefetched into s_x by cp.async (a persistent launch, measured slower and
+// not used: profiles/r2/attempts), else it is loaded here; on_loaded() runs
+// once the data is in registers.
+template <bool SYM_OUT, class OnLoaded>  // SYM_OUT: also write every element's symbol (stage API)
+__device__ __forceinline__ void quantize_tile(const QuantParams& p, uint32_t tile, uint32_t b,
+                                              const float4* s_x, bool staged, OnLoaded on_loaded) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const TensorState& st = p.state[b];
-    if (st.status != SCZ_OK) return;
     const float* xb = p.x + (uint64_t)b * p.total;
     const bool aligned = ((reinterpret_cast<uintptr_t>(xb) & 15) == 0);
     const uint64_t tile_base = (uint64_t)tile * TILE;
@@ -337,7 +339,12 @@ __global__ void __launch_bounds__(TILE_THREADS, SCZ_QUANT_MINB) k_quantize(Quant
     // all eight 16-byte loads in flight first (out-of-range lanes read 0:
     // their bitmap bits are 0 and the exact path re-checks the index)
     float4 vv[8];
-    if (aligned && tile_base + TILE <= p.total) {  // interior tile: no bounds checks
+    if (staged) {
+        cp_async_wait<0>();
+        __syncthreads();  // every thread's copies landed
+#pragma unroll
+        for (int it = 0; it < 8; ++it) vv[it] = s_x[warp * 256 + it * 32 + lane];
+    } else if (aligned && tile_base + TILE <= p.total) {  // interior tile: no bounds checks
         const float4* x4 = reinterpret_cast<const float4*>(xb + tile_base + warp * 1024 + lane * 4);
 #pragma unroll
         for (int it = 0; it < 8; ++it) vv[it] = __ldg(x4 + it * 32);
@@ -348,6 +355,7 @@ __global__ void __launch_bounds__(TILE_THREADS, SCZ_QUANT_MINB) k_quantize(Quant
             vv[it] = load4(xb, tile_base + warp * 1024 + it * 128 + lane * 4, p.total, aligned, &valid);
         }
     }
+    on_loaded();  // the tile's data is in registers: s_x may be refilled
     uint32_t myword = bm[threadIdx.x];
     s_wbits[threadIdx.x] = myword;
     uint32_t tot;
@@ -448,6 +456,14 @@ __global__ void __launch_bounds__(TILE_THREADS, SCZ_QUANT_MINB) k_quantize(Quant
                            (s_hist[4][i] + s_hist[5][i]) + (s_hist[6][i] + s_hist[7][i]);
         if (t) atomicAdd(gh + i, t);
     }
+}
+
+
+template <bool SYM_OUT>
+__global__ void __launch_bounds__(TILE_THREADS, SCZ_QUANT_MINB) k_quantize(QuantParams p) {
+    pdl_wait();
+    if (p.state[blockIdx.y].status != SCZ_OK) return;
+    quantize_tile<SYM_OUT>(p, blockIdx.x, blockIdx.y, nullptr, false, [] {});
 }
 
 // ------------------------------------------------------- search histograms
