@@ -413,6 +413,47 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
     E.x = x;
 }
 
+// The block's bytes -- 32 little-endian states, then the emitted bytes in
+// decoder order -- end at slot_end; publish the length, find the block's
+// payload offset by decoupled look-back, copy it there, drop the slot's L2
+// lines, and (last block) write the tensor's header.
+template <bool CHECK>
+__device__ __forceinline__ void enc_v2_block_tail(const EncParams& p, const PackParams& pk, TensorState& st,
+                                                  uint32_t b, uint32_t blk, uint32_t nblk, uint8_t* slot_end,
+                                                  EncLane E, uint32_t lane) {
+    // block bytes: 32 little-endian states, then the emitted bytes (decoder order)
+    const uint32_t blen = 4 * 32 + E.emitted;
+    uint8_t* start = slot_end - blen;
+    start[4 * lane + 0] = (uint8_t)E.x;
+    start[4 * lane + 1] = (uint8_t)(E.x >> 8);
+    start[4 * lane + 2] = (uint8_t)(E.x >> 16);
+    start[4 * lane + 3] = (uint8_t)(E.x >> 24);
+    if (CHECK) E.err = __reduce_or_sync(0xffffffffu, E.err);
+    if (lane == 0) {
+        p.block_len[(uint64_t)b * p.slots_per_tensor + blk] = blen;
+        if (CHECK && E.err) atomicOr(&st.errbits, E.err);
+    }
+    if (pk.payload) {
+        __threadfence();  // error bits before the length is published
+        __syncwarp();     // the slot bytes of every lane are visible to the warp
+        const uint32_t excl = chunk_prefix(pk.lb + (uint64_t)b * p.slots_per_tensor, blk, blen);
+        warp_copy_bytes(pk.payload + (uint64_t)b * pk.pcap + excl, start, blen, lane);
+        // the slot is dead now: drop its L2 lines without a write-back to HBM
+        // (slots are 128-byte aligned; the lines below `start` hold only this
+        // slot's unused head)
+        __syncwarp();
+        for (uintptr_t a = (reinterpret_cast<uintptr_t>(start) & ~(uintptr_t)127) + 128 * lane;
+             a < reinterpret_cast<uintptr_t>(slot_end); a += 128 * 32)
+            asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(a) : "memory");
+        if (blk == nblk - 1 && lane == 0) {
+            __threadfence();  // every block published: their error bits are visible
+            const uint32_t eb = *(volatile uint32_t*)&st.errbits;
+            write_info(pk.info[b], st, final_status(st, eb), 2, pk.q_bits, p.precision, pk.total, p.block_syms,
+                       nblk, (uint64_t)excl + blen, (uint64_t)b * pk.pcap, p.acap, p.slots_per_tensor, b);
+        }
+    }
+}
+
 template <class Src, bool SMEM, bool CHECK>
 __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, const PackParams& pk) {
     // grid (tensor, block group): a tensor's block groups are dispatched B CTAs
@@ -480,37 +521,7 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
         for (int k = 0; k < 8; ++k)
             if (k <= s0) enc_step<SMEM, CHECK>(E, q[k], true, s_tab, gt, A, n, sh_bound, gtm, slot_end);
     }
-    // block bytes: 32 little-endian states, then the emitted bytes (decoder order)
-    const uint32_t blen = 4 * 32 + E.emitted;
-    uint8_t* start = slot_end - blen;
-    start[4 * lane + 0] = (uint8_t)E.x;
-    start[4 * lane + 1] = (uint8_t)(E.x >> 8);
-    start[4 * lane + 2] = (uint8_t)(E.x >> 16);
-    start[4 * lane + 3] = (uint8_t)(E.x >> 24);
-    if (CHECK) E.err = __reduce_or_sync(0xffffffffu, E.err);
-    if (lane == 0) {
-        p.block_len[(uint64_t)b * p.slots_per_tensor + blk] = blen;
-        if (CHECK && E.err) atomicOr(&st.errbits, E.err);
-    }
-    if (pk.payload) {
-        __threadfence();  // error bits before the length is published
-        __syncwarp();     // the slot bytes of every lane are visible to the warp
-        const uint32_t excl = chunk_prefix(pk.lb + (uint64_t)b * p.slots_per_tensor, blk, blen);
-        warp_copy_bytes(pk.payload + (uint64_t)b * pk.pcap + excl, start, blen, lane);
-        // the slot is dead now: drop its L2 lines without a write-back to HBM
-        // (slots are 128-byte aligned; the lines below `start` hold only this
-        // slot's unused head)
-        __syncwarp();
-        for (uintptr_t a = (reinterpret_cast<uintptr_t>(start) & ~(uintptr_t)127) + 128 * lane;
-             a < reinterpret_cast<uintptr_t>(slot_end); a += 128 * 32)
-            asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(a) : "memory");
-        if (blk == nblk - 1 && lane == 0) {
-            __threadfence();  // every block published: their error bits are visible
-            const uint32_t eb = *(volatile uint32_t*)&st.errbits;
-            write_info(pk.info[b], st, final_status(st, eb), 2, pk.q_bits, p.precision, pk.total, p.block_syms,
-                       nblk, (uint64_t)excl + blen, (uint64_t)b * pk.pcap, p.acap, p.slots_per_tensor, b);
-        }
-    }
+    enc_v2_block_tail<CHECK>(p, pk, st, b, blk, nblk, slot_end, E, lane);
 }
 
 template <class Src, bool SMEM, bool CHECK>

@@ -71,9 +71,7 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // "free"), phase parity = lap of the slot.  Producers arrive after their
 // writes (release), consumers try_wait.parity (acquire); an mbarrier phase
 // cannot run ahead of its consumer, so parities never alias.
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
+// (mbar_arrive: common.cuh)
 
 // Input ring owned by one warp (lane 0 issues, every lane waits): chunk c =
 // bytes [c * CH, (c + 1) * CH) of a 16-byte aligned source region with `end`
