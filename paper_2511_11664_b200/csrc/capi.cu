@@ -14,6 +14,17 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no link dependency, near-free without a tool
+
+// One NVTX range per C-ABI call (tracing), named after the call, so
+// a profiler timeline (ncu --nvtx, Nsight Systems) groups every kernel under
+// the API call that launched it; kernel times come from CUDA events.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define SCZ_NVTX() NvtxRange scz_nvtx_range_(__func__)
+
 #include "encode.cu"
 #include "select.cu"
 #include "rans.cu"
@@ -1427,6 +1438,7 @@ uint64_t scz_launch_count(const scz_ctx* ctx) { return ctx ? ctx->launches : 0; 
 int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t batch, int q_bits,
                      int64_t n_rows, int precision, int format, uint32_t lanes, uint32_t block_syms,
                      scz_batch* out) {
+    SCZ_NVTX();
     if (!ctx || !out) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     ctx->mark();
@@ -1454,6 +1466,7 @@ int scz_encode_batch(scz_ctx* ctx, const float* d_x, uint64_t total, uint32_t ba
 int scz_encode_batch_ptrs(scz_ctx* ctx, const float* const* d_x, const uint64_t* numel, uint32_t batch,
                           int q_bits, int64_t n_rows, int precision, int format, uint32_t lanes,
                           uint32_t block_syms, scz_batch* out) {
+    SCZ_NVTX();
     if (!ctx || !out || !d_x || !numel) return SCZ_INVALID_INPUT;
     if (batch < 1) return ctx->fail(SCZ_INVALID_INPUT, "batch must be >= 1");
     cudaSetDevice(ctx->device);
@@ -1552,6 +1565,7 @@ int scz_encode_batch_ptrs(scz_ctx* ctx, const float* const* d_x, const uint64_t*
 }
 
 int scz_batch_sync(scz_ctx* ctx, scz_batch* b, scz_info* h_info) {
+    SCZ_NVTX();
     if (!ctx || !b || !h_info) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     CK(cudaMemcpyAsync(h_info, b->d_info, (size_t)b->batch * sizeof(scz_info), cudaMemcpyDeviceToHost,
@@ -1573,6 +1587,7 @@ int scz_batch_sync(scz_ctx* ctx, scz_batch* b, scz_info* h_info) {
 
 int scz_decode_batch_async(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, const uint32_t* d_freqs,
                            const uint32_t* d_block_bytes, const uint8_t* d_payload, float* d_out) {
+    SCZ_NVTX();
     if (!ctx || !h_info) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     ctx->mark();
@@ -1584,6 +1599,7 @@ int scz_decode_batch_async(scz_ctx* ctx, const scz_info* h_info, uint32_t batch,
 }
 
 int scz_decode_batch_device(scz_ctx* ctx, float* d_out) {
+    SCZ_NVTX();
     if (!ctx || !d_out) return SCZ_INVALID_INPUT;
     if (!ctx->have_last_plan) return ctx->fail(SCZ_INVALID_INPUT, "no scz_encode_batch on this context");
     cudaSetDevice(ctx->device);
@@ -1643,6 +1659,7 @@ int scz_decode_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, const
 int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64_t n_rows, int precision,
                  int format, uint32_t lanes, uint32_t block_syms, scz_info* info, const uint32_t** freqs,
                  const uint32_t** block_bytes, const uint8_t** payload) {
+    SCZ_NVTX();
     if (!ctx || !x || !info) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     ctx->mark();
@@ -1690,6 +1707,7 @@ int scz_compress(scz_ctx* ctx, const float* x, uint64_t total, int q_bits, int64
 
 int scz_decompress(scz_ctx* ctx, const scz_info* info_in, const uint32_t* freqs, const uint32_t* block_bytes,
                    const uint8_t* payload, float* out) {
+    SCZ_NVTX();
     if (!ctx || !info_in || !freqs || !out) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     ctx->mark();
@@ -1970,6 +1988,7 @@ int scz_normalize(scz_ctx* ctx, const int64_t* counts, uint64_t alphabet, int pr
 int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t* freqs, uint64_t alphabet,
                     int precision, uint32_t lanes, uint32_t block_syms, uint8_t* out, uint64_t* out_len,
                     uint32_t* block_bytes) {
+    SCZ_NVTX();
     ctx_forget_batch(ctx);
     if (!ctx || !freqs || !out || !out_len) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
@@ -2036,6 +2055,7 @@ int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t*
 int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint32_t* freqs, uint64_t alphabet,
                     int precision, uint32_t lanes, uint32_t block_syms, uint64_t n_blocks,
                     const uint32_t* block_bytes, uint64_t count, uint32_t* out) {
+    SCZ_NVTX();
     ctx_forget_batch(ctx);
     if (!ctx || !freqs || !out) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
@@ -2140,6 +2160,7 @@ int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint3
 int scz_search(scz_ctx* ctx, const float* x, uint64_t n, int q_bits, const uint64_t* rows, uint32_t n_rows_list,
                uint32_t max_cand, uint32_t* n_cand, uint64_t* cand, uint32_t* counts, uint32_t counts_stride,
                uint32_t* chosen, uint32_t* chosen_exhaustive, uint32_t* flags) {
+    SCZ_NVTX();
     if (!ctx || !x || !n_cand) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     EncPlan pl;
@@ -2209,6 +2230,7 @@ int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t 
                        int64_t n_rows, int precision, int format, uint32_t lanes, uint32_t block_syms,
                        const scz_info** infos, const uint8_t** payload, const uint32_t** freqs,
                        const uint32_t** block_bytes, uint64_t* sizes) {
+    SCZ_NVTX();
     if (!ctx || !h_x || !infos) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     ctx->mark();
@@ -2307,6 +2329,7 @@ int scz_compress_batch(scz_ctx* ctx, const float* h_x, uint64_t total, uint32_t 
 int scz_decompress_batch(scz_ctx* ctx, const scz_info* h_info, uint32_t batch, const uint32_t* h_freqs,
                          uint64_t freqs_count, const uint32_t* h_blocks, uint64_t blocks_count,
                          const uint8_t* h_payload, uint64_t payload_bytes, float* h_out, int32_t* h_status) {
+    SCZ_NVTX();
     if (!ctx || !h_info || !h_freqs || !h_payload || !h_out || !h_status) return SCZ_INVALID_INPUT;
     cudaSetDevice(ctx->device);
     ctx->mark();
