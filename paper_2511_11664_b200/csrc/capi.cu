@@ -1369,6 +1369,11 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
 extern "C" {
 
 int scz_abi_version(void) { return 1; }
+#ifdef SCZ_ENC_PROBE
+extern "C" int scz_debug_enc_probe(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, scz::g_enc_probe, (size_t)n * 8 * 8) == cudaSuccess ? 0 : 100;
+}
+#endif
 
 int scz_ctx_create(int device, scz_ctx** out) {
     if (!out) return SCZ_INVALID_INPUT;

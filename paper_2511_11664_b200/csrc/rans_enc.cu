@@ -19,6 +19,21 @@
 namespace scz {
 
 constexpr int ENC2_WPB = 4;                  // warps (= blocks) per CTA
+#ifdef SCZ_ENC_PROBE
+// diagnostics build: %globaltimer stamps per block (first 512 blocks of
+// tensor 0): start, table staged, coded, looked back, copied, done
+__device__ unsigned long long g_enc_probe[512][8];
+#define ENC_STAMP(blk, i)                                                                      \
+    do {                                                                                       \
+        if ((threadIdx.x & 31) == 0 && blockIdx.x == 0 && (blk) < 512) {                       \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+            g_enc_probe[(blk)][(i)] = t_;                                                     \
+        }                                                                                      \
+    } while (0)
+#else
+#define ENC_STAMP(blk, i) do { } while (0)
+#endif
 constexpr uint32_t ENC_TAB_SMEM_MAX = 8192;  // table entries staged in smem (128 KB)
 
 // In-kernel packing (pipeline launches; payload == nullptr for the stage
@@ -101,10 +116,14 @@ __device__ __forceinline__ void warp_copy_bytes(uint8_t* dst, const uint8_t* src
                                        __funnelshift_r(b.y, b.z, r), __funnelshift_r(b.z, b.w, r));
         }
     };
-    for (uint32_t c0 = 0; c0 < n16; c0 += 64) {
-        uint4 a[2], bb[2];
+#ifndef SCZ_COPY_K
+#define SCZ_COPY_K 2
+#endif
+    constexpr int CK_ = SCZ_COPY_K;  // chunks per lane in flight
+    for (uint32_t c0 = 0; c0 < n16; c0 += 32 * CK_) {
+        uint4 a[CK_], bb[CK_];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < CK_; ++k) {
             const uint32_t c = c0 + 32 * k + lane;
             if (c < n16) {
                 a[k] = sw[c];
@@ -112,7 +131,7 @@ __device__ __forceinline__ void warp_copy_bytes(uint8_t* dst, const uint8_t* src
             }
         }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < CK_; ++k) {
             const uint32_t c = c0 + 32 * k + lane;
             if (c < n16) d2[c] = sh ? pick(a[k], bb[k]) : a[k];
         }
@@ -436,8 +455,11 @@ __device__ __forceinline__ void enc_v2_block_tail(const EncParams& p, const Pack
     if (pk.payload) {
         __threadfence();  // error bits before the length is published
         __syncwarp();     // the slot bytes of every lane are visible to the warp
+        ENC_STAMP(blk, 3);
         const uint32_t excl = chunk_prefix(pk.lb + (uint64_t)b * p.slots_per_tensor, blk, blen);
+        ENC_STAMP(blk, 4);
         warp_copy_bytes(pk.payload + (uint64_t)b * pk.pcap + excl, start, blen, lane);
+        ENC_STAMP(blk, 5);
         // the slot is dead now: drop its L2 lines without a write-back to HBM
         // (slots are 128-byte aligned; the lines below `start` hold only this
         // slot's unused head)
@@ -445,6 +467,7 @@ __device__ __forceinline__ void enc_v2_block_tail(const EncParams& p, const Pack
         for (uintptr_t a = (reinterpret_cast<uintptr_t>(start) & ~(uintptr_t)127) + 128 * lane;
              a < reinterpret_cast<uintptr_t>(slot_end); a += 128 * 32)
             asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(a) : "memory");
+        ENC_STAMP(blk, 6);
         if (blk == nblk - 1 && lane == 0) {
             __threadfence();  // every block published: their error bits are visible
             const uint32_t eb = *(volatile uint32_t*)&st.errbits;
@@ -460,6 +483,7 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
     // apart, so a group's look-back predecessors started well before it, and
     // the idle groups past a tensor's block count all sit at the grid's tail
     const uint32_t b = blockIdx.x;
+    ENC_STAMP(blockIdx.y * ENC2_WPB + (threadIdx.x >> 5), 0);
     TensorState& st = p.state[b];
     if (st.status != SCZ_OK) {
         if (pk.payload && pk.write_failed && blockIdx.y == 0 && threadIdx.x == 0)
@@ -493,7 +517,9 @@ __device__ __forceinline__ void enc_v2_body(const EncParams& p, const Src& src, 
     uint8_t* slot_end = p.slots + ((uint64_t)b * p.slots_per_tensor + blk + 1) * p.slot_cap;
     EncLane E{STATE_LOW, 0u, 0u};
     if constexpr (RING) {
+        ENC_STAMP(blk, 1);
         enc_v2_ring(E, cur.d, len, steps, s_tab, slot_end, warp, lane, gtm);
+        ENC_STAMP(blk, 2);
     } else if (steps > 0) {
         // the highest step may be partial: peel it
         const int s_top = steps - 1;
