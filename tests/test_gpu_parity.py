@@ -437,6 +437,33 @@ def test_random_round_trips_vs_oracle():
         assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32))
 
 
+def test_precisions_round_trip_vs_oracle():
+    """Every rANS precision of the container API (container.py:80-84: 8..15),
+    both formats, on tensors long enough that the v1 coders' queues and
+    payload-window rings wrap many times (tens of thousands of symbols)."""
+    rng = np.random.default_rng(11)
+    for i, precision in enumerate(range(8, 16)):
+        for fmt in (1, 2):
+            total = int(rng.integers(20000, 90000))
+            q = int(rng.integers(4, 9))
+            x = rng.laplace(0, 1, total).astype(np.float32)
+            if i % 2 == 0:
+                x = np.abs(x)
+                x[rng.random(total) < 0.5] = 0.0
+            t = sz.FeatureTensor((total,), x)
+            try:
+                ref = orc.compress(x, (total,), q, None, precision, fmt=fmt, lanes=32, block_syms=2048)
+            except orc.OracleError as e:
+                assert e.status == orc.PRECISION_TOO_SMALL
+                with pytest.raises(PrecisionTooSmall):
+                    sz.compress(t, q, None, precision=precision, format=fmt, block_syms=2048)
+                continue
+            c = sz.compress(t, q, None, precision=precision, format=fmt, block_syms=2048)
+            assert container.to_bytes(c) == orc.to_bytes(ref), (precision, fmt, total, q)
+            out = sz.decompress(c)
+            assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32))
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
