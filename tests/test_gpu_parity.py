@@ -464,6 +464,44 @@ def test_precisions_round_trip_vs_oracle():
             assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32))
 
 
+def test_corrupt_payload_outcomes_match_oracle():
+    """Bit flips and byte replacements anywhere in the payload of v1 and v2
+    containers: the GPU decoders and the oracle reach the same outcome -- the same error class
+    (rans.py:199-212 underrun / final-state / leftover-byte checks, the row
+    checks of sparse.py:84-97) or bit-identical output."""
+    from paper_2511_11664_b200.errors import STATUS_TO_ERROR, SczipError
+
+    rng = np.random.default_rng(13)
+    total = 40000
+    x = np.abs(rng.laplace(0, 1, total)).astype(np.float32)
+    x[rng.random(total) < 0.5] = 0.0
+    t = sz.FeatureTensor((total,), x)
+    for fmt in (1, 2):
+        ref = orc.compress(x, (total,), 8, None, 14, fmt=fmt, lanes=32, block_syms=2048)
+        raw = container.to_bytes(sz.compress(t, 8, None, format=fmt, block_syms=2048))
+        assert raw == orc.to_bytes(ref)
+        plen = len(ref["payload"])
+        for k in range(64):
+            # 48 single-bit flips, then 16 whole-byte replacements
+            pos = int(rng.integers(0, plen))
+            bit = 1 << int(rng.integers(0, 8)) if k < 48 else int(rng.integers(1, 256))
+            bad = bytearray(raw)
+            bad[len(raw) - plen + pos] ^= bit
+            pl = bytearray(ref["payload"])
+            pl[pos] ^= bit
+            try:
+                want, werr = orc.decompress(dict(ref, payload=bytes(pl))), None
+            except orc.OracleError as e:
+                want, werr = None, STATUS_TO_ERROR[e.status]
+            try:
+                got, gerr = sz.decompress(container.from_bytes(bytes(bad))).data, None
+            except SczipError as e:
+                got, gerr = None, type(e)
+            assert gerr is werr, (fmt, pos, bit, gerr, werr)
+            if werr is None:
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (fmt, pos, bit)
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
