@@ -502,6 +502,57 @@ def test_corrupt_payload_outcomes_match_oracle():
                 assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (fmt, pos, bit)
 
 
+def test_corrupt_block_table_outcomes_match_oracle():
+    """v2 block-length tables edited with the total kept (so the container
+    still parses): lengths swapped, bytes moved between neighbours, a block
+    shorter than its 32 lane states.  GPU decode and oracle agree on the
+    error class or on bit-identical output."""
+    import dataclasses
+
+    from paper_2511_11664_b200.errors import STATUS_TO_ERROR, SczipError
+
+    rng = np.random.default_rng(17)
+    total = 60000
+    x = rng.laplace(0, 1, total).astype(np.float32)
+    t = sz.FeatureTensor((total,), x)
+    ref = orc.compress(x, (total,), 8, None, 14, fmt=2, lanes=32, block_syms=2048)
+    c = sz.compress(t, 8, None, format=2, block_syms=2048)
+    assert container.to_bytes(c) == orc.to_bytes(ref)
+    bb0 = np.asarray(ref["block_bytes"], dtype=np.int64)
+    nb = bb0.size
+    assert nb >= 4
+    cases = []
+    for _ in range(12):
+        i = int(rng.integers(0, nb - 1))
+        kind = int(rng.integers(0, 3))
+        bb = bb0.copy()
+        if kind == 0:
+            bb[i], bb[i + 1] = bb[i + 1], bb[i]
+        elif kind == 1:
+            d = int(rng.integers(1, 5)) * (1 if rng.random() < 0.5 else -1)
+            bb[i] += d
+            bb[i + 1] -= d
+        else:
+            d = int(bb[i]) - 100  # shorter than the 128 state bytes
+            bb[i] -= d
+            bb[i + 1] += d
+        cases.append(bb)
+    for bb in cases:
+        if (bb <= 0).any():
+            continue
+        try:
+            want, werr = orc.decompress(dict(ref, block_bytes=bb.astype(np.uint32))), None
+        except orc.OracleError as e:
+            want, werr = None, STATUS_TO_ERROR[e.status]
+        try:
+            got, gerr = sz.decompress(dataclasses.replace(c, block_bytes=bb.astype(np.uint32))).data, None
+        except SczipError as e:
+            got, gerr = None, type(e)
+        assert gerr is werr, (bb.tolist()[:6], gerr, werr)
+        if werr is None:
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
