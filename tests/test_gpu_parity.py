@@ -553,6 +553,64 @@ def test_corrupt_block_table_outcomes_match_oracle():
             assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+def test_batch_decode_isolates_corrupt_tensors():
+    """One batch decode (scz_decompress_batch) over good and corrupted v1 / v2
+    containers: every corrupted tensor reports the oracle's status, every good
+    tensor decodes bit-identically -- a bad stream never leaks into its
+    neighbours (per-tensor status)."""
+    import ctypes
+
+    from paper_2511_11664_b200 import _native
+
+    rng = np.random.default_rng(19)
+    conts, refs = [], []
+    for i in range(10):
+        total = int(rng.integers(5000, 30000))
+        x = np.abs(rng.laplace(0, 1, total)).astype(np.float32)
+        x[rng.random(total) < 0.5] = 0.0
+        fmt = 1 + i % 2
+        ref = orc.compress(x, (total,), 8, None, 14, fmt=fmt, lanes=32, block_syms=2048)
+        c = sz.compress(sz.FeatureTensor((total,), x), 8, None, format=fmt, block_syms=2048)
+        if i in (2, 5, 6):  # corrupt these: flip a payload byte
+            pos = int(rng.integers(4, len(ref["payload"])))
+            pl = bytearray(ref["payload"])
+            pl[pos] ^= 0x5A
+            ref = dict(ref, payload=bytes(pl))
+            raw = bytearray(container.to_bytes(c))
+            raw[len(raw) - len(pl) + pos] ^= 0x5A
+            c = container.from_bytes(bytes(raw))
+        conts.append(c)
+        refs.append(ref)
+    B = len(conts)
+    infos = (_native.Info * B)()
+    pay_off = fr_off = bl_off = 0
+    for i, c in enumerate(conts):
+        info = container._info_for(c)
+        info.payload_off, info.freqs_off, info.blocks_off = pay_off, fr_off, bl_off
+        infos[i] = info
+        pay_off += len(c.payload)
+        fr_off += c.alphabet_size
+        bl_off += c.n_blocks if c.version == 2 else 0
+    payload = np.frombuffer(b"".join(bytes(c.payload) for c in conts), np.uint8)
+    freqs = np.concatenate([np.asarray(c.freqs, dtype=np.uint32) for c in conts])
+    blocks = np.concatenate([np.asarray(c.block_bytes, dtype=np.uint32) for c in conts if c.version == 2])
+    out = np.empty(sum(c.total for c in conts), np.float32)
+    status = (ctypes.c_int32 * B)()
+    ctx = _native.context()
+    ctx.check(ctx.lib.scz_decompress_batch(ctx.h, infos, B, _native.ptr(freqs), freqs.size, _native.ptr(blocks),
+                                           bl_off, _native.ptr(payload), pay_off, _native.ptr(out), status))
+    pos = 0
+    for i, (c, ref) in enumerate(zip(conts, refs)):
+        try:
+            want, wst = orc.decompress(ref), 0
+        except orc.OracleError as e:
+            want, wst = None, e.status
+        assert int(status[i]) == wst, (i, int(status[i]), wst)
+        if wst == 0:
+            assert np.array_equal(out[pos: pos + c.total].view(np.uint32), want.view(np.uint32)), i
+        pos += c.total
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
