@@ -121,6 +121,43 @@ def test_bench_device_path_bit_exact(wl, fmt):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32)), (name, fmt, "device headers")
 
 
+@pytest.mark.parametrize("fmt", [2, 1])
+def test_unaligned_device_inputs(fmt):
+    """Tensors whose fp32 data starts off a 16-byte boundary (an odd element
+    count and a one-element offset into the allocation): the statistics and
+    quantiser kernels take their bounds-checked scalar loads, and the
+    containers and reconstructions still equal the oracle's.  The decode
+    output goes to an unaligned destination too."""
+    import torch
+
+    B, T, q = 4, 40001, 8
+    xs = np.stack([make_input(dict(kind="relu-laplace", dims=(T,), sparsity=0.5, seed=100 + s)) for s in range(B)])
+    buf = torch.zeros(B * T + 3, dtype=torch.float32, device="cuda")
+    x = buf[1: 1 + B * T]
+    x.copy_(torch.from_numpy(xs.ravel()))
+    obuf = torch.full((B * T + 3,), -7.0, dtype=torch.float32, device="cuda")
+    out = obuf[3: 3 + B * T]
+    ctx = _native.Context(0)
+    lib = ctx.lib
+    batch = _native.Batch()
+    infos = (_native.Info * B)()
+    ctx.check(lib.scz_encode_batch(ctx.h, ctypes.c_void_p(x.data_ptr()), T, B, q, -1, 14, fmt, 32, 2048,
+                                   ctypes.byref(batch)))
+    ctx.check(lib.scz_batch_sync(ctx.h, ctypes.byref(batch), infos))
+    ctx.check(lib.scz_decode_batch_async(ctx.h, infos, B, ctypes.c_void_p(batch.d_freqs),
+                                         ctypes.c_void_p(batch.d_block_bytes), ctypes.c_void_p(batch.d_payload),
+                                         ctypes.c_void_p(out.data_ptr())))
+    st = (ctypes.c_int32 * B)()
+    ctx.check(lib.scz_decode_status(ctx.h, B, st))
+    assert list(st) == [0] * B
+    got = device_batch_containers(ctx, batch, infos, B, (T,))
+    refs = [orc.compress(xs[i], (T,), q, None, 14, fmt=fmt, lanes=32, block_syms=2048) for i in range(B)]
+    for i in range(B):
+        assert container.to_bytes(got[i]) == orc.to_bytes(refs[i]), (fmt, i)
+    want = np.stack([orc.decompress(r) for r in refs]).ravel()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32)), fmt
+
+
 GENERAL = GENERAL_ALPHABET
 
 
