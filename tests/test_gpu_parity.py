@@ -611,6 +611,45 @@ def test_batch_decode_isolates_corrupt_tensors():
         pos += c.total
 
 
+def test_edge_tensors_batch_vs_oracle():
+    """Degenerate and extreme tensors through one batch encode / decode
+    (compress_many / decompress_many) in both formats: all zeros, one
+    nonzero, a constant (hi == lo: scale 1.0), signed with -0.0 entries,
+    subnormal magnitudes and magnitudes near the fp32 maximum (both outside
+    the fp32 guard-band range: the exact fp64 path for every element), one
+    element.  Containers byte-identical to the oracle, outputs bit-identical."""
+    T = 4096
+    rng = np.random.default_rng(23)
+    base = np.abs(rng.laplace(0, 1, T)).astype(np.float32)
+    cases = {
+        "zeros": np.zeros(T, np.float32),
+        "one_nonzero": np.where(np.arange(T) == 1234, np.float32(3.5), np.float32(0.0)).astype(np.float32),
+        "constant": np.full(T, 0.75, np.float32),
+        "signed_negzero": np.where(rng.random(T) < 0.3, np.float32(-0.0),
+                                   rng.laplace(0, 1, T).astype(np.float32)).astype(np.float32),
+        "subnormal": (base * np.float32(1e-41)).astype(np.float32),
+        "huge": (base / base.max() * np.float32(3e38)).astype(np.float32),
+    }
+    for fmt in (1, 2):
+        for q in (2, 8):
+            names = list(cases)
+            ts = [sz.FeatureTensor((T,), cases[n]) for n in names]
+            got = container.compress_many(ts, q, None, format=fmt, block_syms=2048)
+            for n, c in zip(names, got):
+                ref = orc.compress(cases[n], (T,), q, None, 14, fmt=fmt, lanes=32, block_syms=2048)
+                assert container.to_bytes(c) == orc.to_bytes(ref), (n, fmt, q)
+            outs = container.decompress_many(got)
+            for n, o, c in zip(names, outs, got):
+                ref = orc.compress(cases[n], (T,), q, None, 14, fmt=fmt, lanes=32, block_syms=2048)
+                assert np.array_equal(o.data.view(np.uint32), orc.decompress(ref).view(np.uint32)), (n, fmt, q)
+        # a one-element tensor on the single-tensor path
+        one = np.array([1.25], np.float32)
+        c = sz.compress(sz.FeatureTensor((1,), one), 8, None, format=fmt, block_syms=2048)
+        ref = orc.compress(one, (1,), 8, None, 14, fmt=fmt, lanes=32, block_syms=2048)
+        assert container.to_bytes(c) == orc.to_bytes(ref), fmt
+        assert np.array_equal(sz.decompress(c).data.view(np.uint32), orc.decompress(ref).view(np.uint32))
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
