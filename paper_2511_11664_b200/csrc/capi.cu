@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no link dependency, near-free without a tool
@@ -371,6 +372,33 @@ namespace {
 // kernel's CTAs are scheduled while the previous grid drains, and wait in
 // pdl_wait() (every kernel's first statement) for its completion.  Inside a
 // captured graph these become programmatic edges.
+// Dynamic shared memory opt-in.  The attribute is per kernel and process,
+// not per context: contexts on other threads setting it to their own sizes
+// would race (a smaller value set between another thread's set and launch
+// makes that launch fail).  So every kernel is opted in once, to the device
+// maximum minus its static shared memory; occupancy still follows the
+// dynamic size of each launch.
+template <typename K>
+cudaError_t smem_optin(K kern) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;  // (kernel, device)
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& d : done)
+        if (d.first == (const void*)kern && d.second == dev) return cudaSuccess;
+    cudaFuncAttributes a;
+    if ((e = cudaFuncGetAttributes(&a, kern)) != cudaSuccess) return e;
+    int optin = 0;
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - (int)a.sharedSizeBytes)) != cudaSuccess)
+        return e;
+    done.emplace_back((const void*)kern, dev);
+    return cudaSuccess;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {
@@ -936,7 +964,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
     const size_t sel_smem = pl.searching ? select_smem_bytes(pl.acap, (uint32_t)rh_total, sel.nb) : 0;
     auto k_sel = sel_wide ? k_select<SEL_THREADS_WIDE> : k_select<SEL_THREADS>;
     if (sel_smem > 0)  // static BlockScratch + dynamic may pass 48 KB: always opt in
-        CK(cudaFuncSetAttribute(k_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
+        CK(smem_optin(k_sel));
     const bool probe = getenv("SCZ_SELECT_PROBE") && !ctx->timing && B <= 64;
     if (probe) {  // debug timeline of k_select phases (synchronous; graphs off)
         CK(ctx->probe.ensure((size_t)B * sel.groups * 16 * 8));
@@ -1001,8 +1029,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
             using Src = decltype(src);
             if (pl.format == 2) {
                 if (enc_smem_tab) {
-                    CK(cudaFuncSetAttribute(k_rans_enc_v2<Src, true, false>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)enc_smem));
+                    CK(smem_optin(k_rans_enc_v2<Src, true, false>));
                     CK(launch_pdl(k_rans_enc_v2<Src, true, false>, g_enc2, ENC2_WPB * 32, enc_smem, s, ep, src,
                                   pk));
                 } else {
@@ -1033,8 +1060,7 @@ int run_encode(scz_ctx* ctx, const float* d_x, const EncPlan& pl, double* cand_o
         const Contig8Src s8{ctx->v8.as<uint8_t>(), dstride};
         const SplitSrc<uint16_t> s16{ctx->v8.as<uint8_t>(), dstride, ctx->cr.as<uint16_t>(), 2 * T};
         if (enc_smem_tab) {
-            CK(cudaFuncSetAttribute(k_rans_enc_v2_u8u16<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)enc_smem));
+            CK(smem_optin(k_rans_enc_v2_u8u16<true>));
             CK(launch_pdl(k_rans_enc_v2_u8u16<true>, g_enc2, ENC2_WPB * 32, enc_smem, s, ep, s8, s16, pk));
         } else {
             CK(launch_pdl(k_rans_enc_v2_u8u16<false>, g_enc2, ENC2_WPB * 32, 0, s, ep, s8, s16, pk));
@@ -1272,7 +1298,7 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
             const int wpb = small ? DEC2_WPB_SMALL : DEC2_WPB;
             auto kern = small ? k_rans_dec_v2<S, L, DEC2_WPB_SMALL> : k_rans_dec_v2<S, L, DEC2_WPB>;
             size_t smem = dec_v2_smem(wpb, sizeof(L), maxn, (uint32_t)maxA);
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(smem_optin(kern));
             CK(launch_pdl(kern, dim3(ceil_div_u32(nblk_cap, wpb), B), wpb * 32, smem, s, dp));
             LAUNCHED(wname<S>("k_rans_dec_v2"));
         }
@@ -1282,13 +1308,11 @@ int decode_launches(scz_ctx* ctx, uint32_t B, const DecCaps& c, const uint32_t* 
             if (fast) {  // u8 / u16 classes: the role-split serial decoder (rans_v1.cu)
                 const size_t smem = dec_v1p_smem(maxn, sizeof(L));
                 if constexpr (sizeof(L) < 4)
-                    CK(cudaFuncSetAttribute(k_rans_dec_v1p<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem));
+                    CK(smem_optin(k_rans_dec_v1p<S, L>));
                 if constexpr (sizeof(L) < 4) CK(launch_plain(k_rans_dec_v1p<S, L>, B, V1_THREADS, smem, s, dp));
             } else {
                 size_t smem = RING + tab + lut;
-                CK(cudaFuncSetAttribute(k_rans_dec_v1<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
+                CK(smem_optin(k_rans_dec_v1<S, L>));
                 CK(launch_pdl(k_rans_dec_v1<S, L>, B, 32, smem, s, dp));
             }
             LAUNCHED(wname<S>("k_rans_dec_v1"));
@@ -2031,8 +2055,7 @@ int scz_rans_encode(scz_ctx* ctx, const uint32_t* d, uint64_t n, const uint32_t*
     PlainSrc src{ctx->dsym.as<uint32_t>(), 0};
     if (v2 && alphabet <= ENC_TAB_SMEM_MAX) {
         const size_t sm = (size_t)alphabet * sizeof(EncTab);
-        CK(cudaFuncSetAttribute(k_rans_enc_v2<PlainSrc, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm));
+        CK(smem_optin(k_rans_enc_v2<PlainSrc, true, true>));
         k_rans_enc_v2<PlainSrc, true, true><<<dim3(1, ceil_div_u32(nblk, ENC2_WPB)), ENC2_WPB * 32, sm, s>>>(ep, src, PackParams{});
     } else if (v2) {
         k_rans_enc_v2<PlainSrc, false, true><<<dim3(1, ceil_div_u32(nblk, ENC2_WPB)), ENC2_WPB * 32, 0, s>>>(ep, src, PackParams{});
@@ -2132,11 +2155,11 @@ int scz_rans_decode(scz_ctx* ctx, const uint8_t* data, uint64_t len, const uint3
             const int wpb = small ? DEC2_WPB_SMALL : DEC2_WPB;
             auto kern = small ? k_rans_dec_v2<S, S, DEC2_WPB_SMALL> : k_rans_dec_v2<S, S, DEC2_WPB>;
             size_t smem = dec_v2_smem(wpb, sizeof(S), precision, (uint32_t)alphabet);
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(smem_optin(kern));
             kern<<<dim3(ceil_div_u32(n_blocks, wpb), 1), wpb * 32, smem, s>>>(dp);
         } else {
             size_t smem = RING + tab + lut;
-            CK(cudaFuncSetAttribute(k_rans_dec_v1<S, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CK(smem_optin(k_rans_dec_v1<S, S>));
             k_rans_dec_v1<S, S><<<1, 32, smem, s>>>(dp);
         }
         LAUNCHED("k_rans_dec");

@@ -650,6 +650,53 @@ def test_edge_tensors_batch_vs_oracle():
         assert np.array_equal(sz.decompress(c).data.view(np.uint32), orc.decompress(ref).view(np.uint32))
 
 
+def test_concurrent_threads_match_oracle():
+    """Four host threads, each with its own library context (thread-local,
+    _native.context), compress and decompress different tensors at the same
+    time in both formats and through the batch API: every container and
+    reconstruction equals the oracle's (contexts share no mutable state)."""
+    import threading
+
+    rng = np.random.default_rng(29)
+    work = []
+    for k in range(4):
+        xs = []
+        for j in range(3):
+            total = int(rng.integers(3000, 20000))
+            x = np.abs(rng.laplace(0, 1, total)).astype(np.float32)
+            x[rng.random(total) < 0.5] = 0.0
+            xs.append(x)
+        work.append(xs)
+    want = [[(orc.to_bytes(orc.compress(x, (x.size,), 8, None, 14, fmt=f, lanes=32, block_syms=2048)))
+             for x in xs for f in (1, 2)] for xs in work]
+    errors = []
+
+    def run(k):
+        try:
+            for _ in range(4):
+                got = []
+                for x in work[k]:
+                    for f in (1, 2):
+                        c = sz.compress(sz.FeatureTensor((x.size,), x), 8, None, format=f, block_syms=2048)
+                        got.append(container.to_bytes(c))
+                        out = sz.decompress(c)
+                        ref = orc.compress(x, (x.size,), 8, None, 14, fmt=f, lanes=32, block_syms=2048)
+                        assert np.array_equal(out.data.view(np.uint32), orc.decompress(ref).view(np.uint32))
+                assert got == want[k], k
+                many = container.compress_many([sz.FeatureTensor((x.size,), x) for x in work[k]], 8, None,
+                                               format=2, block_syms=2048)
+                assert [container.to_bytes(c) for c in many] == want[k][1::2], k
+        except Exception as e:  # surfaced below
+            errors.append((k, e))
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
