@@ -697,6 +697,50 @@ def test_concurrent_threads_match_oracle():
     assert not errors, errors
 
 
+def test_context_recovers_after_errors():
+    """Failing calls leave the calling thread's context usable: corrupt
+    containers (single and batch decode), invalid arguments and a
+    NonDivisible reshape, each followed by a good round trip on the same
+    context (graph caches included), which must still equal the oracle."""
+    rng = np.random.default_rng(31)
+    total = 24000
+    x = np.abs(rng.laplace(0, 1, total)).astype(np.float32)
+    x[rng.random(total) < 0.5] = 0.0
+    t = sz.FeatureTensor((total,), x)
+    refs = {f: orc.compress(x, (total,), 8, None, 14, fmt=f, lanes=32, block_syms=2048) for f in (1, 2)}
+    good = {f: sz.compress(t, 8, None, format=f, block_syms=2048) for f in (1, 2)}
+
+    def check_good():
+        for f in (1, 2):
+            c = sz.compress(t, 8, None, format=f, block_syms=2048)
+            assert container.to_bytes(c) == orc.to_bytes(refs[f])
+            assert np.array_equal(sz.decompress(c).data.view(np.uint32),
+                                  orc.decompress(refs[f]).view(np.uint32))
+        outs = container.decompress_many([good[1], good[2]])
+        for o, f in zip(outs, (1, 2)):
+            assert np.array_equal(o.data.view(np.uint32), orc.decompress(refs[f]).view(np.uint32))
+
+    for it in range(3):
+        for f in (1, 2):
+            raw = bytearray(container.to_bytes(good[f]))
+            raw[-5] ^= 0xFF  # a payload byte near the end
+            bad = container.from_bytes(bytes(raw))
+            try:
+                sz.decompress(bad)
+            except CorruptStream:
+                pass
+            try:
+                container.decompress_many([good[1], bad, good[2]])
+            except CorruptStream:
+                pass
+            check_good()
+        with pytest.raises(NonDivisible):
+            sz.compress(t, 8, 7)  # 7 does not divide 24000
+        with pytest.raises(InvalidInput):
+            sz.compress(t, 0)
+        check_good()
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
