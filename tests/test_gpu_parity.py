@@ -741,6 +741,32 @@ def test_context_recovers_after_errors():
         check_good()
 
 
+def test_random_mixed_batches_vs_oracle():
+    """Randomised batches through compress_many / decompress_many: tensors of
+    different sizes (heterogeneous batch encode), sparsities and signs, the
+    search on, one Q per batch, both formats, odd block sizes."""
+    rng = np.random.default_rng(37)
+    for it in range(6):
+        q = int(rng.integers(2, 9))
+        fmt = 1 + it % 2
+        bs = int(rng.choice([256, 1024, 4096]))
+        xs = []
+        for _ in range(int(rng.integers(5, 14))):
+            total = int(rng.integers(100, 30000))
+            x = rng.laplace(0, 1, total).astype(np.float32)
+            if rng.random() < 0.6:
+                x = np.abs(x)
+                x[rng.random(total) < rng.uniform(0.0, 0.95)] = 0.0
+            xs.append(x)
+        ts = [sz.FeatureTensor((x.size,), x) for x in xs]
+        got = container.compress_many(ts, q, None, format=fmt, block_syms=bs)
+        outs = container.decompress_many(got)
+        for x, c, o in zip(xs, got, outs):
+            ref = orc.compress(x, (x.size,), q, None, 14, fmt=fmt, lanes=32, block_syms=bs)
+            assert container.to_bytes(c) == orc.to_bytes(ref), (it, x.size, q, fmt)
+            assert np.array_equal(o.data.view(np.uint32), orc.decompress(ref).view(np.uint32)), (it, x.size)
+
+
 def test_batch_api_matches_single_tensor_path():
     """compress_many / decompress_many (one device pass) == per-tensor calls."""
     ts = [sz.gen_synthetic("relu-laplace", [1, 64, 28, 28], 0.5 + 0.05 * i, 100 + i) for i in range(9)]
