@@ -468,25 +468,9 @@ __global__ void k_init_row_lut() {
 template <int KK, bool SUMS, bool VEC = false>
 __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(RowParams p) {
     static_assert(KK == 1 || KK == 2 || KK == 4, "row width");
-    pdl_wait();
-    const uint32_t b = blockIdx.y, chunk = blockIdx.x;
-    const scz_info& in = p.info[b];
-    if (in.sym_bytes != 1 || in.n_cols != (uint32_t)KK) return;
     constexpr uint32_t R = SMALL_ROWS;
     constexpr uint32_t PER = R / SMALL8_THREADS;
     constexpr uint32_t MAXE = R * KK;  // nonzeros of a valid chunk
-    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
-    if (r0 >= N) return;
-    // v2 tensors: the decoder summed every chunk's row counts (no look-back)
-    constexpr bool sums = SUMS;
-    if ((in.version == 2) != SUMS) return;  // the other variant's tensor
-    if constexpr (SUMS) {
-        if (*(const volatile int32_t*)(p.status + b) != SCZ_OK) return;
-    } else if (chunk_dead(p, b, chunk)) {
-        return;
-    }
-    const uint64_t nnz = in.nnz;
-    const uint8_t* d = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
     __shared__ __align__(16) uint8_t s_r[R + 32];
     __shared__ __align__(16) uint8_t s_c[MAXE + 32];
     __shared__ __align__(16) uint8_t s_v[MAXE + 32];
@@ -494,17 +478,11 @@ __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(Ro
     __shared__ uint32_t s_scan[33];
     __shared__ __align__(1024) float s_lut[256];  // bin address = base | 4 * symbol
     __shared__ int s_bad;
-    __shared__ uint32_t s_base, s_own;
-    const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
-    if (threadIdx.x == 0) s_bad = 0;
     // per column-presence mask: the sorted column packing and the PRMT
     // selector that moves the k-th value byte to its column (4 = zero byte)
     __shared__ uint32_t s_pk[1 << KK], s_sel[1 << KK];
     __shared__ __align__(16) uint32_t s_lut4[KK == 4 ? 5 * 256 : 4];
-    if constexpr (KK == 4)
-        for (uint32_t i = threadIdx.x; i < 5 * 256 / 4; i += SMALL8_THREADS)
-            cp_async16(reinterpret_cast<uint4*>(s_lut4) + i, reinterpret_cast<const uint4*>(g_row_lut4) + i);
-    if (threadIdx.x < (1u << KK)) {
+    if (threadIdx.x < (1u << KK)) {  // no dependency on the decoder: before the wait
         uint32_t pk = 0, sel = 0, k = 0;
         for (uint32_t j = 0; j < 4; ++j) {
             const bool here = j < (uint32_t)KK && ((threadIdx.x >> j) & 1u);
@@ -515,53 +493,72 @@ __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(Ro
         s_pk[threadIdx.x] = pk;
         s_sel[threadIdx.x] = sel;
     }
+    if (threadIdx.x == 0) s_bad = 0;
+    pdl_wait();
+    const uint32_t b = blockIdx.y, chunk = blockIdx.x;
+    const scz_info& in = p.info[b];
+    const uint64_t out_off = p.out_off[b];
+    // v2 tensors (SUMS): the decoder summed every chunk's row counts, so the
+    // chunk's nonzero offset (the sum over the earlier chunks) and its own
+    // count load together with the header and the status -- one memory round
+    // trip -- and every warp reduces them itself (no barrier before the r, c
+    // and v windows are staged: a second round trip, then the rows)
     uint32_t cbase = 0, own = 0;
-    const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);  // in flight with the sums
-    if (threadIdx.x < 64)  // the tensor's dequantisation table (k_dec_prepare)
-        cp_async16(reinterpret_cast<uint4*>(s_lut) + threadIdx.x,
-                   reinterpret_cast<const uint4*>(p.dq_lut + (uint64_t)b * 256) + threadIdx.x);
-    cp_async_commit();
-    if (sums) {
-        // chunk offset = sum of the earlier chunks' row counts, and this
-        // chunk's own count, both from the decoder: the r, c and v windows
-        // are then staged together (one memory round trip)
-        if (threadIdx.x < 32) {
-            const unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
-            const unsigned long long mine = threadIdx.x == 0 ? cs[chunk] : 0ull;
-            unsigned long long acc = 0;
-            for (uint32_t j0 = 0; j0 < chunk; j0 += 128) {  // four loads in flight per lane
-                unsigned long long v[4];
+    int32_t st0 = SCZ_OK;
+    if constexpr (SUMS) {
+        const uint32_t lane = threadIdx.x & 31;
+        st0 = *(const volatile int32_t*)(p.status + b);
+        const unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
+        const unsigned long long mine = cs[chunk];
+        unsigned long long acc = 0;
+        for (uint32_t j0 = 0; j0 < chunk; j0 += 128) {  // four loads in flight per lane
+            unsigned long long v[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t j = j0 + 32 * k + threadIdx.x;
-                    v[k] = j < chunk ? cs[j] : 0ull;
-                }
-                acc += (v[0] + v[1]) + (v[2] + v[3]);
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t j = j0 + 32 * k + lane;
+                v[k] = j < chunk ? cs[j] : 0ull;
             }
-            acc = warp_sum(acc);
-            if (threadIdx.x == 0) {
-                s_base = (uint32_t)min(acc, 0xFFFFFFFFull);
-                s_own = (uint32_t)min(mine, 0xFFFFFFFFull);
-            }
+            acc += (v[0] + v[1]) + (v[2] + v[3]);
         }
-        cp_async_wait<0>();
-        __syncthreads();
-        cbase = s_base;
-        own = s_own;
+        acc = warp_sum(acc);
+        st0 = __shfl_sync(0xffffffffu, st0, 0);  // one status per warp
+        cbase = (uint32_t)min(acc, 0xFFFFFFFFull);
+        own = (uint32_t)min(mine, 0xFFFFFFFFull);
+    }
+    if (in.sym_bytes != 1 || in.n_cols != (uint32_t)KK) return;
+    const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
+    if (r0 >= N) return;
+    if ((in.version == 2) != SUMS) return;  // the other variant's tensor
+    const uint64_t nnz = in.nnz;
+    const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
+    if constexpr (SUMS) {
+        if (st0 != SCZ_OK) return;
         if (own > nrow * KK || (uint64_t)cbase + own > nnz) {  // uniform
             if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
             return;
         }
+    } else if (chunk_dead(p, b, chunk)) {
+        return;
     }
+    const uint8_t* d = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    if constexpr (KK == 4)
+        for (uint32_t i = threadIdx.x; i < 5 * 256 / 4; i += SMALL8_THREADS)
+            cp_async16(reinterpret_cast<uint4*>(s_lut4) + i, reinterpret_cast<const uint4*>(g_row_lut4) + i);
+    const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);
+    if (threadIdx.x < 64)  // the tensor's dequantisation table (k_dec_prepare)
+        cp_async16(reinterpret_cast<uint4*>(s_lut) + threadIdx.x,
+                   reinterpret_cast<const uint4*>(p.dq_lut + (uint64_t)b * 256) + threadIdx.x);
+    cp_async_commit();
     uint32_t csh = 0, vsh = 0;
-    if (sums) {  // in flight during the scan below
+    if (SUMS) {  // in flight during the scan below
         csh = stage_window(s_c, d + nnz + cbase, own);
         vsh = stage_window(s_v, d + cbase, own);
         cp_async_commit();
+        cp_async_wait<1>();
     } else {
         cp_async_wait<0>();
-        __syncthreads();
     }
+    __syncthreads();
     // thread t owns rows [8t, 8t + 8) of the chunk for the scan: their count
     // bytes as two words (bytes past nrow masked off), checked, summed and
     // prefix-summed four at a time (SWAR; counts <= K keep every byte sum
@@ -584,7 +581,7 @@ __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(Ro
     uint32_t tot;
     uint32_t ex = block_exclusive_scan<SMALL8_THREADS>(sum, s_scan, &tot);
     if (rbad) s_bad = 1;
-    if (sums) {
+    if (SUMS) {
         if (threadIdx.x == 0 && (tot != own || (r0 + nrow == N && (uint64_t)cbase + tot != nnz)))  // sparse.py:84-87
             s_bad = 1;
         __syncthreads();
@@ -607,14 +604,14 @@ __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(Ro
         dst[1] = make_uint4(__byte_perm(p1, w1, 0x0400) + e1, __byte_perm(p1, w1, 0x0501) + e1,
                             __byte_perm(p1, w1, 0x0602) + e1, __byte_perm(p1, w1, 0x0703) + e1);
     }
-    if (!sums) {  // look-back path: the windows are known only now
+    if (!SUMS) {  // look-back path: the windows are known only now
         csh = stage_window(s_c, d + nnz + cbase, tot);
         vsh = stage_window(s_v, d + cbase, tot);
         cp_async_commit();
     }
     cp_async_wait<0>();
     __syncthreads();
-    float* orow0 = p.out + p.out_off[b] + r0 * KK;
+    float* orow0 = p.out + out_off + r0 * KK;
     const bool vec_ok = VEC || (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
     bool bad = false;
     // explicit 32-bit shared addresses (see lds_u32)
