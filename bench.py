@@ -407,11 +407,11 @@ def run_ours(args):
             e.record(streams[k])
             chain_ev[0] = e
 
-    def enc(k):
+    def enc(k, fmt=None):
         c = ctxs[k]
         chain(k)
         c.check(lib.scz_encode_batch(c.h, ctypes.c_void_p(x_dev.data_ptr()), T, B, wl["q"], -1, 14,
-                                     args.format, 32, args.block_syms, ctypes.byref(batches[k])))
+                                     fmt or args.format, 32, args.block_syms, ctypes.byref(batches[k])))
         mark(k)
 
     def dec(k):
@@ -427,14 +427,14 @@ def run_ours(args):
     host_ms = []  # host time spent queueing each step (diagnostic)
     step_ev = []  # (stream, event) after each step's decode (diagnostic)
 
-    def pipelined(n, clocks=None, record=False):
+    def pipelined(n, clocks=None, record=False, fmt=None):
         # step i's encode is queued NC - 1 steps ahead of its decode
         for i in range(min(NC - 1, n)):
-            enc(i % NC)
+            enc(i % NC, fmt)
         for i in range(n):
             t0 = time.perf_counter()
             if i + NC - 1 < n:
-                enc((i + NC - 1) % NC)
+                enc((i + NC - 1) % NC, fmt)
             dec(i % NC)
             if record:
                 host_ms.append((time.perf_counter() - t0) * 1e3)
@@ -482,6 +482,35 @@ def run_ours(args):
     for k in range(NC):
         ctxs[k].check(lib.scz_decode_status(ctxs[k].h, B, statuses))
         assert all(v == 0 for v in statuses), "decode status"
+
+    # ---- v1 (the reference's wire format) through the same pipeline --------
+    # One serial rANS chain per tensor: a batch costs one chain's latency, so
+    # the contexts' batches in flight (encodes queued NC - 1 steps ahead of
+    # their decodes) are what fill the GPU's schedulers.
+    v1_pipe = None
+    if not args.no_extras and rank == 0 and args.format == 2:
+        for _ in range(3):  # eager, graph capture, replay: per context
+            pipelined(NC, fmt=1)
+        torch.cuda.synchronize()
+        n1 = 2 * NC
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = [torch.cuda.Event(enable_timing=True) for _ in range(NC)]
+        e0.record(streams[0])
+        for st_ in streams[1:]:
+            st_.wait_event(e0)
+        pipelined(n1, fmt=1)
+        for k in range(NC):
+            e1[k].record(streams[k])
+        torch.cuda.synchronize()
+        ms1 = max(e0.elapsed_time(e) for e in e1) / n1
+        for k in range(NC):
+            ctxs[k].check(lib.scz_decode_status(ctxs[k].h, B, statuses))
+            assert all(v == 0 for v in statuses), "v1 decode status"
+        assert torch.equal(outs[0], outs[1]), "v1 reconstructions differ between contexts"
+        v1_pipe = dict(value=4.0 * T * B / (ms1 * 1e-3) / 1e9, unit=UNIT, ms_per_step=ms1, steps=n1,
+                       contexts=NC, batch=B,
+                       schedule=f"{NC} contexts, encodes queued {NC - 1} steps ahead of their decodes "
+                                "(as the headline value)")
 
     # ---- per-kernel times (separate pass: per-launch events, no graphs) ----
     ctx.set_timing(True)
@@ -551,7 +580,7 @@ def run_ours(args):
     # two steps ahead, which keeps both PCIe directions busy).
     e2e = None
     if not args.no_e2e:
-        e2e_ms, io, h_out, e2e_status = run_e2e(args, torch, _native, lib, local, host, T, B, wl)
+        e2e_ms, io, h_out, e2e_status = run_e2e(args, torch, _native, lib, local, host, T, B, wl, pairs=E2E_PAIRS)
         e2e_ms = max_over_ranks(e2e_ms)
         e2e_value = 4.0 * T * total_units / (e2e_ms * 1e-3) / 1e9
         assert all(s == 0 for s in e2e_status)
@@ -559,13 +588,18 @@ def run_ours(args):
         e2e = dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=io["h2d"],
                    d2h_bytes_per_step=io["d2h"], ms_per_step=e2e_ms, stage_ms=io["stage_ms"],
                    path="scz_compress_batch + scz_decompress_batch, pinned host buffers",
-                   schedule="2-stage pipeline: decompress(step i) || compress(step i+1)",
+                   schedule=f"{E2E_PAIRS} x 2-stage pipeline: decompress(step i) || compress(step i+1)",
                    timing="host clock between decompress completions in steady state",
                    host_cpus=f"{len(near)} GPU-local CPUs (NVML affinity)" if near else "unrestricted")
 
     extras = {}
     if not args.no_extras and rank == 0:
         extras = side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch)
+        if v1_pipe and "v1_reference_format" in extras:
+            v1 = extras["v1_reference_format"]
+            seq = dict(value=v1.pop("value"), ms_per_step=v1.pop("ms_per_step"),
+                       schedule="one context: encode, header read, decode")
+            extras["v1_reference_format"] = dict(v1_pipe, sequential=seq, **v1)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -596,36 +630,42 @@ def run_ours(args):
 
 
 E2E_SLOTS = int(os.environ.get("SCZ_E2E_SLOTS", "3"))
+V1_E2E_PAIRS = int(os.environ.get("SCZ_V1_E2E_PAIRS", "1"))
+E2E_PAIRS = int(os.environ.get("SCZ_E2E_PAIRS", "1"))
 
 
-def run_e2e(args, torch, _native, lib, device, host, T, B, wl):
+def run_e2e(args, torch, _native, lib, device, host, T, B, wl, pairs=1):
     """Pipelined round trips through the host-buffer entry points; returns
-    (ms per step, bytes per step, last output, last status)."""
+    (ms per step, bytes per step, last output, last status).  `pairs`
+    compressor/decompressor thread pairs each run the two-stage pipeline over
+    every pairs-th step (v1: one serial chain per tensor, so more batches in
+    flight fill the GPU)."""
     import threading
 
     ns = E2E_SLOTS
-    cctx = [_native.Context(device) for _ in range(ns)]  # compress slots
-    dctx = _native.Context(device)
+    nsl = ns * pairs
+    cctx = [_native.Context(device) for _ in range(nsl)]  # compress slots
+    dctx = [_native.Context(device) for _ in range(pairs)]
     slot = [dict(infos=ctypes.POINTER(_native.Info)(), pay=ctypes.POINTER(ctypes.c_uint8)(),
                  fr=ctypes.POINTER(ctypes.c_uint32)(), bl=ctypes.POINTER(ctypes.c_uint32)(),
-                 sizes=(ctypes.c_uint64 * 3)()) for _ in range(ns)]
-    free = [threading.Semaphore(1) for _ in range(ns)]
-    ready = [threading.Semaphore(0) for _ in range(ns)]
+                 sizes=(ctypes.c_uint64 * 3)()) for _ in range(nsl)]
+    free = [threading.Semaphore(1) for _ in range(nsl)]
+    ready = [threading.Semaphore(0) for _ in range(nsl)]
     h_out = torch.empty((B, T), dtype=torch.float32).pin_memory()
-    status = (ctypes.c_int32 * B)()
+    status = [(ctypes.c_int32 * B)() for _ in range(pairs)]
     # every compress slot and the decompress context see their shapes twice
     # (eager, then graph capture) before the timed window opens
-    n_warm = max(args.warmup, 2 * ns + 1)
+    n_warm = pairs * max(args.warmup, 2 * ns + 1)
     n_total = n_warm + args.steps
     done_at = [0.0] * n_total
     c_ms, d_ms = [], []
     errors = []
     io = {}
 
-    def compressor():
+    def compressor(t):
         try:
-            for i in range(n_total):
-                k = i % ns
+            for i in range(t, n_total, pairs):
+                k = i % nsl
                 free[k].acquire()
                 sl, c = slot[k], cctx[k]
                 t0 = time.perf_counter()
@@ -640,18 +680,19 @@ def run_e2e(args, torch, _native, lib, device, host, T, B, wl):
             for r in ready:
                 r.release()
 
-    def decompressor():
+    def decompressor(t):
         try:
-            for i in range(n_total):
-                k = i % ns
+            dc = dctx[t]
+            for i in range(t, n_total, pairs):
+                k = i % nsl
                 ready[k].acquire()
                 if errors:
                     return
                 sl = slot[k]
                 z = sl["sizes"]
                 t0 = time.perf_counter()
-                dctx.check(lib.scz_decompress_batch(dctx.h, sl["infos"], B, sl["fr"], z[1], sl["bl"], z[2],
-                                                    sl["pay"], z[0], ctypes.c_void_p(h_out.data_ptr()), status))
+                dc.check(lib.scz_decompress_batch(dc.h, sl["infos"], B, sl["fr"], z[1], sl["bl"], z[2],
+                                                  sl["pay"], z[0], ctypes.c_void_p(h_out.data_ptr()), status[t]))
                 done_at[i] = time.perf_counter()
                 d_ms.append((done_at[i] - t0) * 1e3)
                 io["h2d"] = 4 * T * B + z[0] + 4 * z[1] + 4 * z[2]
@@ -662,7 +703,7 @@ def run_e2e(args, torch, _native, lib, device, host, T, B, wl):
             for f in free:
                 f.release()
 
-    th = [threading.Thread(target=compressor), threading.Thread(target=decompressor)]
+    th = [threading.Thread(target=f, args=(t,)) for t in range(pairs) for f in (compressor, decompressor)]
     for t in th:
         t.start()
     for t in th:
@@ -670,9 +711,12 @@ def run_e2e(args, torch, _native, lib, device, host, T, B, wl):
     if errors:
         raise errors[0]
     w = n_warm
-    ms = (done_at[n_total - 1] - done_at[w - 1]) * 1e3 / args.steps
+    # steady state: completions per unit time, from the w-th completion to
+    # the last (pairs > 1 completes steps slightly out of order)
+    t_done = sorted(done_at)
+    ms = (t_done[-1] - t_done[w - 1]) * 1e3 / args.steps
     io["stage_ms"] = dict(compress=statistics.median(c_ms[w:]), decompress=statistics.median(d_ms[w:]))
-    return ms, io, h_out, list(status)
+    return ms, io, h_out, [v for st in status for v in st]
 
 
 def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
@@ -791,12 +835,15 @@ def side_measurements(args, ctx, lib, wl, T, x_dev, out_dev, stream, torch):
         a1 = copy.copy(args)
         a1.format, a1.steps, a1.warmup = 1, 5, 0
         host = x_dev.cpu().pin_memory()
-        e_ms, io, h_out, st1 = run_e2e(a1, torch, _native, lib, x_dev.device.index or 0, host, T, B, wl)
+        a1.steps = 12
+        e_ms, io, h_out, st1 = run_e2e(a1, torch, _native, lib, x_dev.device.index or 0, host, T, B, wl,
+                                       pairs=V1_E2E_PAIRS)
         assert all(v == 0 for v in st1)
         res["v1_reference_format"]["e2e"] = dict(
             value=4.0 * T * B / (e_ms * 1e-3) / 1e9, unit=UNIT, ms_per_step=e_ms, steps=a1.steps,
             h2d_bytes_per_step=io["h2d"], d2h_bytes_per_step=io["d2h"],
-            path="scz_compress_batch + scz_decompress_batch (format 1), pinned host buffers")
+            path="scz_compress_batch + scz_decompress_batch (format 1), pinned host buffers",
+            schedule=f"{V1_E2E_PAIRS} compress/decompress thread pairs, each a 2-stage pipeline")
     if not args.no_configs:
         peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
         peak = float(json.load(open(peaks_path))["hbm_gbs"]) if os.path.exists(peaks_path) else 6650.0
