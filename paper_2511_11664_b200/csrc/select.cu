@@ -269,25 +269,38 @@ __device__ __noinline__ int block_normalize(const uint32_t* counts, uint32_t A, 
         if (k >= A) {
             for (uint32_t i = threadIdx.x; i < A; i += NT) freqs[i] += 1;
         } else if (A <= 1024) {
-            // small alphabets: rank every symbol against all others in one pass
-            // (keys padded with zeros to a multiple of 8: a zero pad never
-            // outranks a real key, since pads sit at indices >= A)
-            const uint32_t A8 = (A + 7) & ~7u;
-            for (uint32_t i = threadIdx.x; i < A8; i += NT)
+            // small alphabets: rank every symbol against all others in one pass.
+            // P threads per symbol (the largest power of two <= 8 with
+            // A * P <= NT; neighbouring lanes) split the others by j mod P,
+            // then add their partial ranks with shuffles.  Keys are padded
+            // with zeros to a multiple of 8P: a zero pad never outranks a
+            // real key, since pads sit at indices >= A.
+            uint32_t P = 1;
+            while (P < 8 && A * (2 * P) <= (uint32_t)NT) P *= 2;
+            const uint32_t AP = (A + 8 * P - 1) & ~(8 * P - 1);
+            for (uint32_t i = threadIdx.x; i < AP; i += NT)
                 s.keys[i] = i < A ? (unsigned long long)__double_as_longlong(rem[i]) : 0ull;
             __syncthreads();
-            for (uint32_t i = threadIdx.x; i < A; i += NT) {
-                const unsigned long long ki = s.keys[i];
+            // P > 1: one pass, every lane of a warp that holds a symbol takes
+            // part in the shuffles (A * P <= NT, rounded up to whole warps)
+            const uint32_t span = P > 1 ? ((A * P + 31) & ~31u) : A;
+            for (uint32_t t = threadIdx.x; t < span; t += NT) {
+                const uint32_t i = t / P, q = t % P;
+                const bool live = i < A;
+                const unsigned long long ki = s.keys[live ? i : 0];
                 uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (uint32_t j = 0; j < A8; j += 8) {
+                // lanes of one symbol read 8-byte keys j = q (mod P): distinct banks
+                for (uint32_t j = q; j < AP; j += 8 * P) {
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        const unsigned long long kj = s.keys[j + u];
-                        r[u] += (kj > ki) | ((kj == ki) & (j + u < i));
+                        const uint32_t jj = j + u * P;
+                        const unsigned long long kj = s.keys[jj];
+                        r[u] += (kj > ki) | ((kj == ki) & (jj < i));
                     }
                 }
-                const uint32_t rank = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-                if (rank < k) freqs[i] += 1;
+                uint32_t rank = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+                for (uint32_t o = 1; o < P; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+                if (live && q == 0 && rank < k) freqs[i] += 1;
             }
         } else {
             deficit_radix(rem, A, k, freqs, s);
