@@ -267,6 +267,17 @@ def gpu_local_cpus(torch, device):
 
 
 # -------------------------------------------------------------- our arm
+# What bounds the rANS kernels below the HBM roofline (ncu --set full,
+# profiles/r2h/ncu_full_summary.txt and DESIGN.md 'Where the step time goes').
+LIMITERS = {
+    "k_rans_dec_v2": "not HBM: instruction issue (~73 % active, ~41 warp instructions per 32-symbol step) and "
+                     "shared-memory wavefronts (two random slot-table lookups per step, ~1.9x the conflict-free "
+                     "count); residency is capped at 32 warps/SM by the 80 KB table per CTA",
+    "k_rans_enc_v2": "not HBM: instruction issue (~73 % active, ~25 instructions per lane-step: renormalisation "
+                     "tests, ballot-scan byte placement, exact-reciprocal state update)",
+}
+
+
 def algorithmic_bytes(name, infos, T, nblk_bytes):
     """Bytes a kernel must move per launch, batch-summed."""
     nnz = sum(int(i["nnz"]) for i in infos)
@@ -564,6 +575,8 @@ def run_ours(args):
                         frac=(achieved / peak) if achieved else None, traffic=traffic,
                         algorithmic_bytes_per_launch=(ab / launches_per_step) if ab else None,
                         launch_ms=per_launch_ms, peak_source=peak_src)
+        if name.split("/")[0] in LIMITERS:
+            roofline["limiter"] = LIMITERS[name.split("/")[0]]
     pipe_bytes = 8 * T * B + 2 * total_bytes
     pipeline_roofline = dict(achieved=pipe_bytes / (ms * 1e-3) / 1e9, peak=peak, unit="GB/s",
                              frac=pipe_bytes / (ms * 1e-3) / 1e9 / peak,
