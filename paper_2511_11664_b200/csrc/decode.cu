@@ -420,6 +420,18 @@ __device__ __forceinline__ uint32_t stage_window(uint8_t* dst, const uint8_t* sr
     return sh;
 }
 
+// The 16-byte aligned span holding n bytes at src, for one bulk copy: byte i
+// lands at dst[sh + i] (same contract as stage_window).
+struct Win {
+    const uint8_t* a;
+    uint32_t sh, bytes;
+};
+__device__ __forceinline__ Win window_of(const uint8_t* src, uint32_t n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(src) - a);
+    return Win{reinterpret_cast<const uint8_t*>(a), sh, ((sh + n + 15) >> 4) << 4};
+}
+
 // 4 consecutive bytes at byte offset o of a shared array (any alignment).
 __device__ __forceinline__ uint32_t smem_word_at(const uint8_t* s, uint32_t o) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(s) + (o >> 2);
@@ -493,72 +505,98 @@ __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(Ro
         s_pk[threadIdx.x] = pk;
         s_sel[threadIdx.x] = sel;
     }
-    if (threadIdx.x == 0) s_bad = 0;
+    // SUMS: [0] r window + both tables, [1] c and v windows (bulk copies)
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ uint32_t s_cb[3];  // SUMS: chunk's nonzero offset, count, ok (warp 0)
+    if (threadIdx.x == 0) {
+        s_bad = 0;
+        if (SUMS) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+        }
+    }
     pdl_wait();
     const uint32_t b = blockIdx.y, chunk = blockIdx.x;
     const scz_info& in = p.info[b];
     const uint64_t out_off = p.out_off[b];
-    // v2 tensors (SUMS): the decoder summed every chunk's row counts, so the
-    // chunk's nonzero offset (the sum over the earlier chunks) and its own
-    // count load together with the header and the status -- one memory round
-    // trip -- and every warp reduces them itself (no barrier before the r, c
-    // and v windows are staged: a second round trip, then the rows)
-    uint32_t cbase = 0, own = 0;
-    int32_t st0 = SCZ_OK;
-    if constexpr (SUMS) {
-        const uint32_t lane = threadIdx.x & 31;
-        st0 = *(const volatile int32_t*)(p.status + b);
-        const unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
-        const unsigned long long mine = cs[chunk];
-        unsigned long long acc = 0;
-        for (uint32_t j0 = 0; j0 < chunk; j0 += 128) {  // four loads in flight per lane
-            unsigned long long v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t j = j0 + 32 * k + lane;
-                v[k] = j < chunk ? cs[j] : 0ull;
-            }
-            acc += (v[0] + v[1]) + (v[2] + v[3]);
-        }
-        acc = warp_sum(acc);
-        st0 = __shfl_sync(0xffffffffu, st0, 0);  // one status per warp
-        cbase = (uint32_t)min(acc, 0xFFFFFFFFull);
-        own = (uint32_t)min(mine, 0xFFFFFFFFull);
-    }
     if (in.sym_bytes != 1 || in.n_cols != (uint32_t)KK) return;
     const uint64_t N = in.n_rows, r0 = (uint64_t)chunk * R;
     if (r0 >= N) return;
     if ((in.version == 2) != SUMS) return;  // the other variant's tensor
     const uint64_t nnz = in.nnz;
     const uint32_t nrow = (uint32_t)((N - r0) < (uint64_t)R ? (N - r0) : (uint64_t)R);
+    const uint8_t* d = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
+    uint32_t cbase = 0, own = 0, rsh, csh = 0, vsh = 0;
     if constexpr (SUMS) {
-        if (st0 != SCZ_OK) return;
-        if (own > nrow * KK || (uint64_t)cbase + own > nnz) {  // uniform
-            if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
+        // v2 tensors: the decoder summed every chunk's row counts.  Warp 0
+        // alone puts the r window and both tables in flight (one bulk copy
+        // each, before the prefix is known), reduces the earlier chunks'
+        // counts to the chunk's nonzero offset, checks it and starts the c
+        // and v windows; the other warps learn the result at one barrier.
+        // Two memory round trips, as before, without a 256-thread copy loop.
+        rsh = window_of(d + 2 * nnz + r0, nrow).sh;
+        if (threadIdx.x < 32) {
+            const uint32_t lane = threadIdx.x;
+            if (lane == 0) {
+                const Win wr = window_of(d + 2 * nnz + r0, nrow);
+                mbar_expect_tx(&s_bar[0], wr.bytes + 1024u + (KK == 4 ? 5u * 256u * 4u : 0u));
+                bulk_g2s(s_r, wr.a, wr.bytes, &s_bar[0]);
+                bulk_g2s(s_lut, p.dq_lut + (uint64_t)b * 256, 1024u, &s_bar[0]);
+                if constexpr (KK == 4) bulk_g2s(s_lut4, g_row_lut4, 5u * 256u * 4u, &s_bar[0]);
+            }
+            const int32_t st0 = *(const volatile int32_t*)(p.status + b);
+            const unsigned long long* cs = p.chunk_state + (uint64_t)b * p.nchunk_cap;
+            const unsigned long long mine = cs[chunk];
+            unsigned long long acc = 0;
+            for (uint32_t j0 = 0; j0 < chunk; j0 += 128) {  // four loads in flight per lane
+                unsigned long long v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t j = j0 + 32 * k + lane;
+                    v[k] = j < chunk ? cs[j] : 0ull;
+                }
+                acc += (v[0] + v[1]) + (v[2] + v[3]);
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) {
+                const uint32_t cb = (uint32_t)min(acc, 0xFFFFFFFFull);
+                const uint32_t ow = (uint32_t)min(mine, 0xFFFFFFFFull);
+                const bool ok = st0 == SCZ_OK && ow <= nrow * KK && (uint64_t)cb + ow <= nnz;
+                if (st0 == SCZ_OK && !ok) p.status[b] = SCZ_CORRUPT_STREAM;
+                if (ok) {
+                    const Win wc = window_of(d + nnz + cb, ow), wv = window_of(d + cb, ow);
+                    mbar_expect_tx(&s_bar[1], wc.bytes + wv.bytes);
+                    if (wc.bytes) bulk_g2s(s_c, wc.a, wc.bytes, &s_bar[1]);
+                    if (wv.bytes) bulk_g2s(s_v, wv.a, wv.bytes, &s_bar[1]);
+                }
+                s_cb[0] = cb;
+                s_cb[1] = ow;
+                s_cb[2] = ok;
+            }
+        }
+        __syncthreads();
+        if (!s_cb[2]) {  // uniform; no copy may land after the CTA is gone
+            if (threadIdx.x == 0) mbar_wait(&s_bar[0], 0);
             return;
         }
-    } else if (chunk_dead(p, b, chunk)) {
-        return;
-    }
-    const uint8_t* d = reinterpret_cast<const uint8_t*>(p.dsym) + (uint64_t)b * p.dsym_stride;
-    if constexpr (KK == 4)
-        for (uint32_t i = threadIdx.x; i < 5 * 256 / 4; i += SMALL8_THREADS)
-            cp_async16(reinterpret_cast<uint4*>(s_lut4) + i, reinterpret_cast<const uint4*>(g_row_lut4) + i);
-    const uint32_t rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);
-    if (threadIdx.x < 64)  // the tensor's dequantisation table (k_dec_prepare)
-        cp_async16(reinterpret_cast<uint4*>(s_lut) + threadIdx.x,
-                   reinterpret_cast<const uint4*>(p.dq_lut + (uint64_t)b * 256) + threadIdx.x);
-    cp_async_commit();
-    uint32_t csh = 0, vsh = 0;
-    if (SUMS) {  // in flight during the scan below
-        csh = stage_window(s_c, d + nnz + cbase, own);
-        vsh = stage_window(s_v, d + cbase, own);
-        cp_async_commit();
-        cp_async_wait<1>();
+        cbase = s_cb[0];
+        own = s_cb[1];
+        csh = window_of(d + nnz + cbase, own).sh;
+        vsh = window_of(d + cbase, own).sh;
+        mbar_wait(&s_bar[0], 0);
     } else {
+        if (chunk_dead(p, b, chunk)) return;
+        if constexpr (KK == 4)
+            for (uint32_t i = threadIdx.x; i < 5 * 256 / 4; i += SMALL8_THREADS)
+                cp_async16(reinterpret_cast<uint4*>(s_lut4) + i, reinterpret_cast<const uint4*>(g_row_lut4) + i);
+        rsh = stage_window(s_r, d + 2 * nnz + r0, nrow);
+        if (threadIdx.x < 64)  // the tensor's dequantisation table (k_dec_prepare)
+            cp_async16(reinterpret_cast<uint4*>(s_lut) + threadIdx.x,
+                       reinterpret_cast<const uint4*>(p.dq_lut + (uint64_t)b * 256) + threadIdx.x);
+        cp_async_commit();
         cp_async_wait<0>();
+        __syncthreads();
     }
-    __syncthreads();
     // thread t owns rows [8t, 8t + 8) of the chunk for the scan: their count
     // bytes as two words (bytes past nrow masked off), checked, summed and
     // prefix-summed four at a time (SWAR; counts <= K keep every byte sum
@@ -589,7 +627,9 @@ __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(Ro
         cbase = block_chunk_base(p, b, chunk, tot, nnz, r0 + nrow == N, &s_bad);
     }
     if (s_bad) {  // from here on tot <= nrow * KK and cbase + tot <= nnz
-        cp_async_wait<0>();  // no copy may land after the CTA is gone
+        // no copy may land after the CTA is gone
+        if (SUMS) mbar_wait(&s_bar[1], 0);
+        else cp_async_wait<0>();
         if (threadIdx.x == 0) p.status[b] = SCZ_CORRUPT_STREAM;
         return;
     }
@@ -608,8 +648,10 @@ __global__ void __launch_bounds__(SMALL8_THREADS, SUMS ? 6 : 1) k_rows_small8(Ro
         csh = stage_window(s_c, d + nnz + cbase, tot);
         vsh = stage_window(s_v, d + cbase, tot);
         cp_async_commit();
+        cp_async_wait<0>();
+    } else {
+        mbar_wait(&s_bar[1], 0);
     }
-    cp_async_wait<0>();
     __syncthreads();
     float* orow0 = p.out + out_off + r0 * KK;
     const bool vec_ok = VEC || (reinterpret_cast<uintptr_t>(orow0) & (KK * 4 - 1)) == 0;
