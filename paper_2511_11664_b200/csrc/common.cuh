@@ -289,6 +289,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
+// Copy len bytes staged in shared memory at s_stage + (dst & 15) -- the
+// staging offset makes shared and global addresses agree mod 16 -- to global
+// dst: the < 16-byte head and tail by threads 0-15 and 32-47, the aligned
+// middle with one bulk copy (TMA) issued by thread 0.  Every thread that
+// wrote the staging area runs fence_proxy_async_smem() before the barrier
+// that precedes this call; thread 0 runs bulk_store_wait() before the CTA
+// exits (the copy still reads shared memory).
+__device__ __forceinline__ uint32_t stage_shift(const void* dst) {
+    return (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 15);
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void block_copy_s2g_bulk(uint8_t* dst, const uint8_t* s_stage, uint32_t len) {
+    const uint32_t sh = stage_shift(dst);
+    const uint8_t* s = s_stage + sh;
+    uint32_t head = (16 - sh) & 15;
+    head = head < len ? head : len;
+    const uint32_t mid = (len - head) & ~15u, t0 = head + mid;
+    if (threadIdx.x < head) dst[threadIdx.x] = s[threadIdx.x];
+    if (threadIdx.x >= 32 && threadIdx.x - 32 < len - t0) dst[t0 + threadIdx.x - 32] = s[t0 + threadIdx.x - 32];
+    if (threadIdx.x == 0 && mid) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst + head),
+                     "r"(smem_u32(s + head)), "r"(mid)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+}
+__device__ __forceinline__ void bulk_store_wait() {
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
 // Programmatic dependent launch: pipeline kernels are launched with the
 // PDL attribute; each one waits here, before touching memory, until the
 // predecessor grid has completed and flushed, then at once allows its own

@@ -370,6 +370,9 @@ __device__ __forceinline__ void quantize_tile(const QuantParams& p, uint32_t til
     const bool fast = st.fast != 0;
     const int qmax = nbins - 1;
     uint8_t* v8 = p.v8 + (uint64_t)b * p.v8_stride;
+    // values are staged at s_v + (destination & 15) so the aligned middle of
+    // the copy-out is one bulk copy (block_copy_s2g_bulk)
+    const uint32_t vsh = stage_shift(v8 + base_rank);
 
     // Branch-free over all 32 elements of the thread: the fp32 estimate for
     // every element and a store predicated on its bitmap bit.  In the fast
@@ -382,7 +385,7 @@ __device__ __forceinline__ void quantize_tile(const QuantParams& p, uint32_t til
     // boundary with the exact fp64 sequence.  The histogram is taken from the
     // staged symbols.
     uint32_t slow = fast ? 0u : 0xFFu;  // bit it: redo group it (4 elements)
-    const uint32_t sv_base = (uint32_t)__cvta_generic_to_shared(s_v);
+    const uint32_t sv_base = (uint32_t)__cvta_generic_to_shared(s_v) + vsh;
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
         const float4 v = vv[it];
@@ -428,34 +431,41 @@ __device__ __forceinline__ void quantize_tile(const QuantParams& p, uint32_t til
             if (fast && fabsf(__fsub_rn(y, rq)) < 0.5f - QGUARD) continue;
             const int bit = 4 * (lane & 7) + j;
             const uint32_t q = quant_exact(x, scale, zf, (double)qmax);
-            if ((wbits >> bit) & 1u) s_v[s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
+            if ((wbits >> bit) & 1u) s_v[vsh + s_wpre[word] + __popc(wbits & ((1u << bit) - 1u))] = (uint8_t)q;
             if constexpr (SYM_OUT) p.sym_out[(uint64_t)b * p.total + tile_base + off] = q;
         }
     }
+    fence_proxy_async_smem();  // the staged values, for the bulk copy-out
     __syncthreads();
     // value histogram of the tile's symbols (per-warp copies): whole words
-    // of four symbols, then the < 4 tail symbols
+    // of four symbols, then the < 4 symbols before and after them
     {
         const uint32_t hb = (uint32_t)__cvta_generic_to_shared(&s_hist[warp][0]);
-        const uint32_t nfull = tot & ~3u;
-        for (uint32_t i = 4 * threadIdx.x; i < nfull; i += 4 * TILE_THREADS) {
-            const uint32_t w4 = lds_u32(sv_base + i);
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(s_v);
+        const uint32_t lo = vsh, hi = vsh + tot;
+        const uint32_t wlo = min((lo + 3u) & ~3u, hi), whi = max(hi & ~3u, wlo);
+        for (uint32_t i = wlo + 4 * threadIdx.x; i < whi; i += 4 * TILE_THREADS) {
+            const uint32_t w4 = lds_u32(sb + i);
             red_shared_inc(hb | ((w4 << 2) & 0x3FCu));
             red_shared_inc(hb | ((w4 >> 6) & 0x3FCu));
             red_shared_inc(hb | ((w4 >> 14) & 0x3FCu));
             red_shared_inc(hb | ((w4 >> 22) & 0x3FCu));
         }
-        if (threadIdx.x < tot - nfull) red_shared_inc(hb | (lds_u8(sv_base + nfull + threadIdx.x) << 2));
+        if (threadIdx.x < wlo - lo) red_shared_inc(hb | (lds_u8(sb + lo + threadIdx.x) << 2));
+        else if (threadIdx.x >= 32 && threadIdx.x - 32 < hi - whi)
+            red_shared_inc(hb | (lds_u8(sb + whi + threadIdx.x - 32) << 2));
     }
     __syncthreads();
-    // the tile's values go out with coalesced 16-byte stores
-    block_copy_s2g<TILE_THREADS>(v8 + base_rank, s_v, tot);
+    // the tile's values go out: head / tail bytes by threads, the aligned
+    // middle as one bulk copy
+    block_copy_s2g_bulk(v8 + base_rank, s_v, tot);
     uint32_t* gh = p.vhist + (uint64_t)b * 256;
     for (int i = threadIdx.x; i < nbins; i += TILE_THREADS) {
         const uint32_t t = (s_hist[0][i] + s_hist[1][i]) + (s_hist[2][i] + s_hist[3][i]) +
                            (s_hist[4][i] + s_hist[5][i]) + (s_hist[6][i] + s_hist[7][i]);
         if (t) atomicAdd(gh + i, t);
     }
+    if (threadIdx.x == 0) bulk_store_wait();  // the copy-out still reads s_v
 }
 
 
@@ -640,7 +650,7 @@ __device__ __forceinline__ void materialize_body(const MatParams& p, uint8_t* s_
     __shared__ uint32_t s_scan[33];
     __shared__ uint32_t s_w[TILE_WORDS + 2];  // this tile's bitmap + the next two words
     __shared__ uint8_t s_mod[64];             // i mod K for i < 64 (K <= 32)
-    S* s_c = reinterpret_cast<S*>(s_buf);     // column indices staged in rank order
+    S* s_c0 = reinterpret_cast<S*>(s_buf);    // column indices staged in rank order
     const uint64_t word = (uint64_t)tile * TILE_WORDS + threadIdx.x;
     uint32_t w = bm[word];
     s_w[threadIdx.x] = w;
@@ -652,6 +662,10 @@ __device__ __forceinline__ void materialize_body(const MatParams& p, uint8_t* s_
     uint32_t tot;
     uint32_t lrank = block_exclusive_scan<TILE_THREADS>(__popc(w), s_scan, &tot);  // syncs
     const uint32_t base_rank = p.tile_off[(uint64_t)b * p.n_tiles + tile];
+    // u8 columns are staged at s_buf + (destination & 15) so the aligned
+    // middle of the copy-out is one bulk copy (block_copy_s2g_bulk)
+    const bool bulk = sizeof(S) == 1 && K <= 32;
+    S* s_c = s_c0 + (bulk ? stage_shift(cr + base_rank) : 0u);
     // column index of every nonzero: p mod K (sparse.py:66-68)
     if (w) {
         // (32 * word) mod K without a 64-bit modulo: T < 2^31 so the fp64
@@ -713,10 +727,11 @@ __device__ __forceinline__ void materialize_body(const MatParams& p, uint8_t* s_
                 s_rc[j] = (uint8_t)__popc(__funnelshift_r(s_w[wi], s_w[wi + 1], sh) & kmask);
             }
         }
+        fence_proxy_async_smem();  // the column bytes, for the bulk copy
         __syncthreads();
-        block_copy_s2g<TILE_THREADS>(reinterpret_cast<uint8_t*>(cr + base_rank),
-                                     reinterpret_cast<const uint8_t*>(s_c), tot);
+        block_copy_s2g_bulk(reinterpret_cast<uint8_t*>(cr + base_rank), reinterpret_cast<const uint8_t*>(s_c0), tot);
         block_copy_s2g<TILE_THREADS>(reinterpret_cast<uint8_t*>(cr + nnz + i0), s_rc, nr);
+        if (threadIdx.x == 0) bulk_store_wait();
         return;
     }
     __syncthreads();

@@ -51,9 +51,7 @@ constexpr uint32_t V1_NQ = 1024 / V1_C;          // chunks in the queue
 constexpr uint32_t V1_G = 512 / V1_C;            // chunks per encoder feeder group (16 loads per lane)
 constexpr int V1_THREADS = 96;                   // chain, feeder, emitter warps
 
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
+// (fence_proxy_async_smem: common.cuh)
 // shared -> global bulk copy (TMA store), completion tracked by bulk groups
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(ssrc)),
