@@ -703,9 +703,17 @@ __device__ __forceinline__ void materialize_body(const MatParams& p, uint8_t* s_
     }
     // row counts for the rows starting in this tile (sparse.py:68)
     const uint64_t ts = (uint64_t)tile * TILE, te = min(ts + TILE, p.total);
-    // 32-bit quotients (T < 2^31, so ts + K - 1 < 2^32): a 64-bit division
-    // here was 11 % of the kernel's instructions
-    const uint64_t i0 = ((uint32_t)ts + K - 1) / K, i1 = ((uint32_t)te + K - 1) / K;
+    // 32-bit quotients (T < 2^31, so ts + K - 1 < 2^32; a 64-bit division
+    // here was 11 % of the kernel's instructions), shifts for K = 2^k
+    uint64_t i0, i1;
+    if ((K & (K - 1)) == 0) {
+        const uint32_t k = __ffs(K) - 1;
+        i0 = ((uint32_t)ts + K - 1) >> k;
+        i1 = ((uint32_t)te + K - 1) >> k;
+    } else {
+        i0 = ((uint32_t)ts + K - 1) / K;
+        i1 = ((uint32_t)te + K - 1) / K;
+    }
     if (sizeof(S) == 1 && K <= 32) {
         // u8: row counts staged too; c and r leave with 16-byte stores
         uint8_t* s_rc = s_buf + TILE + 32;  // (u8 columns use the first TILE + 32 bytes)
