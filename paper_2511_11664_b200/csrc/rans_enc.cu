@@ -380,16 +380,18 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
             if ((s & 15) == 0 && base < low) flush();
             --s;
         }
-        for (; s >= 0 && (s & 3) != 3; --s) {  // align the rest to groups of four steps
+        for (; s >= 0 && (s & 7) != 7; --s) {  // align the rest to groups of eight steps
             ensure(s);
             enc_step_lin<false>(x, base, lds_tab16(tab_s + 16 * lds_u8(sym_at(s))), gtm, true);
             if ((s & 15) == 0 && base < low) flush();
         }
-        // groups of four steps (never across a chunk or a flush boundary).
-        // Entry k of the next group loads right after step k of this one
-        // used its registers, four steps ahead of its use; the next group's
-        // symbols load at the start of this one.
-        if (s >= 3) {
+        // groups of eight steps (s = 7 mod 8: never across a 32-step symbol
+        // chunk; a flush boundary only at the end), four table entries in
+        // flight: entry k of the next half-group loads right after step k of
+        // this one used its registers, four steps ahead of its use.  The
+        // first half's successors (s - 4 .. s - 7) share the chunk of s, so
+        // only the second half checks for a chunk change.
+        if (s >= 7) {
             ensure(s);
             const uint32_t a = sym_at(s);
             uint32_t y0 = lds_u8(a), y1 = lds_u8(a - 32), y2 = lds_u8(a - 64), y3 = lds_u8(a - 96);
@@ -397,8 +399,23 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
             EncTab t2 = lds_tab16(tab_s + 16 * y2), t3 = lds_tab16(tab_s + 16 * y3);
 #pragma unroll 1
             for (;;) {
-                const int sn = s - 4;
-                const bool more = sn >= 3;
+                {
+                    const uint32_t ah = sym_at(s - 4);
+                    y0 = lds_u8(ah);
+                    y1 = lds_u8(ah - 32);
+                    y2 = lds_u8(ah - 64);
+                    y3 = lds_u8(ah - 96);
+                }
+                enc_step_lin<false>(x, base, t0, gtm, true);
+                t0 = lds_tab16(tab_s + 16 * y0);
+                enc_step_lin<false>(x, base, t1, gtm, true);
+                t1 = lds_tab16(tab_s + 16 * y1);
+                enc_step_lin<false>(x, base, t2, gtm, true);
+                t2 = lds_tab16(tab_s + 16 * y2);
+                enc_step_lin<false>(x, base, t3, gtm, true);
+                t3 = lds_tab16(tab_s + 16 * y3);
+                const int sn = s - 8;
+                const bool more = sn >= 7;
                 if (more) {
                     ensure(sn);
                     const uint32_t an = sym_at(sn);
@@ -417,7 +434,7 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
                 t2 = lds_tab16(tab_s + 16 * y2);
                 enc_step_lin<false>(x, base, t3, gtm, true);
                 t3 = lds_tab16(tab_s + 16 * y3);
-                if (((s - 3) & 15) == 0 && base < low) flush();
+                if (((s - 7) & 15) == 0 && base < low) flush();
                 s = sn;
                 if (!more) break;
             }
