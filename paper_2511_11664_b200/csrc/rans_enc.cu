@@ -380,32 +380,24 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
             if ((s & 15) == 0 && base < low) flush();
             --s;
         }
-        for (; s >= 0 && (s & 7) != 7; --s) {  // align the rest to groups of eight steps
+        for (; s >= 0 && (s & 15) != 15; --s) {  // align the rest to groups of sixteen steps
             ensure(s);
             enc_step_lin<false>(x, base, lds_tab16(tab_s + 16 * lds_u8(sym_at(s))), gtm, true);
             if ((s & 15) == 0 && base < low) flush();
         }
-        // groups of eight steps (s = 7 mod 8: never across a 32-step symbol
-        // chunk; a flush boundary only at the end), four table entries in
-        // flight: entry k of the next half-group loads right after step k of
+        // groups of sixteen steps (s = 15 mod 16: never across a 32-step
+        // symbol chunk; a flush boundary only at the end), four table entries
+        // in flight: entry k of the next quarter loads right after step k of
         // this one used its registers, four steps ahead of its use.  The
-        // first half's successors (s - 4 .. s - 7) share the chunk of s, so
-        // only the second half checks for a chunk change.
-        if (s >= 7) {
+        // successors of the first three quarters share the chunk of s, so
+        // only the last quarter checks for a chunk change.
+        if (s >= 15) {
             ensure(s);
             const uint32_t a = sym_at(s);
             uint32_t y0 = lds_u8(a), y1 = lds_u8(a - 32), y2 = lds_u8(a - 64), y3 = lds_u8(a - 96);
             EncTab t0 = lds_tab16(tab_s + 16 * y0), t1 = lds_tab16(tab_s + 16 * y1);
             EncTab t2 = lds_tab16(tab_s + 16 * y2), t3 = lds_tab16(tab_s + 16 * y3);
-#pragma unroll 1
-            for (;;) {
-                {
-                    const uint32_t ah = sym_at(s - 4);
-                    y0 = lds_u8(ah);
-                    y1 = lds_u8(ah - 32);
-                    y2 = lds_u8(ah - 64);
-                    y3 = lds_u8(ah - 96);
-                }
+            auto quarter = [&]() {
                 enc_step_lin<false>(x, base, t0, gtm, true);
                 t0 = lds_tab16(tab_s + 16 * y0);
                 enc_step_lin<false>(x, base, t1, gtm, true);
@@ -414,27 +406,31 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
                 t2 = lds_tab16(tab_s + 16 * y2);
                 enc_step_lin<false>(x, base, t3, gtm, true);
                 t3 = lds_tab16(tab_s + 16 * y3);
-                const int sn = s - 8;
-                const bool more = sn >= 7;
+            };
+            auto load_y = [&](uint32_t an) {
+                y0 = lds_u8(an);
+                y1 = lds_u8(an - 32);
+                y2 = lds_u8(an - 64);
+                y3 = lds_u8(an - 96);
+            };
+#pragma unroll 1
+            for (;;) {
+                load_y(sym_at(s - 4));
+                quarter();
+                load_y(sym_at(s - 8));
+                quarter();
+                load_y(sym_at(s - 12));
+                quarter();
+                const int sn = s - 16;
+                const bool more = sn >= 15;
                 if (more) {
                     ensure(sn);
-                    const uint32_t an = sym_at(sn);
-                    y0 = lds_u8(an);
-                    y1 = lds_u8(an - 32);
-                    y2 = lds_u8(an - 64);
-                    y3 = lds_u8(an - 96);
+                    load_y(sym_at(sn));
                 }
                 // unconditional: after the last group these reload entries
                 // of the last symbols (harmless, unused)
-                enc_step_lin<false>(x, base, t0, gtm, true);
-                t0 = lds_tab16(tab_s + 16 * y0);
-                enc_step_lin<false>(x, base, t1, gtm, true);
-                t1 = lds_tab16(tab_s + 16 * y1);
-                enc_step_lin<false>(x, base, t2, gtm, true);
-                t2 = lds_tab16(tab_s + 16 * y2);
-                enc_step_lin<false>(x, base, t3, gtm, true);
-                t3 = lds_tab16(tab_s + 16 * y3);
-                if (((s - 7) & 15) == 0 && base < low) flush();
+                quarter();
+                if (base < low) flush();  // s - 15 = 0 mod 16
                 s = sn;
                 if (!more) break;
             }
