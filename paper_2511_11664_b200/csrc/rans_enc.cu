@@ -380,7 +380,7 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
             if ((s & 15) == 0 && base < low) flush();
             --s;
         }
-        for (; s >= 0 && (s & 15) != 15; --s) {  // align the rest to groups of sixteen steps
+        for (; s >= 0 && (s & 31) != 31; --s) {  // align the rest to whole 32-step symbol chunks
             ensure(s);
             enc_step_lin<false>(x, base, lds_tab16(tab_s + 16 * lds_u8(sym_at(s))), gtm, true);
             if ((s & 15) == 0 && base < low) flush();
@@ -391,7 +391,7 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
         // this one used its registers, four steps ahead of its use.  The
         // successors of the first three quarters share the chunk of s, so
         // only the last quarter checks for a chunk change.
-        if (s >= 15) {
+        if (s >= 31) {
             ensure(s);
             const uint32_t a = sym_at(s);
             uint32_t y0 = lds_u8(a), y1 = lds_u8(a - 32), y2 = lds_u8(a - 64), y3 = lds_u8(a - 96);
@@ -421,8 +421,17 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
                 quarter();
                 load_y(sym_at(s - 12));
                 quarter();
-                const int sn = s - 16;
-                const bool more = sn >= 15;
+                load_y(sym_at(s - 16));
+                quarter();
+                if (base < low) flush();  // s - 15 = 0 mod 16
+                load_y(sym_at(s - 20));
+                quarter();
+                load_y(sym_at(s - 24));
+                quarter();
+                load_y(sym_at(s - 28));
+                quarter();
+                const int sn = s - 32;
+                const bool more = sn >= 31;
                 if (more) {
                     ensure(sn);
                     load_y(sym_at(sn));
@@ -430,7 +439,7 @@ __device__ __forceinline__ void enc_v2_ring(EncLane& E, const uint8_t* gsym, uin
                 // unconditional: after the last group these reload entries
                 // of the last symbols (harmless, unused)
                 quarter();
-                if (base < low) flush();  // s - 15 = 0 mod 16
+                if (base < low) flush();  // s - 31 = 0 mod 32
                 s = sn;
                 if (!more) break;
             }
